@@ -1,0 +1,481 @@
+"""ORACLE (test infrastructure only) — plain fp64 NumPy t-FDP force step.
+
+Written from the paper, arXiv 2303.03964 (/root/reference/PAPER.md = P:<line>), with
+SPEC.md (S:<line>) for interfaces and worked examples, and the readings R1..R19 of
+DESIGN.md where the paper is silent/ambiguous.  Nothing here is blocked, fused or
+reordered beyond what the definitions state.  Imported only by tests/, smoke() and
+bench.py's CPU-baseline legs; never by the product path.
+
+Notation:  r_ij = x_i - x_j,  s_ij = 1 + |r_ij|^2,
+    R_i = rho * sum_{j != i} r_ij s_ij^-gamma                      (P:463-465 Eq. repfK)
+    A_i = -alpha * sum_{j in adj(i)} (1 + beta / s_ij) r_ij         (P:286-288 Eq. newforce, x alpha P:299-303)
+    D_i = R_i + A_i          (physical displacement, reading R1)
+    x_i <- x_i + eta_t D_i,  eta_t = eta0 (1 - t/T)                 (reading R2)
+"""
+from __future__ import annotations
+
+import dataclasses
+import math
+
+import numpy as np
+
+__all__ = [
+    "Params", "csr_build", "shard_range", "t_force", "repulsion_exact",
+    "repulsion_exact_loops", "attraction", "attraction_loops", "forces_exact",
+    "energy", "eta", "k_schedule", "Box", "box_rule", "interval_coords",
+    "lagrange_weights", "spread", "kernel_tdist", "convolve_direct", "convolve_fft",
+    "gather", "repulsion_ibfft", "forces", "step", "run", "np1", "rel_l2",
+    "equilibrium_distance",
+]
+
+
+@dataclasses.dataclass
+class Params:
+    """Force weights; defaults alpha=0.1, beta=8, gamma=2, rho=1."""
+    alpha: float = 0.1
+    beta: float = 8.0
+    gamma: float = 2.0
+    rho: float = 1.0
+
+
+# ---------------------------------------------------------------------------------------
+# Graph substrate: CSR + shard ranges (S:22-27 invariants; SURVEY §8(b) sharding rule)
+# ---------------------------------------------------------------------------------------
+def csr_build(n: int, u, v):
+    """Undirected simple graph -> symmetric CSR: self-loops dropped, duplicate
+    unordered pairs collapsed, each row's columns sorted ascending.
+    Returns (row_ptr int64[n+1], col int32[2m])."""
+    u = np.asarray(u, dtype=np.int64)
+    v = np.asarray(v, dtype=np.int64)
+    if u.shape != v.shape:
+        raise ValueError("u and v must have equal length")
+    if u.size and (u.min() < 0 or v.min() < 0 or u.max() >= n or v.max() >= n):
+        raise ValueError("edge endpoint out of range")
+    keep = u != v
+    a = np.minimum(u[keep], v[keep])
+    b = np.maximum(u[keep], v[keep])
+    pairs = np.unique(a * n + b)  # each unordered pair once
+    a, b = pairs // n, pairs % n
+    src = np.concatenate([a, b])
+    dst = np.concatenate([b, a])
+    order = np.lexsort((dst, src))  # by row, then column
+    src, dst = src[order], dst[order]
+    row_ptr = np.zeros(n + 1, dtype=np.int64)
+    np.add.at(row_ptr, src + 1, 1)
+    row_ptr = np.cumsum(row_ptr)
+    return row_ptr, dst.astype(np.int32)
+
+
+def shard_range(n: int, world: int, rank: int):
+    """Rank r of p owns targets [floor(r n / p), floor((r+1) n / p))."""
+    return (rank * n) // world, ((rank + 1) * n) // world
+
+
+# ---------------------------------------------------------------------------------------
+# Force model
+# ---------------------------------------------------------------------------------------
+def t_force(d, phi):
+    """t-force f(d) = d / (1 + d^2)^phi (P:268 Eq. forcefunction)."""
+    d = np.asarray(d, dtype=np.float64)
+    return d / (1.0 + d * d) ** phi
+
+
+def rel_l2(a, b) -> float:
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    nb = np.linalg.norm(b)
+    return float(np.linalg.norm(a - b) / nb) if nb > 0 else float(np.linalg.norm(a - b))
+
+
+def repulsion_exact(X, gamma=2.0, rho=1.0, targets=None, block_elems=1 << 22):
+    """Exact O(n^2) repulsion (P:463-465 Eq. repfK):
+    R_i = rho * sum_j (x_i - x_j) (1 + |x_i - x_j|^2)^-gamma.  The j = i term is 0
+    (r_ii = 0), so summing over all j equals the paper's j != i sum.
+    `targets` (optional int array) restricts the output rows; sources are always all n."""
+    X = np.asarray(X, dtype=np.float64)
+    n = X.shape[0]
+    tgt = np.arange(n) if targets is None else np.asarray(targets, dtype=np.int64)
+    out = np.zeros((tgt.size, 2))
+    bs = max(1, block_elems // max(n, 1))
+    for s in range(0, tgt.size, bs):
+        ti = tgt[s:s + bs]
+        r = X[ti, None, :] - X[None, :, :]  # (B, n, 2)
+        sij = 1.0 + (r * r).sum(-1)
+        out[s:s + bs] = rho * (r * (sij ** (-gamma))[..., None]).sum(1)
+    return out
+
+
+def repulsion_exact_loops(X, gamma=2.0, rho=1.0):
+    """Literal double loop of Eq. repfK with the j != i restriction (brute force, n <= 64)."""
+    X = [tuple(map(float, p)) for p in np.asarray(X, dtype=np.float64)]
+    n = len(X)
+    out = np.zeros((n, 2))
+    for i in range(n):
+        fx = fy = 0.0
+        for j in range(n):
+            if j == i:
+                continue
+            dx, dy = X[i][0] - X[j][0], X[i][1] - X[j][1]
+            d = math.sqrt(dx * dx + dy * dy)
+            if d == 0.0:
+                continue  # vector form r s^-gamma is 0 at d = 0 (reading R12)
+            mag = d / (1.0 + d * d) ** gamma  # t-force magnitude
+            fx += mag * dx / d
+            fy += mag * dy / d
+        out[i] = (rho * fx, rho * fy)
+    return out
+
+
+def attraction(X, row_ptr, col, alpha=0.1, beta=8.0, targets=None):
+    """A_i = -alpha * sum_{j in adj(i)} (1 + beta/(1 + d^2)) (x_i - x_j)
+    (P:286-288 Eq. newforce with phi=1 t-force term (reading R17), x alpha P:301-303)."""
+    X = np.asarray(X, dtype=np.float64)
+    row_ptr = np.asarray(row_ptr, dtype=np.int64)
+    col = np.asarray(col, dtype=np.int64)
+    n = X.shape[0]
+    tgt = np.arange(n) if targets is None else np.asarray(targets, dtype=np.int64)
+    deg = row_ptr[1:] - row_ptr[:-1]
+    rows = np.repeat(np.arange(n), deg)
+    r = X[rows] - X[col]
+    s = 1.0 + (r * r).sum(1)
+    contrib = -alpha * (1.0 + beta / s)[:, None] * r
+    out = np.zeros((n, 2))
+    np.add.at(out, rows, contrib)
+    return out[tgt]
+
+
+def attraction_loops(X, row_ptr, col, alpha=0.1, beta=8.0):
+    """Literal per-edge loop of Eq. newforce (brute force for small graphs)."""
+    X = np.asarray(X, dtype=np.float64)
+    n = X.shape[0]
+    out = np.zeros((n, 2))
+    for i in range(n):
+        for e in range(int(row_ptr[i]), int(row_ptr[i + 1])):
+            j = int(col[e])
+            dx, dy = X[i, 0] - X[j, 0], X[i, 1] - X[j, 1]
+            d = math.sqrt(dx * dx + dy * dy)
+            if d == 0.0:
+                continue
+            mag = d + beta * d / (1.0 + d * d)
+            out[i, 0] -= alpha * mag * dx / d  # pulls x_i toward x_j (reading R1)
+            out[i, 1] -= alpha * mag * dy / d
+    return out
+
+
+def forces_exact(X, row_ptr, col, p: Params = Params(), targets=None):
+    """(R, A) for the exact path (SURVEY §8(c) definition)."""
+    R = repulsion_exact(X, p.gamma, p.rho, targets)
+    A = attraction(X, row_ptr, col, p.alpha, p.beta, targets)
+    return R, A
+
+
+def energy(X, row_ptr, col, p: Params = Params()):
+    """E with D = -grad E (pin P9): rho sum_{i<j} s^(1-gamma)/(2(gamma-1))
+    + alpha sum_edges (d^2/2 + (beta/2) ln s)  (potentials of S:214-219; gamma > 1)."""
+    X = np.asarray(X, dtype=np.float64)
+    n = X.shape[0]
+    r = X[:, None, :] - X[None, :, :]
+    s = 1.0 + (r * r).sum(-1)
+    iu = np.triu_indices(n, 1)
+    e_rep = p.rho * (s[iu] ** (1.0 - p.gamma)).sum() / (2.0 * (p.gamma - 1.0))
+    deg = np.diff(row_ptr)
+    rows = np.repeat(np.arange(n), deg)
+    cols = np.asarray(col, dtype=np.int64)
+    up = rows < cols  # each undirected edge once
+    d2 = ((X[rows[up]] - X[cols[up]]) ** 2).sum(1)
+    e_att = p.alpha * (0.5 * d2 + 0.5 * p.beta * np.log1p(d2)).sum()
+    return e_rep + e_att
+
+
+def equilibrium_distance(p: Params = Params()):
+    """Two connected nodes: net force 0 where rho u^-gamma = alpha (1 + beta/u), u = 1 + d^2
+    (P:345-355 crossover; closed form for gamma = 2, rho = 1: alpha u^2 + alpha beta u - 1 = 0)."""
+    a, b = p.alpha, p.beta
+    if p.gamma == 2.0 and p.rho == 1.0:
+        u = (-a * b + math.sqrt(a * a * b * b + 4.0 * a)) / (2.0 * a)
+        return math.sqrt(u - 1.0)
+    lo, hi = 1e-9, 1e3  # bisection on net(d) = rep - att (repulsive for small d)
+    f = lambda d: p.rho * (1 + d * d) ** (-p.gamma) - a * (1 + b / (1 + d * d))
+    for _ in range(200):
+        mid = 0.5 * (lo + hi)
+        lo, hi = (mid, hi) if f(mid) > 0 else (lo, mid)
+    return 0.5 * (lo + hi)
+
+
+# ---------------------------------------------------------------------------------------
+# Schedules (reading R2/R4)
+# ---------------------------------------------------------------------------------------
+def eta(t: int, T: int, eta0: float = 0.1, cooling: str = "linear") -> float:
+    """Step size.  The paper never states its integrator ("the resultant force will
+    move the node until convergence").  Reading R2 (default): linear cooling
+    eta_t = eta0 (1 - t/T).  Reading R2' ("constant"): eta_t = eta0, which is what
+    the P:680 observation (NP1 recovers in the last 30 iterations) needs; see DESIGN.md."""
+    if cooling == "linear":
+        return eta0 * (1.0 - t / T)
+    if cooling == "constant":
+        return eta0
+    raise ValueError(cooling)
+
+
+def k_schedule(T: int) -> np.ndarray:
+    """Dynamic k: k=1 for ceil(0.9T) iterations, k=2 for ceil(0.05T), k=3 for the
+    rest; T < 20 -> k=3 throughout (reading R4)."""
+    if T < 1:
+        raise ValueError("T >= 1")
+    if T < 20:
+        return np.full(T, 3, dtype=np.int32)
+    n1 = math.ceil(0.9 * T - 1e-9)
+    n2 = math.ceil(0.05 * T - 1e-9)
+    n1 = min(n1, T)
+    n2 = min(n2, T - n1)
+    return np.array([1] * n1 + [2] * n2 + [3] * (T - n1 - n2), dtype=np.int32)
+
+
+# ---------------------------------------------------------------------------------------
+# ibFFT — step by step
+# ---------------------------------------------------------------------------------------
+@dataclasses.dataclass
+class Box:
+    lo: np.ndarray  # float32[2]  lower-left corner of the bounding square (R6)
+    L: np.float32  # side of the square (R6)
+    n_int: int  # intervals per axis (R5)
+    w: np.float32  # interval width L / n_int
+    center: np.ndarray  # float64[2] = lo + L/2 (R11)
+
+
+def box_rule(X, n_int_min: int = 50, n_int_fixed: int = 0) -> Box:
+    """Bounding square + interval rule.  P:531 divides "[x_min,x_max] x [x_min,x_max]" into
+    N_int x N_int intervals; P:540 N_int = max(50, [y_max - y_min]).  Readings: R6 square
+    anchored at (min x, min y) with side L = max(span_x, span_y); R5 bracket = ceil.
+    R19: lo, L, w are computed in fp32 (the kernel's precision) because they decide the
+    integer interval index; degenerate L = 0 -> unit square centred on the point."""
+    X32 = np.asarray(X, dtype=np.float32)
+    mn = X32.min(0)
+    mx = X32.max(0)
+    span = (mx - mn).astype(np.float32)  # fp32 subtraction
+    L = np.float32(max(span[0], span[1]))
+    lo = mn.astype(np.float32)
+    if L == np.float32(0.0):
+        lo = (mn - np.float32(0.5)).astype(np.float32)
+        L = np.float32(1.0)
+    n_int = int(n_int_fixed) if n_int_fixed > 0 else max(int(n_int_min), int(math.ceil(float(L))))
+    w = np.float32(L / np.float32(n_int))  # IEEE fp32 division
+    center = lo.astype(np.float64) + 0.5 * np.float64(L)
+    return Box(lo=lo, L=L, n_int=n_int, w=w, center=center)
+
+
+def interval_coords(X, box: Box):
+    """Interval index b = min(floor((x - lo)/w), N_int - 1) (top edge -> last interval, R7)
+    and local coordinate u = (x - lo)/w - b in [0, 1].  (x - lo)/w is evaluated in fp32
+    (R19) so the integer decision matches the device bit for bit; u is then exact."""
+    X32 = np.asarray(X, dtype=np.float32)
+    t32 = ((X32 - box.lo) / box.w).astype(np.float32)
+    b = np.minimum(np.floor(t32).astype(np.int64), box.n_int - 1)
+    b = np.maximum(b, 0)
+    u = t32.astype(np.float64) - b
+    return b, u
+
+
+def lagrange_weights(u, k: int):
+    """Lagrange basis on k equispaced nodes t_c = (c + 1/2)/k of the unit interval
+    ("k x k equi-spaced nodes"; node placement reading R8):
+    l_c(u) = prod_{c' != c} (u - t_c') / (t_c - t_c').  Returns array (..., k)."""
+    u = np.asarray(u, dtype=np.float64)
+    t = (np.arange(k) + 0.5) / k
+    out = np.ones(u.shape + (k,))
+    for c in range(k):
+        for cp in range(k):
+            if cp != c:
+                out[..., c] *= (u - t[cp]) / (t[c] - t[cp])
+    return out
+
+
+def spread(X, box: Box, k: int):
+    """Step 1 ("projecting all data points onto the grid by using Lagrange
+    polynomials"): C_v[b_x k + a, b_y k + c] += l_a(u_x) l_c(u_y) v_i for v in
+    {1, x~, y~} (x~ = x - center, R11).  Each node touches only its own interval's k x k
+    nodes.  Returns C[3, M, M] indexed [channel, gx, gy], M = N_int k."""
+    X = np.asarray(X, dtype=np.float64)
+    n = X.shape[0]
+    M = box.n_int * k
+    b, u = interval_coords(X, box)
+    lx = lagrange_weights(u[:, 0], k)  # (n, k)
+    ly = lagrange_weights(u[:, 1], k)
+    xt = X - box.center
+    vals = np.stack([np.ones(n), xt[:, 0], xt[:, 1]], 0)  # (3, n)
+    C = np.zeros((3, M, M))
+    for a in range(k):
+        for c in range(k):
+            gx = b[:, 0] * k + a
+            gy = b[:, 1] * k + c
+            wgt = lx[:, a] * ly[:, c]
+            for ch in range(3):
+                np.add.at(C[ch], (gx, gy), wgt * vals[ch])
+    return C
+
+
+def kernel_tdist(gamma: float):
+    """K(x_i, x_j) = 1 / (1 + |x_i - x_j|^2)^gamma as a function of (dx, dy)."""
+    return lambda dx, dy: (1.0 + dx * dx + dy * dy) ** (-gamma)
+
+
+def convolve_direct(C, h: float, kernel):
+    """Step 2 by definition ("computing the interaction of the grid nodes"):
+    Phi_v[a, b] = sum_{a', b'} K(h (a - a'), h (b - b')) C_v[a', b']  (linear, R9).
+    Dense M^2 x M^2 matrix — small M only."""
+    M = C.shape[1]
+    if M > 64:
+        raise ValueError("direct convolution is for M <= 64")
+    a = np.arange(M)
+    gx, gy = np.meshgrid(a, a, indexing="ij")
+    gx, gy = gx.ravel(), gy.ravel()
+    Kmat = kernel(h * (gx[:, None] - gx[None, :]), h * (gy[:, None] - gy[None, :]))
+    return np.stack([(Kmat @ C[ch].ravel()).reshape(M, M) for ch in range(C.shape[0])])
+
+
+def convolve_fft(C, h: float, kernel, P: int | None = None):
+    """Step 2 "accelerated by FFT": the same linear convolution via a
+    zero-padded P x P circular convolution, P >= 2M - 1 (R9), numpy.fft in fp64."""
+    M = C.shape[1]
+    if P is None:
+        P = 2 * M
+    if P < 2 * M - 1:
+        raise ValueError("P must be >= 2M-1 for a linear convolution")
+    off = np.arange(-(M - 1), M)
+    dx, dy = np.meshgrid(off, off, indexing="ij")
+    Kp = np.zeros((P, P))
+    Kp[dx % P, dy % P] = kernel(h * dx, h * dy)
+    Khat = np.fft.rfft2(Kp)
+    out = np.empty_like(C)
+    for ch in range(C.shape[0]):
+        Cp = np.zeros((P, P))
+        Cp[:M, :M] = C[ch]
+        out[ch] = np.fft.irfft2(np.fft.rfft2(Cp) * Khat, s=(P, P))[:M, :M]
+    return out
+
+
+def gather(Phi, X, box: Box, k: int):
+    """Step 3 ("back-projecting the interaction of all grid nodes to the original
+    points"): psi_v(x_i) = sum_{a,c} l_a(u_x) l_c(u_y) Phi_v[b_x k + a, b_y k + c]."""
+    b, u = interval_coords(X, box)
+    lx = lagrange_weights(u[:, 0], k)
+    ly = lagrange_weights(u[:, 1], k)
+    psi = np.zeros((Phi.shape[0], b.shape[0]))
+    for a in range(k):
+        for c in range(k):
+            wgt = lx[:, a] * ly[:, c]
+            psi += wgt[None, :] * Phi[:, b[:, 0] * k + a, b[:, 1] * k + c]
+    return psi
+
+
+def repulsion_ibfft(X, k: int, gamma: float = 2.0, rho: float = 1.0, n_int_min: int = 50,
+                    n_int_fixed: int = 0, P: int | None = None, backend: str = "fft",
+                    kernel=None, return_info: bool = False):
+    """ibFFT repulsion.  F^r(i) = x_i psi_1(i) - psi_x(i)
+    (P:465 Eq. repfK, P:474-475 Eqs. Fr1/Fr2) with the three kernel sums of Eq.
+    kernelproduct approximated by spread -> grid convolution -> gather.
+    The j = i term is kept in psi and cancels exactly (R10).  Coordinates are
+    box-centred (R11; exact by translation invariance)."""
+    if k not in (1, 2, 3):
+        raise ValueError("k in {1,2,3}")
+    X = np.asarray(X, dtype=np.float64)
+    box = box_rule(X, n_int_min, n_int_fixed)
+    M = box.n_int * k
+    h = float(box.w) / k
+    K = kernel_tdist(gamma) if kernel is None else kernel
+    C = spread(X, box, k)
+    Phi = convolve_direct(C, h, K) if backend == "direct" else convolve_fft(C, h, K, P)
+    psi = gather(Phi, X, box, k)
+    xt = X - box.center
+    R = rho * np.stack([xt[:, 0] * psi[0] - psi[1], xt[:, 1] * psi[0] - psi[2]], 1)
+    if return_info:
+        return R, dict(box=box, M=M, h=h, psi=psi, C=C, Phi=Phi)
+    return R
+
+
+# ---------------------------------------------------------------------------------------
+# Runner
+# ---------------------------------------------------------------------------------------
+def forces(X, row_ptr, col, p: Params = Params(), solver: str = "exact", k: int = 3,
+           n_int_min: int = 50, n_int_fixed: int = 0, P: int | None = None):
+    """(R, A) for either repulsion path."""
+    if solver == "exact":
+        R = repulsion_exact(X, p.gamma, p.rho)
+    elif solver == "ibfft":
+        R = repulsion_ibfft(X, k, p.gamma, p.rho, n_int_min, n_int_fixed, P)
+    else:
+        raise ValueError(solver)
+    return R, attraction(X, row_ptr, col, p.alpha, p.beta)
+
+
+def step(X, row_ptr, col, p: Params, eta_t: float, **kw):
+    """One Jacobi iteration x <- x + eta_t (R + A), all forces from the snapshot."""
+    R, A = forces(X, row_ptr, col, p, **kw)
+    return np.asarray(X, dtype=np.float64) + eta_t * (R + A)
+
+
+def run(X0, row_ptr, col, p: Params = Params(), T: int = 300, eta0: float = 0.1,
+        t0: int = 0, solver: str = "exact", k: int = 0, n_int_min: int = 50,
+        n_int_fixed: int = 0, P: int | None = None, t_end: int | None = None,
+        cooling: str = "linear"):
+    """Iterations t = t0 .. t_end-1 (default T-1) of the layout loop.
+    k = 0 -> dynamic 90/5/5 schedule; raises on a non-finite position with the
+    iteration and node."""
+    if T < 1 or eta0 <= 0:
+        raise ValueError("T >= 1 and eta0 > 0")
+    X = np.asarray(X0, dtype=np.float64).copy()
+    ks = k_schedule(T)
+    for t in range(t0, T if t_end is None else t_end):
+        kt = int(ks[t]) if k == 0 else k
+        X = step(X, row_ptr, col, p, eta(t, T, eta0, cooling), solver=solver, k=kt,
+                 n_int_min=n_int_min, n_int_fixed=n_int_fixed, P=P)
+        bad = ~np.isfinite(X).all(1)
+        if bad.any():
+            raise FloatingPointError(f"diverged at iter {t} node {int(np.argmax(bad))}")
+    return X
+
+
+# ---------------------------------------------------------------------------------------
+# Neighbourhood preservation NP1
+# ---------------------------------------------------------------------------------------
+def np1(X, row_ptr, col, brute_max: int = 4096):
+    """NP = (1/n) sum_i |N_G(i,1) ∩ N_L(x_i,k_i)| / |N_G(i,1) ∪ N_L(x_i,k_i)|, k_i = deg(i);
+    layout kNN excludes i; ties by lower index; k_i = 0 contributes 1."""
+    X = np.asarray(X, dtype=np.float64)
+    n = X.shape[0]
+    row_ptr = np.asarray(row_ptr, dtype=np.int64)
+    deg = np.diff(row_ptr)
+    total = 0.0
+    if n <= brute_max:
+        for i in range(n):
+            ki = int(deg[i])
+            if ki == 0:
+                total += 1.0
+                continue
+            d2 = ((X - X[i]) ** 2).sum(1)
+            d2[i] = np.inf
+            nn = np.argsort(d2, kind="stable")[:ki]  # stable: ties -> lower index
+            G = set(col[row_ptr[i]:row_ptr[i + 1]].tolist())
+            Lset = set(nn.tolist())
+            total += len(G & Lset) / len(G | Lset)
+        return total / n
+    from scipy.spatial import cKDTree  # library kNN primitive for large n (pinned vs brute force)
+
+    tree = cKDTree(X)
+    order = np.argsort(deg, kind="stable")
+    for kval in np.unique(deg):
+        idx = order[deg[order] == kval]
+        if kval == 0:
+            total += idx.size
+            continue
+        kq = int(min(n, kval + 1))
+        for s in range(0, idx.size, 65536):
+            ii = idx[s:s + 65536]
+            _, nb = tree.query(X[ii], k=kq)
+            nb = np.asarray(nb).reshape(ii.size, kq)
+            for r, i in enumerate(ii):
+                cand = [j for j in nb[r].tolist() if j != i][: int(kval)]
+                G = set(col[row_ptr[i]:row_ptr[i + 1]].tolist())
+                Lset = set(cand)
+                total += len(G & Lset) / len(G | Lset)
+    return total / n
