@@ -1,0 +1,180 @@
+/*
+ * tfdp.h — C ABI of libtfdp.so, the B200-native t-FDP force step.
+ *
+ * t-FDP: Zhong et al., "Force-directed graph layouts revisited: a new force based on the
+ * t-Distribution", arXiv 2303.03964.  Citations: P:n = /root/reference/PAPER.md line n,
+ * S:n = /root/reference/SPEC.md line n, R<k> = reading k of DESIGN.md (§Readings).
+ *
+ * What one iteration computes, for x_i in R^2:
+ *   R_i = rho * sum_j (x_i - x_j) (1 + |x_i - x_j|^2)^-gamma      repulsion
+ *         exact all-pairs (TFDP_EXACT) or interpolation+FFT (TFDP_IBFFT)
+ *   A_i = -alpha * sum_{j in adj(i)} (1 + beta / (1 + d_ij^2)) (x_i - x_j)
+ *   x_i <- x_i + eta_t (R_i + A_i)                                 P:412, S:352 (R1, R2)
+ *
+ * Conventions for every entry point:
+ *   - Positions and forces are float32, 2 per node, node-major (x0,y0,x1,y1,...).
+ *   - Returned status: TFDP_OK or an error code; nothing aborts or throws across the ABI.
+ *     The message of the last error is kept per context (tfdp_last_error).
+ *   - Pointers marked "host or device" are classified with cudaPointerGetAttributes; all
+ *     work is ordered on the context stream; calls that write HOST memory synchronize
+ *     that stream before returning, calls that write DEVICE memory do not.
+ *   - The context owns every device buffer it allocates; callers own their pointers.
+ *   - There is no CPU fallback: every force evaluation runs in sm_100a kernels.
+ */
+#ifndef TFDP_H_
+#define TFDP_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TFDP_VERSION_MAJOR 0
+#define TFDP_VERSION_MINOR 1
+
+typedef struct tfdp_ctx tfdp_ctx; /* opaque; owns all device memory and FFT plans */
+
+typedef enum {
+  TFDP_OK = 0,
+  TFDP_ERR_ARG = 1,         /* invalid argument (see each call)                          */
+  TFDP_ERR_CUDA = 2,        /* CUDA runtime / cuFFT failure                               */
+  TFDP_ERR_OOM = 3,         /* device allocation failed                                   */
+  TFDP_ERR_DIVERGED = 4,    /* non-finite position after a step; ctx -> errored   */
+  TFDP_ERR_STATE = 5,       /* ctx is errored, or iteration t >= T under linear cooling   */
+  TFDP_ERR_NCCL = 6,        /* NCCL failure (multi-GPU)                                   */
+  TFDP_ERR_UNSUPPORTED = 7  /* dim != 2, or a feature not built                           */
+} tfdp_status;
+
+enum { TFDP_EXACT = 0, TFDP_IBFFT = 1 };                 /* repulsion path (P:454 / P:488) */
+enum { TFDP_COOL_LINEAR = 0, TFDP_COOL_CONSTANT = 1 };    /* integrator readings R2 / R2'   */
+enum { TFDP_DIST_SPREAD_ALL = 0, TFDP_DIST_GRID_ALLREDUCE = 1 }; /* FFT path, p > 1 (§8(e)) */
+
+/* Warning bits (returned by tfdp_warnings; the call itself returns TFDP_OK). */
+enum {
+  TFDP_WARN_ALPHA_BETA = 1u,  /* alpha (1 + beta) >= 1 violates Eq. limitweight      */
+  TFDP_WARN_GAMMA = 2u,       /* gamma <= 1 violates Eq. exponentcondiction          */
+  TFDP_WARN_NINT_CAPPED = 4u  /* an FFT iteration ran with N_int below the rule (grid cap);
+                                 the next tfdp_step call re-plans a larger grid            */
+};
+
+typedef struct {
+  int32_t dim;         /* must be 2; else TFDP_ERR_UNSUPPORTED              */
+  double alpha;        /* attraction weight, default 0.1                           */
+  double beta;         /* short-range attraction weight, default 8                 */
+  double gamma;        /* repulsion exponent, default 2; integer 1..8 fast paths   */
+  double rho;          /* repulsion scale, default 1 (global refinement P:13-18)    */
+  int32_t solver;      /* TFDP_EXACT | TFDP_IBFFT                                          */
+  int32_t k;           /* interpolation nodes per interval: 1,2,3; 0 = dynamic 90/5/5 */
+  int32_t n_int_min;   /* 50                                                       */
+  int32_t n_int_fixed; /* 0 = rule N_int = max(n_int_min, ceil L) (R5); > 0 forces N_int  */
+  int32_t fft_size;    /* 0 = automatic P; > 0 forces P (must be >= 2 N_int k - 1, R9)     */
+  double step0;        /* eta_0, default 0.1                                       */
+  int32_t iterations;  /* T >= 1 (cooling + dynamic-k length), default 300 (R3)            */
+  int32_t t0;          /* first iteration index (resume), default 0                        */
+  int32_t cooling;     /* TFDP_COOL_LINEAR (eta_t = eta0 (1 - t/T), R2, default) |
+                          TFDP_COOL_CONSTANT (eta_t = eta0, R2')                           */
+  int32_t dist_mode;   /* TFDP_DIST_SPREAD_ALL (default) | TFDP_DIST_GRID_ALLREDUCE        */
+} tfdp_params;
+
+/* Multi-GPU description: one process per GPU.  nccl_uid = 128 bytes from
+ * tfdp_nccl_unique_id() on rank 0, broadcast by the caller (e.g. over torch.distributed).
+ * nccl_uid == NULL with world > 1 is a "virtual shard": no communicator, the context
+ * evaluates rank's shard [lo, hi) on one GPU (tfdp_forces only; tfdp_step returns
+ * TFDP_ERR_UNSUPPORTED) — used to test the shard rule and determinism on one device. */
+typedef struct {
+  int32_t rank, world, device;
+  const unsigned char* nccl_uid;
+} tfdp_dist;
+
+/* Fills *p with the defaults above.  TFDP_ERR_ARG if p == NULL. */
+tfdp_status tfdp_params_default(tfdp_params* p);
+
+/* Host-side symmetric CSR build of an undirected simple graph:
+ * self-loops dropped, duplicate unordered pairs collapsed, columns of each row sorted.
+ *   n        node count (>= 1);  m  number of input pairs (>= 0)
+ *   u, v     host int32[m] endpoints in [0, n)
+ *   row_ptr  host int64[n+1] out;  col  host int32[capacity 2m] out;  *nnz = row_ptr[n]
+ * TFDP_ERR_ARG on n < 1, m < 0, NULL pointers (when m > 0) or endpoints out of range.
+ * Deterministic; bit-identical to the oracle's csr_build. */
+tfdp_status tfdp_csr_build(int64_t n, int64_t m, const int32_t* u, const int32_t* v,
+                           int64_t* row_ptr, int32_t* col, int64_t* nnz);
+
+/* Shard rule: rank r of p owns targets [floor(r n / p), floor((r+1) n / p)).
+ * TFDP_ERR_ARG unless n >= 0, 0 <= rank < world. */
+tfdp_status tfdp_shard_range(int64_t n, int32_t world, int32_t rank, int64_t* lo, int64_t* hi);
+
+/* Creates a context on the current (or dist->device) GPU.
+ *   n        node count >= 1
+ *   row_ptr  host int64[n+1], col host int32[row_ptr[n]]: a symmetric CSR as produced by
+ *            tfdp_csr_build (validated in O(m log d): symmetric, sorted, no self-loop, no
+ *            duplicate, in range; else TFDP_ERR_ARG)
+ *   xy0      host or device float32[2n] starting layout (finite; else TFDP_ERR_ARG)
+ *   p        parameters (NULL = defaults).  TFDP_ERR_ARG if T < 1, eta0 <= 0, gamma <= 0,
+ *            rho <= 0, alpha < 0, beta < 0, any value non-finite, k not in 0..3,
+ *            solver/cooling/dist_mode unknown.  TFDP_ERR_UNSUPPORTED if dim != 2.
+ *            Parameter-validity violations only set warning bits.
+ *   dist     NULL = single GPU; else rank/world/device + NCCL unique id
+ *   stream   cudaStream_t to order all work on (NULL = the context creates its own)
+ * The context copies the CSR and xy0; the caller may free them on return. */
+tfdp_status tfdp_init(tfdp_ctx** ctx, int64_t n, const int64_t* row_ptr, const int32_t* col,
+                      const float* xy0, const tfdp_params* p, const tfdp_dist* dist,
+                      void* stream);
+
+/* Runs n_iters >= 0 iterations t = t_cur .. t_cur + n_iters - 1 of the layout loop:
+ * k_t and eta_t from the schedules (R2/R2'), repulsion + attraction from the
+ * snapshot (Jacobi), position update, and (p > 1) the position exchange.
+ * Reads one 8-byte divergence word back at the end (the only host sync).
+ * TFDP_ERR_DIVERGED with "diverged at iter t node i"; TFDP_ERR_STATE if the ctx
+ * is errored or, under linear cooling, t would reach T. */
+tfdp_status tfdp_step(tfdp_ctx* ctx, int32_t n_iters);
+
+/* Evaluates R (rep_xy) and A (att_xy) at the current layout for this rank's shard
+ * [lo, hi) without updating; rep_xy / att_xy are host or device float32[2 (hi - lo)]
+ * (either may be NULL).  The ibFFT path uses k = params.k, or the schedule's k at the
+ * current iteration when params.k == 0.  Parity entry point of the tests. */
+tfdp_status tfdp_forces(tfdp_ctx* ctx, float* rep_xy, float* att_xy);
+
+/* Copies the full current layout (all n nodes, every rank) to xy_out (host or device
+ * float32[2n]). */
+tfdp_status tfdp_layout(tfdp_ctx* ctx, float* xy_out);
+
+/* Replaces the full layout with xy (host or device float32[2n], finite).  With
+ * tfdp_set_iteration this is the resume path (checkpoint = tfdp_layout + iteration). */
+tfdp_status tfdp_set_layout(tfdp_ctx* ctx, const float* xy);
+tfdp_status tfdp_set_iteration(tfdp_ctx* ctx, int32_t t);
+int32_t tfdp_iteration(const tfdp_ctx* ctx);
+
+/* This rank's target shard. */
+tfdp_status tfdp_shard(const tfdp_ctx* ctx, int64_t* lo, int64_t* hi);
+
+/* Geometry of the most recent ibFFT evaluation (diagnostics; syncs the stream):
+ * box4 = {lo_x, lo_y, L, w} (fp32, R6/R19), *n_int, *k, *fft_size (any may be NULL). */
+tfdp_status tfdp_fft_geometry(tfdp_ctx* ctx, float* box4, int32_t* n_int, int32_t* k,
+                              int32_t* fft_size);
+
+/* Per-kernel device timing (CUDA events around every launch on the ctx stream).
+ * tfdp_profile(ctx, 1) resets and enables, 0 disables.  tfdp_profile_read fills up to
+ * cap entries: names (static strings), total milliseconds and launch counts; returns the
+ * number of kernel kinds (or -1 on error).  Syncs the stream. */
+tfdp_status tfdp_profile(tfdp_ctx* ctx, int32_t enable);
+int32_t tfdp_profile_read(tfdp_ctx* ctx, const char** names, double* ms, int64_t* launches,
+                          int32_t cap);
+
+/* Number of kernel launches this library has issued on the ctx (its own kernels, not
+ * cuFFT/NCCL).  For the bench's gpu_launches claim. */
+int64_t tfdp_launch_count(const tfdp_ctx* ctx);
+
+uint32_t tfdp_warnings(const tfdp_ctx* ctx);
+const char* tfdp_last_error(const tfdp_ctx* ctx); /* "" if none; never NULL            */
+const char* tfdp_status_string(tfdp_status s);
+void tfdp_destroy(tfdp_ctx* ctx);                 /* NULL is a no-op                   */
+
+/* NCCL bootstrap for multi-GPU: writes a 128-byte ncclUniqueId.  Resolves NCCL from the
+ * process (libnccl.so.2, e.g. the one torch loaded).  TFDP_ERR_NCCL if unavailable. */
+tfdp_status tfdp_nccl_unique_id(unsigned char* uid128);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TFDP_H_ */

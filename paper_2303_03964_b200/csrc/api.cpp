@@ -1,0 +1,994 @@
+// libtfdp host runtime: the C ABI of include/tfdp.h.
+//
+// Owns device memory, the per-iteration schedule (k_t, eta_t), the FFT plans, the NCCL
+// communicator and the CSR/shard indexing.  Every force evaluation is enqueued as sm_100a
+// kernels (kernels_exact.cu, kernels_fft.cu) or cuFFT on the context stream; there is no
+// host compute path.  Citations as in include/tfdp.h.
+#include <cuda_runtime.h>
+#include <cufft.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/tfdp.h"
+#include "nccl_shim.h"
+#include "tfdp_internal.h"
+
+using tfdp::BoxKeys;
+using tfdp::ForceArgs;
+using tfdp::GridGeom;
+
+namespace {
+
+enum Kind {
+  K_EXACT_PARTIAL = 0,
+  K_EXACT_FINISH,
+  K_BBOX,
+  K_SETUP,
+  K_ZERO,
+  K_SPREAD,
+  K_KGRID,
+  K_FFT_K,
+  K_FFT_FWD,
+  K_MULT,
+  K_FFT_INV,
+  K_GATHER_UPDATE,
+  K_COMM,
+  K_COUNT
+};
+const char* kKindNames[K_COUNT] = {"exact_partial", "exact_finish", "bbox",   "setup",
+                                   "zero_grid",     "spread",       "kgrid",  "cufft_r2c_kernel",
+                                   "cufft_r2c_grid", "mult",        "cufft_c2r", "gather_update",
+                                   "nccl"};
+const bool kOwnKernel[K_COUNT] = {true, true, true, true, true, true, true,
+                                  false, false, true, false, true, false};
+
+struct FftPlan {
+  int P = 0;
+  cufftHandle r2c3 = 0, r2c1 = 0, c2r3 = 0;
+};
+
+}  // namespace
+
+struct tfdp_ctx {
+  int64_t n = 0, lo = 0, hi = 0;
+  tfdp_params p{};
+  int rank = 0, world = 1, device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  float2* xy[2] = {nullptr, nullptr};
+  int cur = 0;
+  int64_t* row_ptr = nullptr;
+  int32_t* col = nullptr;
+  int64_t nnz = 0;
+  // exact path
+  double2* part = nullptr;
+  int n_chunks = 1;
+  int64_t chunk = 0;
+  // outputs of tfdp_forces
+  float2* rep = nullptr;
+  float2* att = nullptr;
+  // status words
+  unsigned long long* diverge = nullptr;
+  int* capped = nullptr;
+  unsigned long long* h_status = nullptr;  // pinned [2]
+  BoxKeys* keys = nullptr;
+  GridGeom* geom = nullptr;
+  bool box_valid = false;
+  // ibFFT
+  int nint_cap = 0;
+  int P_of_k[4] = {0, 0, 0, 0};
+  int cap_of_k[4] = {0, 0, 0, 0};
+  std::map<int, FftPlan> plans;
+  int64_t P_alloc = 0;
+  float* grid = nullptr;
+  float* phi = nullptr;
+  float* kreal = nullptr;
+  float2* khat = nullptr;
+  float2* chat = nullptr;
+  // schedule
+  int t = 0;
+  std::vector<int32_t> ksched;
+  ForceArgs fa{};
+  // state
+  uint32_t warnings = 0;
+  bool errored = false;
+  std::string err;
+  // NCCL
+  const tfdp::NcclApi* nccl = nullptr;
+  ncclComm_t comm = nullptr;
+  // profiling
+  bool prof = false;
+  struct Pend {
+    int kind;
+    cudaEvent_t a, b;
+  };
+  std::vector<Pend> pend;
+  std::vector<cudaEvent_t> ev_pool;
+  double prof_ms[K_COUNT] = {};
+  int64_t prof_n[K_COUNT] = {};
+  int64_t launches = 0;
+};
+
+namespace {
+
+thread_local std::string g_noctx_err;
+
+tfdp_status fail(tfdp_ctx* c, tfdp_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  else g_noctx_err = buf;
+  return s;
+}
+
+#define CUDA_TRY(c, call)                                                                  \
+  do {                                                                                     \
+    cudaError_t e_ = (call);                                                               \
+    if (e_ != cudaSuccess)                                                                 \
+      return fail(c, e_ == cudaErrorMemoryAllocation ? TFDP_ERR_OOM : TFDP_ERR_CUDA,       \
+                  "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__);    \
+  } while (0)
+
+#define CUFFT_TRY(c, call)                                                        \
+  do {                                                                            \
+    cufftResult r_ = (call);                                                      \
+    if (r_ != CUFFT_SUCCESS)                                                      \
+      return fail(c, r_ == CUFFT_ALLOC_FAILED ? TFDP_ERR_OOM : TFDP_ERR_CUDA,     \
+                  "%s: cufft error %d (%s:%d)", #call, (int)r_, __FILE__, __LINE__); \
+  } while (0)
+
+#define NCCL_TRY(c, call)                                                                  \
+  do {                                                                                     \
+    ncclResult_t r_ = (call);                                                              \
+    if (r_ != ncclSuccess)                                                                 \
+      return fail(c, TFDP_ERR_NCCL, "%s: %s", #call, (c)->nccl->GetErrorString(r_));      \
+  } while (0)
+
+#define TRY(x)                          \
+  do {                                  \
+    tfdp_status s_ = (x);               \
+    if (s_ != TFDP_OK) return s_;       \
+  } while (0)
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// ---------------------------------------------------------------- profiling
+cudaEvent_t ev_get(tfdp_ctx* c) {
+  if (!c->ev_pool.empty()) {
+    cudaEvent_t e = c->ev_pool.back();
+    c->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+struct Scope {
+  tfdp_ctx* c;
+  int kind;
+  cudaEvent_t a = nullptr;
+  Scope(tfdp_ctx* c_, int k) : c(c_), kind(k) {
+    if (c->prof) {
+      a = ev_get(c);
+      cudaEventRecord(a, c->stream);
+    }
+    if (kOwnKernel[k]) c->launches++;
+  }
+  ~Scope() {
+    if (c->prof) {
+      cudaEvent_t b = ev_get(c);
+      cudaEventRecord(b, c->stream);
+      c->pend.push_back({kind, a, b});
+    }
+  }
+};
+
+void prof_collect(tfdp_ctx* c) {
+  if (c->pend.empty()) return;
+  cudaStreamSynchronize(c->stream);
+  for (auto& q : c->pend) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, q.a, q.b);
+    c->prof_ms[q.kind] += ms;
+    c->prof_n[q.kind] += 1;
+    c->ev_pool.push_back(q.a);
+    c->ev_pool.push_back(q.b);
+  }
+  c->pend.clear();
+}
+
+// ---------------------------------------------------------------- helpers
+int nice_fft_size(int64_t target) {
+  // smallest even m >= target with only factors 2,3,5,7 (fast cuFFT radices)
+  for (int64_t m = std::max<int64_t>(target, 2);; ++m) {
+    if (m & 1) continue;
+    int64_t r = m;
+    for (int f : {2, 3, 5, 7})
+      while (r % f == 0) r /= f;
+    if (r == 1) return (int)m;
+  }
+}
+
+int gamma_int_of(double g) {
+  for (int q : {1, 2, 3, 4, 8})
+    if (g == (double)q) return q;
+  return 0;
+}
+
+std::vector<int32_t> k_schedule(int T) {
+  // P:545 / S:303 (reading R4): ceil(0.9T) x k1, ceil(0.05T) x k2, rest k3; T < 20 -> all 3
+  std::vector<int32_t> ks(T, 3);
+  if (T < 20) return ks;
+  int n1 = (int)std::ceil(0.9 * T - 1e-9);
+  int n2 = (int)std::ceil(0.05 * T - 1e-9);
+  n1 = std::min(n1, T);
+  n2 = std::min(n2, T - n1);
+  for (int i = 0; i < T; ++i) ks[i] = i < n1 ? 1 : (i < n1 + n2 ? 2 : 3);
+  return ks;
+}
+
+bool finite_d(double x) { return std::isfinite(x); }
+
+tfdp_status validate_params(const tfdp_params* p, uint32_t* warn, std::string* msg) {
+  char b[256];
+  if (p->dim != 2) {
+    *msg = "dim must be 2 (P:410)";
+    return TFDP_ERR_UNSUPPORTED;
+  }
+  if (!finite_d(p->alpha) || !finite_d(p->beta) || !finite_d(p->gamma) || !finite_d(p->rho) ||
+      !finite_d(p->step0)) {
+    *msg = "non-finite parameter";
+    return TFDP_ERR_ARG;
+  }
+  if (p->gamma <= 0 || p->rho <= 0 || p->alpha < 0 || p->beta < 0 || p->step0 <= 0 ||
+      p->iterations < 1 || p->t0 < 0) {
+    snprintf(b, sizeof b, "invalid parameter (need gamma>0, rho>0, alpha>=0, beta>=0, eta0>0, T>=1, t0>=0)");
+    *msg = b;
+    return TFDP_ERR_ARG;
+  }
+  if (p->solver != TFDP_EXACT && p->solver != TFDP_IBFFT) {
+    *msg = "unknown solver";
+    return TFDP_ERR_ARG;
+  }
+  if (p->k < 0 || p->k > 3) {
+    *msg = "k must be 0 (dynamic) or 1..3";
+    return TFDP_ERR_ARG;
+  }
+  if (p->cooling != TFDP_COOL_LINEAR && p->cooling != TFDP_COOL_CONSTANT) {
+    *msg = "unknown cooling";
+    return TFDP_ERR_ARG;
+  }
+  if (p->dist_mode != TFDP_DIST_SPREAD_ALL && p->dist_mode != TFDP_DIST_GRID_ALLREDUCE) {
+    *msg = "unknown dist_mode";
+    return TFDP_ERR_ARG;
+  }
+  if (p->n_int_min < 1 || p->n_int_fixed < 0 || p->fft_size < 0) {
+    *msg = "n_int_min >= 1, n_int_fixed >= 0, fft_size >= 0";
+    return TFDP_ERR_ARG;
+  }
+  uint32_t w = 0;
+  if (p->alpha * (1.0 + p->beta) >= 1.0) w |= TFDP_WARN_ALPHA_BETA;  // Eq. limitweight
+  if (p->gamma <= 1.0) w |= TFDP_WARN_GAMMA;                          // Eq. exponentcondiction
+  *warn = w;
+  return TFDP_OK;
+}
+
+// O(m log d) check of the CSR invariants.
+bool validate_csr(int64_t n, const int64_t* rp, const int32_t* col, std::string* msg) {
+  char b[256];
+  if (rp[0] != 0) {
+    *msg = "row_ptr[0] != 0";
+    return false;
+  }
+  for (int64_t i = 0; i < n; ++i) {
+    if (rp[i + 1] < rp[i]) {
+      snprintf(b, sizeof b, "row_ptr not monotone at %lld", (long long)i);
+      *msg = b;
+      return false;
+    }
+  }
+  bool ok = true;
+  int64_t bad = -1;
+#pragma omp parallel for schedule(dynamic, 4096) reduction(&& : ok)
+  for (int64_t i = 0; i < n; ++i) {
+    for (int64_t e = rp[i]; e < rp[i + 1]; ++e) {
+      const int64_t j = col[e];
+      bool good = j >= 0 && j < n && j != i && (e == rp[i] || col[e - 1] < col[e]);
+      if (good) {  // symmetric: i in row j
+        const int32_t* a = col + rp[j];
+        const int32_t* z = col + rp[j + 1];
+        good = std::binary_search(a, z, (int32_t)i);
+      }
+      if (!good) {
+        ok = false;
+#pragma omp critical
+        bad = i;
+      }
+    }
+  }
+  if (!ok) {
+    snprintf(b, sizeof b,
+             "CSR invalid at row %lld (need sorted, symmetric, no self-loop/duplicate, in range)",
+             (long long)bad);
+    *msg = b;
+  }
+  return ok;
+}
+
+void host_box(const float* xy, int64_t n, float* L) {
+  float mnx = INFINITY, mny = INFINITY, mxx = -INFINITY, mxy = -INFINITY;
+  for (int64_t i = 0; i < n; ++i) {
+    mnx = std::min(mnx, xy[2 * i]);
+    mxx = std::max(mxx, xy[2 * i]);
+    mny = std::min(mny, xy[2 * i + 1]);
+    mxy = std::max(mxy, xy[2 * i + 1]);
+  }
+  *L = std::max(mxx - mnx, mxy - mny);
+}
+
+// ---------------------------------------------------------------- FFT resources
+tfdp_status plan_for(tfdp_ctx* c, int P, FftPlan** out) {
+  auto it = c->plans.find(P);
+  if (it != c->plans.end()) {
+    *out = &it->second;
+    return TFDP_OK;
+  }
+  FftPlan fp;
+  fp.P = P;
+  int dims[2] = {P, P};
+  CUFFT_TRY(c, cufftPlanMany(&fp.r2c3, 2, dims, nullptr, 1, 0, nullptr, 1, 0, CUFFT_R2C, 3));
+  CUFFT_TRY(c, cufftPlanMany(&fp.r2c1, 2, dims, nullptr, 1, 0, nullptr, 1, 0, CUFFT_R2C, 1));
+  CUFFT_TRY(c, cufftPlanMany(&fp.c2r3, 2, dims, nullptr, 1, 0, nullptr, 1, 0, CUFFT_C2R, 3));
+  CUFFT_TRY(c, cufftSetStream(fp.r2c3, c->stream));
+  CUFFT_TRY(c, cufftSetStream(fp.r2c1, c->stream));
+  CUFFT_TRY(c, cufftSetStream(fp.c2r3, c->stream));
+  c->plans[P] = fp;
+  *out = &c->plans[P];
+  return TFDP_OK;
+}
+
+void free_fft_buffers(tfdp_ctx* c) {
+  cudaFree(c->grid);
+  cudaFree(c->phi);
+  cudaFree(c->kreal);
+  cudaFree(c->khat);
+  cudaFree(c->chat);
+  c->grid = c->phi = c->kreal = nullptr;
+  c->khat = c->chat = nullptr;
+  c->P_alloc = 0;
+}
+
+// Grid cap + FFT size per k from a box side L: N_int cap with
+// 25% headroom over the rule, P_k = smallest 2^a3^b5^c7^d >= 2 N_cap k - 1 (R9).
+tfdp_status configure_fft(tfdp_ctx* c, float L) {
+  const tfdp_params& p = c->p;
+  int cap;
+  if (p.n_int_fixed > 0) {
+    cap = p.n_int_fixed;
+  } else {
+    const double want = std::max<double>(p.n_int_min, std::ceil((double)L * 1.25) + 8.0);
+    cap = (int)std::min(want, 20000.0);
+  }
+  c->nint_cap = cap;
+  int64_t Pmax = 0;
+  for (int k = 1; k <= 3; ++k) {
+    int P;
+    if (p.fft_size > 0) {
+      P = p.fft_size;
+      const int capk = (P + 1) / (2 * k);
+      if (p.n_int_fixed > 0 && capk < cap) {
+        if (p.k == 0 || p.k == k)
+          return fail(c, TFDP_ERR_ARG, "fft_size %d < 2*N_int*k-1 = %d (k=%d)", P,
+                      2 * cap * k - 1, k);
+      }
+      c->cap_of_k[k] = std::min(cap, capk);
+    } else {
+      P = nice_fft_size(2LL * cap * k - 1);
+      c->cap_of_k[k] = cap;
+    }
+    c->P_of_k[k] = P;
+    if (p.k == 0 || p.k == k) Pmax = std::max<int64_t>(Pmax, P);
+  }
+  if (Pmax > c->P_alloc) {
+    free_fft_buffers(c);
+    const size_t pp = (size_t)Pmax * Pmax;
+    const size_t pc = (size_t)Pmax * (Pmax / 2 + 1);
+    CUDA_TRY(c, cudaMalloc(&c->grid, 3 * pp * sizeof(float)));
+    CUDA_TRY(c, cudaMalloc(&c->phi, 3 * pp * sizeof(float)));
+    CUDA_TRY(c, cudaMalloc(&c->kreal, pp * sizeof(float)));
+    CUDA_TRY(c, cudaMalloc(&c->khat, pc * sizeof(float2)));
+    CUDA_TRY(c, cudaMalloc(&c->chat, 3 * pc * sizeof(float2)));
+    c->P_alloc = Pmax;
+  }
+  return TFDP_OK;
+}
+
+// ---------------------------------------------------------------- exchange (p > 1)
+tfdp_status exchange_positions(tfdp_ctx* c, float2* xy) {
+  if (c->world == 1) return TFDP_OK;
+  if (!c->comm)
+    return fail(c, TFDP_ERR_UNSUPPORTED,
+                "virtual shard context (no NCCL id): only tfdp_forces is available");
+  Scope sc(c, K_COMM);
+  NCCL_TRY(c, c->nccl->GroupStart());
+  for (int r = 0; r < c->world; ++r) {
+    int64_t lo, hi;
+    tfdp_shard_range(c->n, c->world, r, &lo, &hi);
+    if (hi > lo)
+      NCCL_TRY(c, c->nccl->Broadcast(xy + lo, xy + lo, (size_t)(hi - lo) * 2, ncclFloat, r,
+                                     c->comm, c->stream));
+  }
+  NCCL_TRY(c, c->nccl->GroupEnd());
+  return TFDP_OK;
+}
+
+// ---------------------------------------------------------------- one evaluation
+// update = 1: x_{t+1} into xy[cur^1] (own shard), exchange; update = 0: forces to rep/att.
+tfdp_status evaluate(tfdp_ctx* c, int update, float eta, int k) {
+  const int64_t n_local = c->hi - c->lo;
+  float2* xy = c->xy[c->cur];
+  float2* xyn = c->xy[c->cur ^ 1];
+  if (c->p.solver == TFDP_EXACT) {
+    {
+      Scope sc(c, K_EXACT_PARTIAL);
+      tfdp::launch_exact_partial(xy, c->n, c->lo, n_local, c->chunk, c->n_chunks, c->fa, c->part,
+                                 c->stream);
+    }
+    {
+      Scope sc(c, K_EXACT_FINISH);
+      tfdp::launch_exact_finish(xy, xyn, c->lo, n_local, c->n_chunks, c->part, c->row_ptr,
+                                c->col, c->fa, eta, c->t, update, c->rep, c->att, c->diverge,
+                                c->stream);
+    }
+  } else {
+    const int P = c->P_of_k[k];
+    FftPlan* fp = nullptr;
+    TRY(plan_for(c, P, &fp));
+    if (!c->box_valid || c->world > 1) {
+      {
+        Scope sc(c, K_BBOX);
+        tfdp::launch_reset_keys(c->keys, c->stream);
+        tfdp::launch_bbox(xy, c->n, c->keys, c->stream);
+      }
+    }
+    {
+      Scope sc(c, K_SETUP);
+      tfdp::launch_setup(c->keys, c->geom, k, c->p.n_int_min, c->p.n_int_fixed, c->cap_of_k[k],
+                         P, c->capped, c->stream);
+    }
+    {
+      Scope sc(c, K_ZERO);
+      tfdp::launch_zero_grid(c->grid, P, std::min(c->cap_of_k[k] * k, P), c->stream);
+    }
+    const bool allreduce = c->world > 1 && c->p.dist_mode == TFDP_DIST_GRID_ALLREDUCE;
+    {
+      Scope sc(c, K_SPREAD);
+      if (allreduce)
+        tfdp::launch_spread(xy, c->lo, n_local, c->geom, k, c->grid, c->stream);
+      else
+        tfdp::launch_spread(xy, 0, c->n, c->geom, k, c->grid, c->stream);
+    }
+    if (allreduce) {
+      if (!c->comm)
+        return fail(c, TFDP_ERR_UNSUPPORTED, "grid all-reduce needs an NCCL communicator");
+      Scope sc(c, K_COMM);
+      NCCL_TRY(c, c->nccl->AllReduce(c->grid, c->grid, (size_t)3 * P * P, ncclFloat, ncclSum,
+                                     c->comm, c->stream));
+    }
+    {
+      Scope sc(c, K_KGRID);
+      tfdp::launch_kgrid(c->geom, P, c->fa, c->kreal, c->stream);
+    }
+    {
+      Scope sc(c, K_FFT_K);
+      CUFFT_TRY(c, cufftExecR2C(fp->r2c1, c->kreal, reinterpret_cast<cufftComplex*>(c->khat)));
+    }
+    {
+      Scope sc(c, K_FFT_FWD);
+      CUFFT_TRY(c, cufftExecR2C(fp->r2c3, c->grid, reinterpret_cast<cufftComplex*>(c->chat)));
+    }
+    {
+      Scope sc(c, K_MULT);
+      tfdp::launch_mult(c->chat, c->khat, P, c->stream);
+    }
+    {
+      Scope sc(c, K_FFT_INV);
+      CUFFT_TRY(c, cufftExecC2R(fp->c2r3, reinterpret_cast<cufftComplex*>(c->chat), c->phi));
+    }
+    {
+      Scope sc(c, K_GATHER_UPDATE);
+      BoxKeys* nk = (update && c->world == 1) ? c->keys : nullptr;
+      tfdp::launch_gather_update(xy, xyn, c->lo, n_local, c->geom, k, c->phi, c->row_ptr, c->col,
+                                 c->fa, eta, c->t, update, c->rep, c->att, c->diverge, nk,
+                                 c->stream);
+    }
+    c->box_valid = update && c->world == 1;
+  }
+  CUDA_TRY(c, cudaGetLastError());
+  if (update) {
+    TRY(exchange_positions(c, xyn));
+    c->cur ^= 1;
+  }
+  return TFDP_OK;
+}
+
+int k_at(const tfdp_ctx* c, int t) {
+  if (c->p.k != 0) return c->p.k;
+  const int T = c->p.iterations;
+  return c->ksched[std::min(std::max(t, 0), T - 1)];
+}
+
+// Reads the divergence word and the grid-cap flag (the only host sync of a step call).
+tfdp_status check_status(tfdp_ctx* c, bool* capped) {
+  CUDA_TRY(c, cudaMemcpyAsync(c->h_status, c->diverge, sizeof(unsigned long long),
+                              cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(c->h_status + 1, c->capped, sizeof(int), cudaMemcpyDeviceToHost,
+                              c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  const unsigned long long d = c->h_status[0];
+  *capped = (int)(c->h_status[1] & 0xffffffffu) != 0;
+  if (d != ~0ULL) {
+    c->errored = true;
+    return fail(c, TFDP_ERR_DIVERGED, "diverged at iter %u node %u", (unsigned)(d >> 32),
+                (unsigned)(d & 0xffffffffu));
+  }
+  return TFDP_OK;
+}
+
+tfdp_status replan_after_cap(tfdp_ctx* c) {
+  // The rule wanted more intervals than the grid holds: warn, re-size from the current box.
+  c->warnings |= TFDP_WARN_NINT_CAPPED;
+  CUDA_TRY(c, cudaMemsetAsync(c->capped, 0, sizeof(int), c->stream));
+  tfdp::launch_reset_keys(c->keys, c->stream);
+  tfdp::launch_bbox(c->xy[c->cur], c->n, c->keys, c->stream);
+  c->launches += 2;
+  BoxKeys hk;
+  CUDA_TRY(c, cudaMemcpyAsync(&hk, c->keys, sizeof hk, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  auto k2f = [](unsigned k) {
+    unsigned u = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
+    float f;
+    memcpy(&f, &u, 4);
+    return f;
+  };
+  const float L = std::max(k2f(hk.maxx) - k2f(hk.minx), k2f(hk.maxy) - k2f(hk.miny));
+  c->box_valid = true;
+  return configure_fft(c, L);
+}
+
+}  // namespace
+
+// =============================================================================== C ABI
+extern "C" {
+
+tfdp_status tfdp_params_default(tfdp_params* p) {
+  if (!p) return TFDP_ERR_ARG;
+  memset(p, 0, sizeof(*p));
+  p->dim = 2;
+  p->alpha = 0.1;
+  p->beta = 8.0;
+  p->gamma = 2.0;
+  p->rho = 1.0;
+  p->solver = TFDP_EXACT;
+  p->k = 0;
+  p->n_int_min = 50;
+  p->n_int_fixed = 0;
+  p->fft_size = 0;
+  p->step0 = 0.1;
+  p->iterations = 300;
+  p->t0 = 0;
+  p->cooling = TFDP_COOL_LINEAR;
+  p->dist_mode = TFDP_DIST_SPREAD_ALL;
+  return TFDP_OK;
+}
+
+tfdp_status tfdp_shard_range(int64_t n, int32_t world, int32_t rank, int64_t* lo, int64_t* hi) {
+  if (n < 0 || world < 1 || rank < 0 || rank >= world || !lo || !hi) return TFDP_ERR_ARG;
+  *lo = (int64_t)((__int128)rank * n / world);
+  *hi = (int64_t)((__int128)(rank + 1) * n / world);
+  return TFDP_OK;
+}
+
+tfdp_status tfdp_csr_build(int64_t n, int64_t m, const int32_t* u, const int32_t* v,
+                           int64_t* row_ptr, int32_t* col, int64_t* nnz) {
+  if (n < 1 || m < 0 || !row_ptr || !nnz || (m > 0 && (!u || !v || !col)))
+    return fail(nullptr, TFDP_ERR_ARG, "tfdp_csr_build: bad arguments");
+  for (int64_t e = 0; e < m; ++e)
+    if (u[e] < 0 || u[e] >= n || v[e] < 0 || v[e] >= n)
+      return fail(nullptr, TFDP_ERR_ARG, "tfdp_csr_build: endpoint out of range at pair %lld",
+                  (long long)e);
+  std::vector<int64_t> cnt(n + 1, 0);
+  for (int64_t e = 0; e < m; ++e)
+    if (u[e] != v[e]) {
+      cnt[u[e] + 1]++;
+      cnt[v[e] + 1]++;
+    }
+  for (int64_t i = 0; i < n; ++i) cnt[i + 1] += cnt[i];
+  std::vector<int32_t> tmp((size_t)cnt[n]);
+  {
+    std::vector<int64_t> pos(cnt.begin(), cnt.end() - 1);
+    for (int64_t e = 0; e < m; ++e)
+      if (u[e] != v[e]) {
+        tmp[pos[u[e]]++] = v[e];
+        tmp[pos[v[e]]++] = u[e];
+      }
+  }
+  std::vector<int64_t> len(n, 0);
+#pragma omp parallel for schedule(dynamic, 1024)
+  for (int64_t i = 0; i < n; ++i) {
+    int32_t* a = tmp.data() + cnt[i];
+    int32_t* z = tmp.data() + cnt[i + 1];
+    std::sort(a, z);
+    len[i] = std::unique(a, z) - a;  // duplicate unordered pairs collapse
+  }
+  row_ptr[0] = 0;
+  for (int64_t i = 0; i < n; ++i) row_ptr[i + 1] = row_ptr[i] + len[i];
+#pragma omp parallel for schedule(dynamic, 1024)
+  for (int64_t i = 0; i < n; ++i)
+    memcpy(col + row_ptr[i], tmp.data() + cnt[i], (size_t)len[i] * sizeof(int32_t));
+  *nnz = row_ptr[n];
+  return TFDP_OK;
+}
+
+tfdp_status tfdp_init(tfdp_ctx** out, int64_t n, const int64_t* row_ptr, const int32_t* col,
+                      const float* xy0, const tfdp_params* pin, const tfdp_dist* dist,
+                      void* stream) {
+  if (!out) return fail(nullptr, TFDP_ERR_ARG, "ctx out-pointer is NULL");
+  *out = nullptr;
+  if (n < 1 || n > (int64_t)INT32_MAX || !row_ptr || !xy0)
+    return fail(nullptr, TFDP_ERR_ARG, "need 1 <= n <= 2^31-1, row_ptr and xy0");
+  tfdp_params p;
+  if (pin) p = *pin;
+  else tfdp_params_default(&p);
+  uint32_t warn = 0;
+  std::string msg;
+  tfdp_status st = validate_params(&p, &warn, &msg);
+  if (st != TFDP_OK) return fail(nullptr, st, "%s", msg.c_str());
+  const int64_t nnz = row_ptr[n];
+  if (nnz > 0 && !col) return fail(nullptr, TFDP_ERR_ARG, "col is NULL");
+  if (!validate_csr(n, row_ptr, col, &msg)) return fail(nullptr, TFDP_ERR_ARG, "%s", msg.c_str());
+
+  tfdp_ctx* c = new tfdp_ctx();
+  c->n = n;
+  c->p = p;
+  c->warnings = warn;
+  c->nnz = nnz;
+  c->t = p.t0;
+  c->ksched = k_schedule(p.iterations);
+  c->fa.alpha = (float)p.alpha;
+  c->fa.beta = (float)p.beta;
+  c->fa.gamma = (float)p.gamma;
+  c->fa.rho = (float)p.rho;
+  c->fa.gamma_int = gamma_int_of(p.gamma);
+  if (dist) {
+    if (dist->world < 1 || dist->rank < 0 || dist->rank >= dist->world) {
+      delete c;
+      return fail(nullptr, TFDP_ERR_ARG, "bad dist rank/world");
+    }
+    c->rank = dist->rank;
+    c->world = dist->world;
+    c->device = dist->device;
+  } else {
+    cudaGetDevice(&c->device);
+  }
+  auto bail = [&](tfdp_status s) {
+    g_noctx_err = c->err;
+    tfdp_destroy(c);
+    return s;
+  };
+  if (cudaSetDevice(c->device) != cudaSuccess)
+    return bail(fail(c, TFDP_ERR_CUDA, "cudaSetDevice(%d) failed (no GPU?)", c->device));
+  tfdp_shard_range(n, c->world, c->rank, &c->lo, &c->hi);
+  if (stream) {
+    c->stream = (cudaStream_t)stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess)
+      return bail(fail(c, TFDP_ERR_CUDA, "cudaStreamCreate failed"));
+    c->own_stream = true;
+  }
+  const bool xy_dev = is_device_ptr(xy0);
+  float L0 = 1.f;
+  if (!xy_dev) {
+    for (int64_t i = 0; i < 2 * n; ++i)
+      if (!std::isfinite(xy0[i]))
+        return bail(fail(c, TFDP_ERR_ARG, "xy0 non-finite at node %lld", (long long)(i / 2)));
+    host_box(xy0, n, &L0);
+  }
+  const int64_t n_local = c->hi - c->lo;
+#define ALLOC(ptr, bytes)                                                           \
+  if (cudaMalloc((void**)&(ptr), (bytes)) != cudaSuccess) {                         \
+    cudaGetLastError();                                                             \
+    return bail(fail(c, TFDP_ERR_OOM, "cudaMalloc(%zu) failed", (size_t)(bytes)));  \
+  }
+  ALLOC(c->xy[0], n * sizeof(float2));
+  ALLOC(c->xy[1], n * sizeof(float2));
+  ALLOC(c->row_ptr, (n + 1) * sizeof(int64_t));
+  ALLOC(c->col, std::max<int64_t>(nnz, 1) * sizeof(int32_t));
+  ALLOC(c->rep, std::max<int64_t>(n_local, 1) * sizeof(float2));
+  ALLOC(c->att, std::max<int64_t>(n_local, 1) * sizeof(float2));
+  ALLOC(c->diverge, sizeof(unsigned long long));
+  ALLOC(c->capped, sizeof(int));
+  ALLOC(c->keys, sizeof(BoxKeys));
+  ALLOC(c->geom, sizeof(GridGeom));
+  if (cudaMallocHost((void**)&c->h_status, 2 * sizeof(unsigned long long)) != cudaSuccess)
+    return bail(fail(c, TFDP_ERR_OOM, "cudaMallocHost failed"));
+  if (p.solver == TFDP_EXACT) {
+    // source chunks depend on n only (bitwise-identical results for any shard count, R15)
+    int64_t ch = std::max<int64_t>(1024, (n + 31) / 32);
+    ch = (ch + tfdp::kExactTile - 1) / tfdp::kExactTile * tfdp::kExactTile;
+    c->chunk = ch;
+    c->n_chunks = (int)((n + ch - 1) / ch);
+    ALLOC(c->part, (size_t)c->n_chunks * std::max<int64_t>(n_local, 1) * sizeof(double2));
+  }
+#undef ALLOC
+  cudaStream_t s = c->stream;
+  if (cudaMemcpyAsync(c->xy[0], xy0, n * sizeof(float2),
+                      xy_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s) != cudaSuccess ||
+      cudaMemcpyAsync(c->row_ptr, row_ptr, (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s) !=
+          cudaSuccess ||
+      (nnz > 0 && cudaMemcpyAsync(c->col, col, nnz * sizeof(int32_t), cudaMemcpyHostToDevice, s) !=
+                      cudaSuccess) ||
+      cudaMemsetAsync(c->diverge, 0xff, sizeof(unsigned long long), s) != cudaSuccess ||
+      cudaMemsetAsync(c->capped, 0, sizeof(int), s) != cudaSuccess)
+    return bail(fail(c, TFDP_ERR_CUDA, "initial copies failed: %s", cudaGetErrorString(cudaGetLastError())));
+  if (p.solver == TFDP_IBFFT) {
+    if (xy_dev) {  // box of a device layout: one bbox pass
+      tfdp::launch_reset_keys(c->keys, s);
+      tfdp::launch_bbox(c->xy[0], n, c->keys, s);
+      BoxKeys hk;
+      cudaMemcpyAsync(&hk, c->keys, sizeof hk, cudaMemcpyDeviceToHost, s);
+      cudaStreamSynchronize(s);
+      auto k2f = [](unsigned k) {
+        unsigned u = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
+        float f;
+        memcpy(&f, &u, 4);
+        return f;
+      };
+      L0 = std::max(k2f(hk.maxx) - k2f(hk.minx), k2f(hk.maxy) - k2f(hk.miny));
+    }
+    st = configure_fft(c, L0);
+    if (st != TFDP_OK) return bail(st);
+  }
+  if (c->world > 1 && dist->nccl_uid) {
+    const char* e = nullptr;
+    c->nccl = tfdp::nccl_api(&e);
+    if (!c->nccl) return bail(fail(c, TFDP_ERR_NCCL, "%s", e));
+  }
+  if (c->world > 1 && dist->nccl_uid) {
+    ncclUniqueId uid;
+    memcpy(&uid, dist->nccl_uid, sizeof uid);
+    ncclResult_t r = c->nccl->CommInitRank(&c->comm, c->world, uid, c->rank);
+    if (r != ncclSuccess)
+      return bail(fail(c, TFDP_ERR_NCCL, "ncclCommInitRank: %s", c->nccl->GetErrorString(r)));
+  }
+  if (cudaStreamSynchronize(s) != cudaSuccess)
+    return bail(fail(c, TFDP_ERR_CUDA, "init sync: %s", cudaGetErrorString(cudaGetLastError())));
+  *out = c;
+  return TFDP_OK;
+}
+
+tfdp_status tfdp_step(tfdp_ctx* c, int32_t n_iters) {
+  if (!c) return fail(nullptr, TFDP_ERR_ARG, "ctx is NULL");
+  if (c->errored) return fail(c, TFDP_ERR_STATE, "context is errored: %s", c->err.c_str());
+  if (n_iters < 0) return fail(c, TFDP_ERR_ARG, "n_iters < 0");
+  cudaSetDevice(c->device);
+  const int T = c->p.iterations;
+  if (c->p.cooling == TFDP_COOL_LINEAR && c->t + n_iters > T)
+    return fail(c, TFDP_ERR_STATE, "iteration %d + %d exceeds T = %d under linear cooling",
+                c->t, n_iters, T);
+  int done = 0;
+  while (done < n_iters) {
+    const int block = std::min(n_iters - done, 32);  // host check every 32 iterations
+    for (int b = 0; b < block; ++b) {
+      const double eta = c->p.cooling == TFDP_COOL_LINEAR
+                             ? c->p.step0 * (1.0 - (double)c->t / T)  // R2
+                             : c->p.step0;                            // R2'
+      TRY(evaluate(c, 1, (float)eta, k_at(c, c->t)));
+      c->t++;
+    }
+    done += block;
+    bool capped = false;
+    TRY(check_status(c, &capped));
+    if (capped && c->p.solver == TFDP_IBFFT) TRY(replan_after_cap(c));
+  }
+  return TFDP_OK;
+}
+
+tfdp_status tfdp_forces(tfdp_ctx* c, float* rep_xy, float* att_xy) {
+  if (!c) return fail(nullptr, TFDP_ERR_ARG, "ctx is NULL");
+  if (c->errored) return fail(c, TFDP_ERR_STATE, "context is errored: %s", c->err.c_str());
+  cudaSetDevice(c->device);
+  TRY(evaluate(c, 0, 0.f, k_at(c, c->t)));
+  c->box_valid = false;  // setup consumed the box keys without an update
+  const int64_t n_local = c->hi - c->lo;
+  bool host_out = false;
+  if (rep_xy) {
+    const bool d = is_device_ptr(rep_xy);
+    host_out |= !d;
+    CUDA_TRY(c, cudaMemcpyAsync(rep_xy, c->rep, n_local * sizeof(float2),
+                                d ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->stream));
+  }
+  if (att_xy) {
+    const bool d = is_device_ptr(att_xy);
+    host_out |= !d;
+    CUDA_TRY(c, cudaMemcpyAsync(att_xy, c->att, n_local * sizeof(float2),
+                                d ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->stream));
+  }
+  bool capped = false;
+  TRY(check_status(c, &capped));
+  if (capped && c->p.solver == TFDP_IBFFT) {
+    TRY(replan_after_cap(c));
+    c->box_valid = false;
+  }
+  (void)host_out;
+  return TFDP_OK;
+}
+
+tfdp_status tfdp_layout(tfdp_ctx* c, float* xy_out) {
+  if (!c || !xy_out) return fail(c, TFDP_ERR_ARG, "NULL argument");
+  cudaSetDevice(c->device);
+  const bool d = is_device_ptr(xy_out);
+  CUDA_TRY(c, cudaMemcpyAsync(xy_out, c->xy[c->cur], c->n * sizeof(float2),
+                              d ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->stream));
+  if (!d) CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return TFDP_OK;
+}
+
+tfdp_status tfdp_set_layout(tfdp_ctx* c, const float* xy) {
+  if (!c || !xy) return fail(c, TFDP_ERR_ARG, "NULL argument");
+  cudaSetDevice(c->device);
+  const bool d = is_device_ptr(xy);
+  if (!d)
+    for (int64_t i = 0; i < 2 * c->n; ++i)
+      if (!std::isfinite(xy[i]))
+        return fail(c, TFDP_ERR_ARG, "layout non-finite at node %lld", (long long)(i / 2));
+  CUDA_TRY(c, cudaMemcpyAsync(c->xy[c->cur], xy, c->n * sizeof(float2),
+                              d ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->stream));
+  c->box_valid = false;
+  return TFDP_OK;
+}
+
+tfdp_status tfdp_set_iteration(tfdp_ctx* c, int32_t t) {
+  if (!c || t < 0) return fail(c, TFDP_ERR_ARG, "bad iteration");
+  c->t = t;
+  return TFDP_OK;
+}
+
+int32_t tfdp_iteration(const tfdp_ctx* c) { return c ? c->t : -1; }
+
+tfdp_status tfdp_shard(const tfdp_ctx* c, int64_t* lo, int64_t* hi) {
+  if (!c || !lo || !hi) return TFDP_ERR_ARG;
+  *lo = c->lo;
+  *hi = c->hi;
+  return TFDP_OK;
+}
+
+tfdp_status tfdp_fft_geometry(tfdp_ctx* c, float* box4, int32_t* n_int, int32_t* k,
+                              int32_t* fft_size) {
+  if (!c) return TFDP_ERR_ARG;
+  if (c->p.solver != TFDP_IBFFT) return fail(c, TFDP_ERR_STATE, "not an ibFFT context");
+  GridGeom g;
+  CUDA_TRY(c, cudaMemcpyAsync(&g, c->geom, sizeof g, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  if (box4) {
+    box4[0] = g.lo_x;
+    box4[1] = g.lo_y;
+    box4[2] = g.L;
+    box4[3] = g.w;
+  }
+  if (n_int) *n_int = g.n_int;
+  if (k) *k = g.k;
+  if (fft_size) *fft_size = g.P;
+  return TFDP_OK;
+}
+
+tfdp_status tfdp_profile(tfdp_ctx* c, int32_t enable) {
+  if (!c) return TFDP_ERR_ARG;
+  prof_collect(c);
+  for (int i = 0; i < K_COUNT; ++i) {
+    c->prof_ms[i] = 0;
+    c->prof_n[i] = 0;
+  }
+  c->prof = enable != 0;
+  return TFDP_OK;
+}
+
+int32_t tfdp_profile_read(tfdp_ctx* c, const char** names, double* ms, int64_t* launches,
+                          int32_t cap) {
+  if (!c) return -1;
+  prof_collect(c);
+  for (int i = 0; i < K_COUNT && i < cap; ++i) {
+    if (names) names[i] = kKindNames[i];
+    if (ms) ms[i] = c->prof_ms[i];
+    if (launches) launches[i] = c->prof_n[i];
+  }
+  return K_COUNT;
+}
+
+int64_t tfdp_launch_count(const tfdp_ctx* c) { return c ? c->launches : -1; }
+
+uint32_t tfdp_warnings(const tfdp_ctx* c) { return c ? c->warnings : 0u; }
+
+const char* tfdp_last_error(const tfdp_ctx* c) {
+  return c ? c->err.c_str() : g_noctx_err.c_str();
+}
+
+const char* tfdp_status_string(tfdp_status s) {
+  switch (s) {
+    case TFDP_OK: return "TFDP_OK";
+    case TFDP_ERR_ARG: return "TFDP_ERR_ARG";
+    case TFDP_ERR_CUDA: return "TFDP_ERR_CUDA";
+    case TFDP_ERR_OOM: return "TFDP_ERR_OOM";
+    case TFDP_ERR_DIVERGED: return "TFDP_ERR_DIVERGED";
+    case TFDP_ERR_STATE: return "TFDP_ERR_STATE";
+    case TFDP_ERR_NCCL: return "TFDP_ERR_NCCL";
+    case TFDP_ERR_UNSUPPORTED: return "TFDP_ERR_UNSUPPORTED";
+  }
+  return "TFDP_ERR_UNKNOWN";
+}
+
+void tfdp_destroy(tfdp_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (auto& q : c->pend) {
+    cudaEventDestroy(q.a);
+    cudaEventDestroy(q.b);
+  }
+  for (auto e : c->ev_pool) cudaEventDestroy(e);
+  for (auto& kv : c->plans) {
+    cufftDestroy(kv.second.r2c3);
+    cufftDestroy(kv.second.r2c1);
+    cufftDestroy(kv.second.c2r3);
+  }
+  free_fft_buffers(c);
+  cudaFree(c->xy[0]);
+  cudaFree(c->xy[1]);
+  cudaFree(c->row_ptr);
+  cudaFree(c->col);
+  cudaFree(c->part);
+  cudaFree(c->rep);
+  cudaFree(c->att);
+  cudaFree(c->diverge);
+  cudaFree(c->capped);
+  cudaFree(c->keys);
+  cudaFree(c->geom);
+  if (c->h_status) cudaFreeHost(c->h_status);
+  if (c->comm && c->nccl) c->nccl->CommDestroy(c->comm);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+tfdp_status tfdp_nccl_unique_id(unsigned char* uid128) {
+  if (!uid128) return TFDP_ERR_ARG;
+  const char* e = nullptr;
+  const tfdp::NcclApi* api = tfdp::nccl_api(&e);
+  if (!api) return fail(nullptr, TFDP_ERR_NCCL, "%s", e);
+  ncclUniqueId id;
+  ncclResult_t r = api->GetUniqueId(&id);
+  if (r != ncclSuccess) return fail(nullptr, TFDP_ERR_NCCL, "ncclGetUniqueId: %s", api->GetErrorString(r));
+  memcpy(uid128, &id, sizeof id);
+  return TFDP_OK;
+}
+
+}  // extern "C"

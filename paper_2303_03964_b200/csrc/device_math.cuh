@@ -1,0 +1,73 @@
+// Small device helpers shared by the sm_100a kernels (product path only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace tfdp {
+
+// MUFU.RCP: one SFU op, ~1 ulp.  s = 1 + d^2 >= 1 so no denormal inputs.
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float ex2_approx(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float lg2_approx(float x) {
+  float r;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// s^-gamma for s >= 1.  G = 1..8: integer gamma (1 MUFU + G-1.. FMULs); G = 0: general
+// gamma via exp2(-gamma log2 s) (2 MUFU).  The t-kernel K = (1 + d^2)^-gamma.
+template <int G>
+__device__ __forceinline__ float pow_neg(float s, float neg_gamma) {
+  if constexpr (G == 0) {
+    return ex2_approx(neg_gamma * lg2_approx(s));
+  } else {
+    const float r = rcp_approx(s);
+    if constexpr (G == 1) return r;
+    if constexpr (G == 2) return r * r;
+    if constexpr (G == 3) return r * r * r;
+    if constexpr (G == 4) { const float r2 = r * r; return r2 * r2; }
+    float q = r;
+#pragma unroll
+    for (int i = 1; i < G; ++i) q *= r;
+    return q;
+  }
+}
+
+// Order-preserving float <-> uint mapping for exact atomic min/max of fp32 values.
+__device__ __forceinline__ unsigned int f2key(float f) {
+  const unsigned int u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float key2f(unsigned int k) {
+  const unsigned int u = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
+  return __uint_as_float(u);
+}
+
+// Lagrange basis on K equispaced nodes t_c = (c + 1/2)/K of [0, 1] (R8):
+// l_c(u) = prod_{c' != c} (u - t_c') / (t_c - t_c').  Constants fold at compile time.
+template <int K>
+__device__ __forceinline__ void lagrange(float u, float (&l)[K]) {
+#pragma unroll
+  for (int c = 0; c < K; ++c) {
+    float v = 1.0f;
+#pragma unroll
+    for (int cp = 0; cp < K; ++cp) {
+      if (cp != c) {
+        const float tc = (c + 0.5f) / K, tcp = (cp + 0.5f) / K;
+        v *= (u - tcp) * (1.0f / (tc - tcp));
+      }
+    }
+    l[c] = v;
+  }
+}
+
+}  // namespace tfdp

@@ -1,0 +1,331 @@
+// ibFFT path kernels — sm_100a.
+//   bbox          exact fp32 min/max of the positions (ordered-uint atomics)
+//   setup         box -> (lo, L, N_int, w, h, centre) on the device, no host sync (R5/R6/R19)
+//   zero_grid     clears the M_cap x M_cap corner of the 3 zero-padded P x P charge planes
+//   spread        step 1: Lagrange charges {1, x~, y~} onto the k x k nodes of each
+//                 node's own interval; fp32 atomics into L2
+//   kgrid         kernel samples K(h da, h db) / P^2 on the circulant embedding (R9)
+//   mult          step 2 in frequency space: C^_v *= K^ (K real and even => K^ real)
+//   gather_update step 3 + assemble + attraction + update,
+//                 fused bbox of the new positions for the next iteration
+// The FFTs themselves are cuFFT R2C/C2R (library call).
+#include <algorithm>
+
+#include "device_math.cuh"
+#include "tfdp_internal.h"
+
+namespace tfdp {
+
+// ------------------------------------------------------------------ bbox
+__device__ __forceinline__ void box_reduce_commit(unsigned kx0, unsigned ky0, unsigned kx1,
+                                                  unsigned ky1, BoxKeys* keys) {
+  kx0 = __reduce_min_sync(0xffffffffu, kx0);
+  ky0 = __reduce_min_sync(0xffffffffu, ky0);
+  kx1 = __reduce_max_sync(0xffffffffu, kx1);
+  ky1 = __reduce_max_sync(0xffffffffu, ky1);
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(&keys->minx, kx0);
+    atomicMin(&keys->miny, ky0);
+    atomicMax(&keys->maxx, kx1);
+    atomicMax(&keys->maxy, ky1);
+  }
+}
+
+__global__ void __launch_bounds__(kNodeThreads)
+bbox_kernel(const float2* __restrict__ xy, int64_t n, BoxKeys* keys) {
+  unsigned kx0 = 0xffffffffu, ky0 = 0xffffffffu, kx1 = 0u, ky1 = 0u;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float2 p = xy[i];
+    const unsigned a = f2key(p.x), b = f2key(p.y);
+    kx0 = min(kx0, a);
+    ky0 = min(ky0, b);
+    kx1 = max(kx1, a);
+    ky1 = max(ky1, b);
+  }
+  box_reduce_commit(kx0, ky0, kx1, ky1, keys);
+}
+
+__global__ void reset_keys_kernel(BoxKeys* keys) {
+  keys->minx = keys->miny = 0xffffffffu;
+  keys->maxx = keys->maxy = 0u;
+}
+
+void launch_reset_keys(BoxKeys* keys, cudaStream_t s) { reset_keys_kernel<<<1, 1, 0, s>>>(keys); }
+
+void launch_bbox(const float2* xy, int64_t n, BoxKeys* keys, cudaStream_t s) {
+  int blocks = (int)std::min<int64_t>((n + kNodeThreads - 1) / kNodeThreads, 148 * 8);
+  if (blocks < 1) blocks = 1;
+  bbox_kernel<<<blocks, kNodeThreads, 0, s>>>(xy, n, keys);
+}
+
+// ------------------------------------------------------------------ setup
+__global__ void setup_kernel(BoxKeys* keys, GridGeom* geom, int k, int n_int_min,
+                             int n_int_fixed, int n_int_cap, int P, int* capped_flag) {
+  const float mnx = key2f(keys->minx), mny = key2f(keys->miny);
+  const float mxx = key2f(keys->maxx), mxy = key2f(keys->maxy);
+  // R6: bounding square anchored at (min x, min y), side L = max(span_x, span_y) (fp32, R19)
+  float L = fmaxf(__fsub_rn(mxx, mnx), __fsub_rn(mxy, mny));
+  float lox = mnx, loy = mny;
+  if (L == 0.0f) {  // all points coincident: unit square centred on them
+    lox = __fsub_rn(mnx, 0.5f);
+    loy = __fsub_rn(mny, 0.5f);
+    L = 1.0f;
+  }
+  int nint;
+  int capped = 0;
+  if (n_int_fixed > 0) {
+    nint = n_int_fixed;
+  } else {
+    const float cl = ceilf(L);  // R5: N_int = max(n_int_min, ceil L)
+    if (!(cl <= (float)n_int_cap)) {
+      nint = n_int_cap;
+      capped = 1;
+    } else {
+      nint = max(n_int_min, (int)cl);
+    }
+  }
+  if (nint > n_int_cap) {
+    nint = n_int_cap;
+    capped = 1;
+  }
+  GridGeom g;
+  g.lo_x = lox;
+  g.lo_y = loy;
+  g.L = L;
+  g.w = __fdiv_rn(L, (float)nint);
+  g.h = __fdiv_rn(g.w, (float)k);
+  g.cx = __fmaf_rn(0.5f, L, lox);
+  g.cy = __fmaf_rn(0.5f, L, loy);
+  g.n_int = nint;
+  g.k = k;
+  g.M = nint * k;
+  g.P = P;
+  g.capped = capped;
+  g.pad = 0;
+  *geom = g;
+  if (capped) atomicOr(capped_flag, 1);
+  // consumed: reset for the bbox fused into this iteration's update
+  keys->minx = keys->miny = 0xffffffffu;
+  keys->maxx = keys->maxy = 0u;
+}
+
+void launch_setup(BoxKeys* keys, GridGeom* geom, int k, int n_int_min, int n_int_fixed,
+                  int n_int_cap, int P, int* capped_flag, cudaStream_t s) {
+  setup_kernel<<<1, 1, 0, s>>>(keys, geom, k, n_int_min, n_int_fixed, n_int_cap, P, capped_flag);
+}
+
+// ------------------------------------------------------------------ zero
+__global__ void zero_grid_kernel(float* __restrict__ grid, int P, int Mcap) {
+  // rows [0, Mcap) x columns [0, Mcap) of each of the 3 planes (blockIdx.z)
+  float* base = grid + ((int64_t)blockIdx.z * P + blockIdx.y) * P;
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < Mcap; c += gridDim.x * blockDim.x)
+    base[c] = 0.0f;
+}
+
+void launch_zero_grid(float* grid, int P, int Mcap, cudaStream_t s) {
+  const int threads = 256;
+  dim3 g((unsigned)max(1, min(8, (Mcap + threads - 1) / threads)), (unsigned)Mcap, 3);
+  zero_grid_kernel<<<g, threads, 0, s>>>(grid, P, Mcap);
+}
+
+// ------------------------------------------------------------------ interval coords
+struct Cell {
+  int bx, by;
+  float ux, uy;
+};
+
+// b = min(floor((x - lo)/w), N_int - 1), u = (x - lo)/w - b, all in IEEE fp32 (R7, R19):
+// the same operations as the oracle's interval_coords, so the integer decision matches.
+__device__ __forceinline__ Cell cell_of(float2 p, const GridGeom& g) {
+  Cell c;
+  const float tx = __fdiv_rn(__fsub_rn(p.x, g.lo_x), g.w);
+  const float ty = __fdiv_rn(__fsub_rn(p.y, g.lo_y), g.w);
+  c.bx = max(0, min((int)floorf(tx), g.n_int - 1));
+  c.by = max(0, min((int)floorf(ty), g.n_int - 1));
+  c.ux = __fsub_rn(tx, (float)c.bx);
+  c.uy = __fsub_rn(ty, (float)c.by);
+  return c;
+}
+
+// ------------------------------------------------------------------ spread (step 1)
+template <int K>
+__global__ void __launch_bounds__(kNodeThreads)
+spread_kernel(const float2* __restrict__ xy, int64_t lo, int64_t cnt,
+              const GridGeom* __restrict__ geom, float* __restrict__ grid) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= cnt) return;
+  const GridGeom g = *geom;
+  const float2 p = xy[lo + t];
+  const Cell c = cell_of(p, g);
+  float lx[K], ly[K];
+  lagrange<K>(c.ux, lx);
+  lagrange<K>(c.uy, ly);
+  const float xt = p.x - g.cx, yt = p.y - g.cy;  // box-centred channels (R11)
+  const int64_t plane = (int64_t)g.P * g.P;
+#pragma unroll
+  for (int b = 0; b < K; ++b) {
+    const int64_t row = (int64_t)(c.by * K + b) * g.P;
+#pragma unroll
+    for (int a = 0; a < K; ++a) {
+      const int64_t idx = row + c.bx * K + a;
+      const float wgt = lx[a] * ly[b];
+      atomicAdd(grid + idx, wgt);
+      atomicAdd(grid + plane + idx, wgt * xt);
+      atomicAdd(grid + 2 * plane + idx, wgt * yt);
+    }
+  }
+}
+
+void launch_spread(const float2* xy, int64_t lo, int64_t cnt, const GridGeom* geom, int k,
+                   float* grid, cudaStream_t s) {
+  if (cnt <= 0) return;
+  const unsigned blocks = (unsigned)((cnt + kNodeThreads - 1) / kNodeThreads);
+  if (k == 1) spread_kernel<1><<<blocks, kNodeThreads, 0, s>>>(xy, lo, cnt, geom, grid);
+  else if (k == 2) spread_kernel<2><<<blocks, kNodeThreads, 0, s>>>(xy, lo, cnt, geom, grid);
+  else spread_kernel<3><<<blocks, kNodeThreads, 0, s>>>(xy, lo, cnt, geom, grid);
+}
+
+// ------------------------------------------------------------------ kernel grid
+template <int G>
+__global__ void __launch_bounds__(256)
+kgrid_kernel(const GridGeom* __restrict__ geom, int P, float neg_gamma, float* __restrict__ kreal) {
+  const int i1 = blockIdx.x * blockDim.x + threadIdx.x;  // x offset index
+  const int i0 = blockIdx.y;                             // y offset index
+  if (i1 >= P) return;
+  const GridGeom g = *geom;
+  const int M = g.M;
+  // circulant embedding of the offsets -(M-1)..(M-1) (linear convolution, R9)
+  const int dx = (i1 <= M - 1) ? i1 : ((i1 >= P - (M - 1)) ? i1 - P : INT32_MAX);
+  const int dy = (i0 <= M - 1) ? i0 : ((i0 >= P - (M - 1)) ? i0 - P : INT32_MAX);
+  float v = 0.0f;
+  if (dx != INT32_MAX && dy != INT32_MAX) {
+    const float d2 = (float)(dx * dx + dy * dy);  // exact integer < 2^24
+    const float s = fmaf(g.h * g.h, d2, 1.0f);
+    v = pow_neg<G>(s, neg_gamma) * (1.0f / ((float)P * (float)P));  // 1/P^2 of the C2R
+  }
+  kreal[(int64_t)i0 * P + i1] = v;
+}
+
+void launch_kgrid(const GridGeom* geom, int P, ForceArgs fa, float* kreal, cudaStream_t s) {
+  dim3 grid((unsigned)((P + 255) / 256), (unsigned)P);
+  const float ng = -fa.gamma;
+  switch (fa.gamma_int) {
+    case 1: kgrid_kernel<1><<<grid, 256, 0, s>>>(geom, P, ng, kreal); break;
+    case 2: kgrid_kernel<2><<<grid, 256, 0, s>>>(geom, P, ng, kreal); break;
+    case 3: kgrid_kernel<3><<<grid, 256, 0, s>>>(geom, P, ng, kreal); break;
+    case 4: kgrid_kernel<4><<<grid, 256, 0, s>>>(geom, P, ng, kreal); break;
+    case 8: kgrid_kernel<8><<<grid, 256, 0, s>>>(geom, P, ng, kreal); break;
+    default: kgrid_kernel<0><<<grid, 256, 0, s>>>(geom, P, ng, kreal); break;
+  }
+}
+
+// ------------------------------------------------------------------ spectral multiply
+__global__ void __launch_bounds__(256)
+mult_kernel(float2* __restrict__ chat, const float2* __restrict__ khat, int64_t ncplx) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < ncplx;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const float kr = khat[e].x;  // K even in both axes => K^ real (imaginary part = rounding)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      float2 v = chat[c * ncplx + e];
+      v.x *= kr;
+      v.y *= kr;
+      chat[c * ncplx + e] = v;
+    }
+  }
+}
+
+void launch_mult(float2* chat, const float2* khat, int P, cudaStream_t s) {
+  const int64_t ncplx = (int64_t)P * (P / 2 + 1);
+  const int blocks = (int)std::min<int64_t>((ncplx + 255) / 256, 148 * 16);
+  mult_kernel<<<blocks, 256, 0, s>>>(chat, khat, ncplx);
+}
+
+// ------------------------------------------------------------------ gather + update
+template <int K>
+__global__ void __launch_bounds__(kNodeThreads)
+gather_update_kernel(const float2* __restrict__ xy, float2* __restrict__ xy_next, int64_t lo,
+                     int64_t n_local, const GridGeom* __restrict__ geom,
+                     const float* __restrict__ phi, const int64_t* __restrict__ row_ptr,
+                     const int32_t* __restrict__ col, ForceArgs fa, float eta, int iter,
+                     int update, float2* __restrict__ rep_out, float2* __restrict__ att_out,
+                     unsigned long long* diverge, BoxKeys* next_keys) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool active = t < n_local;
+  unsigned kx0 = 0xffffffffu, ky0 = 0xffffffffu, kx1 = 0u, ky1 = 0u;
+  if (active) {
+    const int64_t i = lo + t;
+    const GridGeom g = *geom;
+    const float2 p = xy[i];
+    const Cell c = cell_of(p, g);
+    float lx[K], ly[K];
+    lagrange<K>(c.ux, lx);
+    lagrange<K>(c.uy, ly);
+    const int64_t plane = (int64_t)g.P * g.P;
+    float psi0 = 0.f, psi1 = 0.f, psi2 = 0.f;
+#pragma unroll
+    for (int b = 0; b < K; ++b) {
+      const int64_t row = (int64_t)(c.by * K + b) * g.P;
+#pragma unroll
+      for (int a = 0; a < K; ++a) {
+        const int64_t idx = row + c.bx * K + a;
+        const float wgt = lx[a] * ly[b];
+        psi0 = fmaf(wgt, __ldg(phi + idx), psi0);
+        psi1 = fmaf(wgt, __ldg(phi + plane + idx), psi1);
+        psi2 = fmaf(wgt, __ldg(phi + 2 * plane + idx), psi2);
+      }
+    }
+    const float xt = p.x - g.cx, yt = p.y - g.cy;
+    // F^r = x~ psi_1 - psi_x~  (Eqs. Fr1/Fr2); fused to limit cancellation (R11)
+    const float Rx = fa.rho * fmaf(xt, psi0, -psi1);
+    const float Ry = fa.rho * fmaf(yt, psi0, -psi2);
+    float ax = 0.f, ay = 0.f;
+    const int64_t e1 = row_ptr[i + 1];
+    for (int64_t e = row_ptr[i]; e < e1; ++e) {
+      const float2 xj = xy[col[e]];
+      const float dx = p.x - xj.x, dy = p.y - xj.y;
+      const float s = fmaf(dx, dx, fmaf(dy, dy, 1.0f));
+      const float cc = fmaf(fa.beta, rcp_approx(s), 1.0f);
+      ax = fmaf(cc, dx, ax);
+      ay = fmaf(cc, dy, ay);
+    }
+    ax *= -fa.alpha;
+    ay *= -fa.alpha;
+    if (update) {
+      const float nx = fmaf(eta, Rx + ax, p.x);
+      const float ny = fmaf(eta, Ry + ay, p.y);
+      xy_next[i] = make_float2(nx, ny);
+      if (!isfinite(nx) || !isfinite(ny)) {
+        atomicMin(diverge, ((unsigned long long)(unsigned)iter << 32) | (unsigned long long)i);
+      } else {
+        kx0 = kx1 = f2key(nx);
+        ky0 = ky1 = f2key(ny);
+      }
+    } else {
+      if (rep_out) rep_out[t] = make_float2(Rx, Ry);
+      if (att_out) att_out[t] = make_float2(ax, ay);
+    }
+  }
+  if (update && next_keys) box_reduce_commit(kx0, ky0, kx1, ky1, next_keys);
+}
+
+void launch_gather_update(const float2* xy, float2* xy_next, int64_t lo, int64_t n_local,
+                          const GridGeom* geom, int k, const float* phi,
+                          const int64_t* row_ptr, const int32_t* col, ForceArgs fa,
+                          float eta, int iter, int update, float2* rep_out, float2* att_out,
+                          unsigned long long* diverge, BoxKeys* next_keys, cudaStream_t s) {
+  if (n_local <= 0) return;
+  const unsigned blocks = (unsigned)((n_local + kNodeThreads - 1) / kNodeThreads);
+#define TFDP_GU(KK)                                                                         \
+  gather_update_kernel<KK><<<blocks, kNodeThreads, 0, s>>>(xy, xy_next, lo, n_local, geom,  \
+                                                           phi, row_ptr, col, fa, eta, iter, \
+                                                           update, rep_out, att_out, diverge,\
+                                                           next_keys)
+  if (k == 1) TFDP_GU(1);
+  else if (k == 2) TFDP_GU(2);
+  else TFDP_GU(3);
+#undef TFDP_GU
+}
+
+}  // namespace tfdp

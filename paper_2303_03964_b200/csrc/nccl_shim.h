@@ -1,0 +1,26 @@
+// NCCL resolved at run time (dlopen of libnccl.so.2 — normally the copy torch already
+// loaded), so libtfdp.so has no link-time NCCL dependency and loads on CPU-only hosts.
+#pragma once
+
+#include <nccl.h>
+
+namespace tfdp {
+
+struct NcclApi {
+  bool loaded = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t,
+                            ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+// Returns nullptr (and fills err) if NCCL cannot be resolved.
+const NcclApi* nccl_api(const char** err);
+
+}  // namespace tfdp

@@ -1,0 +1,71 @@
+// Internal declarations shared by the host runtime (api.cpp) and the sm_100a kernels.
+// See DESIGN.md §Kernels for the roofline of each kernel.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace tfdp {
+
+constexpr int kExactThreads = 256;  // exact kernel block
+constexpr int kExactTPT = 4;        // targets per thread (register blocking)
+constexpr int kExactTargetsPerBlock = kExactThreads * kExactTPT;
+constexpr int kExactTile = 1024;    // sources per smem tile (fp32 partial sum length)
+constexpr int kNodeThreads = 256;   // per-node kernels
+
+// Geometry of one ibFFT evaluation, computed on the device from the box (no host sync).
+struct GridGeom {
+  float lo_x, lo_y;  // lower-left corner of the bounding square (R6)
+  float L;           // side (R6)
+  float w;           // interval width L / N_int (fp32, R19)
+  float h;           // grid spacing w / k
+  float cx, cy;      // centre lo + L/2 (R11)
+  int n_int;         // intervals per axis (R5)
+  int k;             // nodes per interval (1..3)
+  int M;             // grid points per axis = n_int * k
+  int P;             // FFT size (>= 2M - 1, R9)
+  int capped;        // 1 if n_int was clamped to the allocated grid (warning)
+  int pad;
+};
+
+// Box as order-preserving uint keys so atomicMin/atomicMax give the exact fp32 min/max.
+struct BoxKeys {
+  unsigned int minx, miny, maxx, maxy;
+};
+
+// Kernel-side parameters of the force law.
+struct ForceArgs {
+  float alpha, beta, gamma, rho;
+  int gamma_int;  // 1..8 if gamma is that integer, else 0 (general path)
+};
+
+// ---- launchers (kernels.cu / kernels_fft.cu); all enqueue on `s` ---------------------
+// exact path
+void launch_exact_partial(const float2* xy, int64_t n, int64_t lo, int64_t n_local,
+                          int64_t chunk, int n_chunks, ForceArgs fa, double2* part,
+                          cudaStream_t s);
+// finish: sum partials (fixed chunk order) + CSR attraction + (update | write forces)
+void launch_exact_finish(const float2* xy, float2* xy_next, int64_t lo, int64_t n_local,
+                         int n_chunks, const double2* part, const int64_t* row_ptr,
+                         const int32_t* col, ForceArgs fa, float eta, int iter, int update,
+                         float2* rep_out, float2* att_out, unsigned long long* diverge,
+                         cudaStream_t s);
+
+// ibFFT path
+void launch_bbox(const float2* xy, int64_t n, BoxKeys* keys, cudaStream_t s);
+void launch_setup(BoxKeys* keys, GridGeom* geom, int k, int n_int_min, int n_int_fixed,
+                  int n_int_cap, int P, int* capped_flag, cudaStream_t s);
+void launch_zero_grid(float* grid, int P, int Mcap, cudaStream_t s);
+void launch_spread(const float2* xy, int64_t lo, int64_t cnt, const GridGeom* geom, int k,
+                   float* grid, cudaStream_t s);
+void launch_kgrid(const GridGeom* geom, int P, ForceArgs fa, float* kreal, cudaStream_t s);
+void launch_mult(float2* chat, const float2* khat, int P, cudaStream_t s);
+void launch_gather_update(const float2* xy, float2* xy_next, int64_t lo, int64_t n_local,
+                          const GridGeom* geom, int k, const float* phi,
+                          const int64_t* row_ptr, const int32_t* col, ForceArgs fa,
+                          float eta, int iter, int update, float2* rep_out, float2* att_out,
+                          unsigned long long* diverge, BoxKeys* next_keys,
+                          cudaStream_t s);
+void launch_reset_keys(BoxKeys* keys, cudaStream_t s);
+
+}  // namespace tfdp

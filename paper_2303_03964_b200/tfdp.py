@@ -1,0 +1,211 @@
+"""Python binding of libtfdp (include/tfdp.h) — argument marshalling only.
+
+    from paper_2303_03964_b200 import Params, Layout, csr_build
+    row_ptr, col = csr_build(n, u, v)
+    L = Layout(n, row_ptr, col, xy0, Params(solver="ibfft"))
+    L.step(300); xy = L.layout()
+
+Arrays may be NumPy (host) or torch tensors (host or CUDA); torch supplies device memory
+and the stream (torch.cuda.current_stream()) — the computation is libtfdp's kernels.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+
+import numpy as np
+
+from . import _lib as _L
+from ._lib import check, lib
+
+
+@dataclasses.dataclass
+class Params:
+    """Mirror of tfdp_params (defaults: P:372 alpha=0.1 beta=8 gamma=2; S:340 eta0=0.1;
+    T=300 (R3); N_int >= 50)."""
+    alpha: float = 0.1
+    beta: float = 8.0
+    gamma: float = 2.0
+    rho: float = 1.0
+    solver: str = "exact"  # "exact" | "ibfft"
+    k: int = 0  # 0 = dynamic 90/5/5
+    n_int_min: int = 50
+    n_int_fixed: int = 0
+    fft_size: int = 0
+    step0: float = 0.1
+    iterations: int = 300
+    t0: int = 0
+    cooling: str = "linear"  # "linear" (R2) | "constant" (R2')
+    dist_mode: str = "spread_all"  # "spread_all" | "grid_allreduce"
+    dim: int = 2
+
+    def to_c(self) -> _L.tfdp_params:
+        p = _L.tfdp_params()
+        check(lib().tfdp_params_default(C.byref(p)))
+        p.dim = self.dim
+        p.alpha, p.beta, p.gamma, p.rho = self.alpha, self.beta, self.gamma, self.rho
+        p.solver = {"exact": _L.EXACT, "ibfft": _L.IBFFT}[self.solver]
+        p.k, p.n_int_min, p.n_int_fixed, p.fft_size = self.k, self.n_int_min, self.n_int_fixed, self.fft_size
+        p.step0, p.iterations, p.t0 = self.step0, self.iterations, self.t0
+        p.cooling = {"linear": _L.COOL_LINEAR, "constant": _L.COOL_CONSTANT}[self.cooling]
+        p.dist_mode = {"spread_all": _L.DIST_SPREAD_ALL, "grid_allreduce": _L.DIST_GRID_ALLREDUCE}[self.dist_mode]
+        return p
+
+
+def _ptr(a):
+    """(pointer, keepalive) of a NumPy array or torch tensor (contiguous)."""
+    if a is None:
+        return None, None
+    if isinstance(a, np.ndarray):
+        if not a.flags["C_CONTIGUOUS"]:
+            a = np.ascontiguousarray(a)
+        return a.ctypes.data, a
+    try:
+        import torch
+    except ImportError:  # pragma: no cover
+        torch = None
+    if torch is not None and isinstance(a, torch.Tensor):
+        if not a.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return a.data_ptr(), a
+    raise TypeError(f"unsupported array type {type(a)}")
+
+
+def csr_build(n: int, u, v):
+    """Symmetric CSR via the library (tfdp_csr_build)."""
+    u = np.ascontiguousarray(u, dtype=np.int32)
+    v = np.ascontiguousarray(v, dtype=np.int32)
+    m = int(u.shape[0])
+    row_ptr = np.empty(n + 1, dtype=np.int64)
+    col = np.empty(max(2 * m, 1), dtype=np.int32)
+    nnz = C.c_int64(0)
+    check(lib().tfdp_csr_build(n, m, u.ctypes.data, v.ctypes.data, row_ptr.ctypes.data,
+                               col.ctypes.data, C.byref(nnz)))
+    return row_ptr, col[: nnz.value].copy()
+
+
+def shard_range(n: int, world: int, rank: int):
+    lo, hi = C.c_int64(), C.c_int64()
+    check(lib().tfdp_shard_range(n, world, rank, C.byref(lo), C.byref(hi)))
+    return lo.value, hi.value
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_ubyte * 128)()
+    check(lib().tfdp_nccl_unique_id(C.cast(buf, C.c_void_p)))
+    return bytes(buf)
+
+
+class Dist:
+    """rank/world/device + the 128-byte NCCL unique id (see dist.bootstrap)."""
+
+    def __init__(self, rank: int, world: int, device: int, uid: bytes | None):
+        self._uid = (C.c_ubyte * 128).from_buffer_copy(uid) if uid else None
+        self.c = _L.tfdp_dist(rank, world, device, C.cast(self._uid, C.c_void_p) if uid else None)
+        self.rank, self.world, self.device = rank, world, device
+
+
+class Layout:
+    """One t-FDP layout context (tfdp_init ... tfdp_destroy)."""
+
+    def __init__(self, n: int, row_ptr, col, xy0, params: Params | None = None,
+                 dist: Dist | None = None, stream: int | None = None):
+        self.n = int(n)
+        self.params = params or Params()
+        rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+        cl = np.ascontiguousarray(col, dtype=np.int32)
+        if rp.shape[0] != self.n + 1:
+            raise ValueError("row_ptr must have n+1 entries")
+        xp, keep = _ptr(xy0 if not isinstance(xy0, np.ndarray) else np.ascontiguousarray(xy0, np.float32))
+        self._ctx = C.c_void_p()
+        pc = self.params.to_c()
+        st = lib().tfdp_init(C.byref(self._ctx), self.n, rp.ctypes.data,
+                             cl.ctypes.data if cl.size else None, xp, C.byref(pc),
+                             C.byref(dist.c) if dist else None, stream)
+        if st != _L.TFDP_OK:
+            m = lib().tfdp_last_error(None)
+            raise _L.TfdpError(st, m.decode() if m else "")
+        del keep
+        lo, hi = C.c_int64(), C.c_int64()
+        check(lib().tfdp_shard(self._ctx, C.byref(lo), C.byref(hi)), self._ctx)
+        self.lo, self.hi = lo.value, hi.value
+
+    # -- lifecycle --------------------------------------------------------------------
+    def close(self):
+        if getattr(self, "_ctx", None) and self._ctx.value:
+            lib().tfdp_destroy(self._ctx)
+            self._ctx = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # -- calls --------------------------------------------------------------------------
+    def step(self, n_iters: int = 1):
+        check(lib().tfdp_step(self._ctx, int(n_iters)), self._ctx)
+
+    def forces(self, rep=None, att=None):
+        """(R, A) for this rank's shard.  With no arguments returns NumPy float32 (hi-lo, 2)."""
+        own = rep is None and att is None
+        if own:
+            m = self.hi - self.lo
+            rep = np.empty((m, 2), np.float32)
+            att = np.empty((m, 2), np.float32)
+        rp, k1 = _ptr(rep)
+        ap, k2 = _ptr(att)
+        check(lib().tfdp_forces(self._ctx, rp, ap), self._ctx)
+        return rep, att
+
+    def layout(self, out=None):
+        if out is None:
+            out = np.empty((self.n, 2), np.float32)
+        p, k = _ptr(out)
+        check(lib().tfdp_layout(self._ctx, p), self._ctx)
+        return out
+
+    def set_layout(self, xy):
+        if isinstance(xy, np.ndarray):
+            xy = np.ascontiguousarray(xy, np.float32)
+        p, k = _ptr(xy)
+        check(lib().tfdp_set_layout(self._ctx, p), self._ctx)
+
+    def set_iteration(self, t: int):
+        check(lib().tfdp_set_iteration(self._ctx, int(t)), self._ctx)
+
+    @property
+    def iteration(self) -> int:
+        return int(lib().tfdp_iteration(self._ctx))
+
+    @property
+    def warnings(self) -> int:
+        return int(lib().tfdp_warnings(self._ctx))
+
+    def fft_geometry(self):
+        box = (C.c_float * 4)()
+        ni, k, P = C.c_int32(), C.c_int32(), C.c_int32()
+        check(lib().tfdp_fft_geometry(self._ctx, C.cast(box, C.c_void_p), C.byref(ni), C.byref(k),
+                                      C.byref(P)), self._ctx)
+        return dict(lo=(box[0], box[1]), L=box[2], w=box[3], n_int=ni.value, k=k.value, P=P.value)
+
+    def profile(self, enable: bool = True):
+        check(lib().tfdp_profile(self._ctx, int(enable)), self._ctx)
+
+    def profile_read(self) -> dict:
+        cap = 32
+        names = (C.c_char_p * cap)()
+        ms = (C.c_double * cap)()
+        cnt = (C.c_int64 * cap)()
+        k = lib().tfdp_profile_read(self._ctx, names, ms, cnt, cap)
+        return {names[i].decode(): (ms[i], cnt[i]) for i in range(k) if cnt[i] > 0}
+
+    @property
+    def launch_count(self) -> int:
+        return int(lib().tfdp_launch_count(self._ctx))

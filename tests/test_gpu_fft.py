@@ -1,0 +1,154 @@
+"""GPU parity of the ibFFT path: libtfdp's tfdp_forces vs the oracle's
+step-by-step ibFFT at identical (box, N_int, k) — the box and interval index are decided in
+fp32 on both sides (R19) — and vs the exact oracle within the oracle's own ibFFT error.
+Bar: (i) rel-L2 <= 1e-3 vs oracle-ibFFT; (ii) <= e_k + 1e-3 vs exact; full-run NP1 within
+0.01 (C3, dynamic k, T=300)."""
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2303_03964_b200 as P
+from synth import make_config, random_graph, random_layout
+
+pytestmark = pytest.mark.gpu
+TOL_IB = 1e-3
+
+
+def _case(name):
+    w = make_config(name)
+    rp, col = P.csr_build(w.n, w.u, w.v)
+    return w, rp, col
+
+
+def _fft_forces(w_n, rp, col, X, k, **kw):
+    with P.Layout(w_n, rp, col, X, P.Params(solver="ibfft", k=k, **kw)) as L:
+        R, A = L.forces()
+        geo = L.fft_geometry()
+    return R, A, geo
+
+
+@pytest.mark.parametrize("name", ["C2", "C2rgg"])
+@pytest.mark.parametrize("k", [1, 2, 3])
+def test_c2_vs_oracle_ibfft_and_exact(name, k):
+    w, rp, col = _case(name)
+    X = w.xy.astype(np.float64)
+    R, A, geo = _fft_forces(w.n, rp, col, w.xy, k)
+    box = O.box_rule(w.xy)
+    assert geo["n_int"] == box.n_int and geo["k"] == k
+    assert np.float32(geo["L"]) == box.L and np.float32(geo["w"]) == box.w
+    assert (np.float32(geo["lo"][0]), np.float32(geo["lo"][1])) == (box.lo[0], box.lo[1])
+    assert geo["P"] >= 2 * box.n_int * k - 1
+    Ro = O.repulsion_ibfft(X, k)
+    Re = O.repulsion_exact(X)
+    e_ib = O.rel_l2(R, Ro)
+    e_k = O.rel_l2(Ro, Re)
+    assert e_ib <= TOL_IB, (e_ib, e_k)
+    assert O.rel_l2(R, Re) <= e_k + 1e-3
+    assert O.rel_l2(A, O.attraction(X, rp, col)) <= 1e-4
+
+
+@pytest.mark.parametrize("k", [1, 2, 3])
+def test_fixed_grid_and_fft_size(k):
+    """n_int_fixed / fft_size overrides: any P >= 2M-1 gives the same linear convolution."""
+    n = 4000
+    X = random_layout(n, 31, 8.0)
+    u, v = random_graph(n, 4 * n, 32)
+    rp, col = P.csr_build(n, u, v)
+    Ro = O.repulsion_ibfft(X.astype(np.float64), k, n_int_fixed=64)
+    outs = []
+    for P_ in (0, 2 * 64 * k + 40):
+        R, _, geo = _fft_forces(n, rp, col, X, k, n_int_fixed=64, fft_size=P_)
+        assert geo["n_int"] == 64
+        outs.append(R)
+        assert O.rel_l2(R, Ro) <= TOL_IB
+    assert O.rel_l2(outs[0], outs[1]) <= 2e-5
+
+
+def test_c3_snapshot_all_k():
+    w, rp, col = _case("C3")
+    X = w.xy.astype(np.float64)
+    for k in (1, 3):
+        R, A, geo = _fft_forces(w.n, rp, col, w.xy, k)
+        assert geo["n_int"] == O.box_rule(w.xy).n_int
+        assert O.rel_l2(R, O.repulsion_ibfft(X, k)) <= TOL_IB
+
+
+def test_coincident_and_degenerate():
+    n = 300
+    X = np.tile(np.array([[2.5, -1.0]], np.float32), (n, 1))
+    u, v = random_graph(n, 600, 3)
+    rp, col = P.csr_build(n, u, v)
+    R, A, geo = _fft_forces(n, rp, col, X, 3)
+    assert geo["L"] == 1.0 and geo["n_int"] == 50  # unit square
+    assert np.abs(R).max() < 1e-4 and np.abs(A).max() == 0
+    R1, _, _ = _fft_forces(1, np.zeros(2, np.int64), np.zeros(0, np.int32), X[:1], 1)
+    assert np.abs(R1).max() < 1e-6
+
+
+@pytest.mark.parametrize("world", [2, 5])
+def test_virtual_shards(world):
+    w, rp, col = _case("C2rgg")
+    R1, A1, _ = _fft_forces(w.n, rp, col, w.xy, 2)
+    for r in range(world):
+        with P.Layout(w.n, rp, col, w.xy, P.Params(solver="ibfft", k=2), dist=P.Dist(r, world, 0, None)) as L:
+            R, A = L.forces()
+            lo, hi = L.lo, L.hi
+        assert O.rel_l2(R, R1[lo:hi]) <= 1e-5  # atomics order only (R15)
+        np.testing.assert_array_equal(A, A1[lo:hi])
+
+
+def test_step_and_dynamic_schedule():
+    """Iterations follow the 90/5/5 schedule with the fused box of the update."""
+    w, rp, col = _case("C2")
+    with P.Layout(w.n, rp, col, w.xy, P.Params(solver="ibfft", k=0, iterations=20)) as L:
+        L.step(18)
+        L.forces()
+        assert L.fft_geometry()["k"] == 2  # T=20 -> 18/1/1
+        L.step(1)
+        L.forces()
+        assert L.fft_geometry()["k"] == 3
+        Xg = L.layout()
+    Xo = O.run(w.xy, rp, col, O.Params(), T=20, solver="ibfft", k=0, t_end=19)
+    assert O.rel_l2(Xg - w.xy, Xo - w.xy) < 1e-2  # chaotic amplification is small over 19 steps
+
+
+def test_grid_cap_replans():
+    """A layout that outgrows the preallocated grid: warning + re-plan, still correct."""
+    n = 2000
+    X = random_layout(n, 41, 3.0)
+    u, v = random_graph(n, 2 * n, 42)
+    rp, col = P.csr_build(n, u, v)
+    with P.Layout(n, rp, col, X, P.Params(solver="ibfft", k=1)) as L:
+        big = (X * 60.0).astype(np.float32)  # span ~ 1000 >> initial cap
+        L.set_layout(big)
+        L.forces()  # runs capped, then re-plans
+        assert L.warnings & 4
+        R, _ = L.forces()
+        geo = L.fft_geometry()
+    box = O.box_rule(big)
+    assert geo["n_int"] == box.n_int
+    assert O.rel_l2(R, O.repulsion_ibfft(big.astype(np.float64), 1)) <= TOL_IB
+
+
+@pytest.mark.slow
+def test_c4_forces_vs_oracle():
+    """1M-node RGG at the bench configuration, k = 1 and 3."""
+    w, rp, col = _case("C4")
+    X = w.xy.astype(np.float64)
+    for k in (1, 3):
+        R, A, geo = _fft_forces(w.n, rp, col, w.xy, k)
+        assert geo["n_int"] == O.box_rule(w.xy).n_int
+        e = O.rel_l2(R, O.repulsion_ibfft(X, k))
+        assert e <= TOL_IB, (k, e)
+
+
+@pytest.mark.slow
+def test_full_run_np1_C3():
+    """C3: 300 iterations, dynamic k; NP1 of the GPU layout within 0.01 of the oracle's."""
+    w, rp, col = _case("C3")
+    with P.Layout(w.n, rp, col, w.xy, P.Params(solver="ibfft", k=0)) as L:
+        L.step(300)
+        Xg = L.layout()
+    Xo = O.run(w.xy, rp, col, O.Params(), T=300, solver="ibfft", k=0)
+    ng, no = O.np1(Xg, rp, col), O.np1(Xo, rp, col)
+    assert abs(ng - no) <= 0.01, (ng, no)
