@@ -153,6 +153,10 @@ tfdp_status tfdp_shard(const tfdp_ctx* ctx, int64_t* lo, int64_t* hi);
 tfdp_status tfdp_fft_geometry(tfdp_ctx* ctx, float* box4, int32_t* n_int, int32_t* k,
                               int32_t* fft_size);
 
+/* FFT plan for interpolation order k (1..3): *fft_size = P_k, *n_int_cap = largest N_int
+ * the allocated grid holds at that k (TFDP_ERR_STATE unless an ibFFT context). */
+tfdp_status tfdp_fft_plan(const tfdp_ctx* ctx, int32_t k, int32_t* fft_size, int32_t* n_int_cap);
+
 /* Per-kernel device timing (CUDA events around every launch on the ctx stream).
  * tfdp_profile(ctx, 1) resets and enables, 0 disables.  tfdp_profile_read fills up to
  * cap entries: names (static strings), total milliseconds and launch counts; returns the

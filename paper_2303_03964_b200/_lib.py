@@ -52,6 +52,7 @@ _SIGS = {
     "tfdp_shard": (C.c_int, [_P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "tfdp_fft_geometry": (C.c_int, [_P, _P, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                     C.POINTER(C.c_int32)]),
+    "tfdp_fft_plan": (C.c_int, [_P, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     "tfdp_profile": (C.c_int, [_P, C.c_int32]),
     "tfdp_profile_read": (C.c_int32, [_P, C.POINTER(C.c_char_p), C.POINTER(C.c_double),
                                       C.POINTER(C.c_int64), C.c_int32]),

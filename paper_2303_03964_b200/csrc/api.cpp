@@ -89,6 +89,7 @@ struct tfdp_ctx {
   int cap_of_k[4] = {0, 0, 0, 0};
   std::map<int, FftPlan> plans;
   int64_t P_alloc = 0;
+  int grid_pitch = 0;  // P the charge planes were last laid out with (0 = not zeroed)
   float* grid = nullptr;
   float* phi = nullptr;
   float* kreal = nullptr;
@@ -419,6 +420,7 @@ tfdp_status configure_fft(tfdp_ctx* c, float L) {
     CUDA_TRY(c, cudaMalloc(&c->khat, pc * sizeof(float2)));
     CUDA_TRY(c, cudaMalloc(&c->chat, 3 * pc * sizeof(float2)));
     c->P_alloc = Pmax;
+    c->grid_pitch = 0;  // fresh buffers: padding must be zeroed before first use
   }
   return TFDP_OK;
 }
@@ -478,7 +480,16 @@ tfdp_status evaluate(tfdp_ctx* c, int update, float eta, int k) {
     }
     {
       Scope sc(c, K_ZERO);
-      tfdp::launch_zero_grid(c->grid, P, std::min(c->cap_of_k[k] * k, P), c->stream);
+      if (c->grid_pitch != P) {
+        // New buffers, or k changed the FFT size: charges written under the old row pitch
+        // can sit anywhere in the padding, so clear all planes once.  Afterwards only the
+        // M_cap x M_cap corner is ever written, and only that corner is cleared per call.
+        CUDA_TRY(c, cudaMemsetAsync(c->grid, 0, (size_t)3 * c->P_alloc * c->P_alloc * sizeof(float),
+                                    c->stream));
+        c->grid_pitch = P;
+      } else {
+        tfdp::launch_zero_grid(c->grid, P, std::min(c->cap_of_k[k] * k, P), c->stream);
+      }
     }
     const bool allreduce = c->world > 1 && c->p.dist_mode == TFDP_DIST_GRID_ALLREDUCE;
     {
@@ -899,6 +910,14 @@ tfdp_status tfdp_fft_geometry(tfdp_ctx* c, float* box4, int32_t* n_int, int32_t*
   if (n_int) *n_int = g.n_int;
   if (k) *k = g.k;
   if (fft_size) *fft_size = g.P;
+  return TFDP_OK;
+}
+
+tfdp_status tfdp_fft_plan(const tfdp_ctx* c, int32_t k, int32_t* fft_size, int32_t* n_int_cap) {
+  if (!c || k < 1 || k > 3) return TFDP_ERR_ARG;
+  if (c->p.solver != TFDP_IBFFT) return TFDP_ERR_STATE;
+  if (fft_size) *fft_size = c->P_of_k[k];
+  if (n_int_cap) *n_int_cap = c->cap_of_k[k];
   return TFDP_OK;
 }
 

@@ -195,6 +195,11 @@ class Layout:
                                       C.byref(P)), self._ctx)
         return dict(lo=(box[0], box[1]), L=box[2], w=box[3], n_int=ni.value, k=k.value, P=P.value)
 
+    def fft_plan(self, k: int):
+        P, cap = C.c_int32(), C.c_int32()
+        check(lib().tfdp_fft_plan(self._ctx, int(k), C.byref(P), C.byref(cap)), self._ctx)
+        return P.value, cap.value
+
     def profile(self, enable: bool = True):
         check(lib().tfdp_profile(self._ctx, int(enable)), self._ctx)
 
