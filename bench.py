@@ -107,25 +107,23 @@ def load_peaks():
 
 def alg_bytes(kind: str, n: int, nnz: int, M: int, P: int, n_spread: int) -> float:
     """Algorithmic HBM bytes of one launch (DESIGN.md §Kernels table)."""
-    pc = P * (P // 2 + 1)
-    if kind == "gather_update":  # x read, phi 3 planes (M^2), CSR + x_j, x' write
+    hq = P // 2 + 1  # half-spectrum length
+    if kind == "gather_update":  # x read, Phi 3 planes (M^2), CSR + x_j, x' write
         return 8 * n + 12 * M * M + 8 * (n + 1) + 12 * nnz + 8 * n
     if kind == "spread":
         return 8 * n_spread + 12 * M * M
-    if kind == "kgrid":
-        return 4 * P * P
-    if kind == "mult":
-        return 24 * pc * 2 + 8 * pc
-    if kind == "zero_grid":
+    if kind == "zero_planes":
         return 12 * M * M
+    if kind == "kspec_rows":
+        return 4 * hq * M
+    if kind == "rows_fwd":
+        return 12 * M * M + 24 * hq * M
+    if kind == "cols":
+        return 4 * hq * M + 48 * hq * M
+    if kind == "rows_inv":
+        return 24 * hq * M + 12 * M * M
     if kind == "bbox":
         return 8 * n
-    if kind == "cufft_r2c_grid":
-        return 12 * P * P + 24 * pc
-    if kind == "cufft_c2r":
-        return 24 * pc + 12 * P * P
-    if kind == "cufft_r2c_kernel":
-        return 4 * P * P + 8 * pc
     return 0.0
 
 
@@ -247,7 +245,7 @@ def run_fft(args, rank, world, local):
                "h2d_bytes_per_step": int(xy_host.numel() * 4), "d2h_bytes_per_step": int(out_host.numel() * 4)}
     # --- roofline of the dominant own kernel
     peak, peak_src, _ = load_peaks()
-    own = {k: v for k, v in prof.items() if not k.startswith("cufft") and k != "nccl"}
+    own = {k: v for k, v in prof.items() if k != "nccl"}
     dom = max(own, key=lambda k: own[k][0])
     N_int = geo["n_int"]
     nspread = w.n

@@ -52,15 +52,13 @@ def needs_build() -> bool:
 def build(verbose: bool = False, force: bool = False) -> str:
     if not force and not needs_build():
         return LIB
-    cuda_lib = "/usr/local/cuda/lib64"
     cmd = [
         _nvcc(), "-O3", "-std=c++17", *ARCH, "-lineinfo", "--shared",
         "-Xcompiler", "-fPIC,-fopenmp,-O3",
         "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", _nccl_include(),
         *(["-Xptxas", "-v"] if verbose else []),
         *sources(),
-        "-L", cuda_lib, "-lcufft", "-lgomp", "-ldl",
-        "-Xlinker", f"-rpath,{cuda_lib}",
+        "-lgomp", "-ldl",
         "-o", LIB + ".tmp",
     ]
     r = subprocess.run(cmd, capture_output=True, text=True)

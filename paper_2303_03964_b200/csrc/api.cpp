@@ -1,11 +1,10 @@
 // libtfdp host runtime: the C ABI of include/tfdp.h.
 //
-// Owns device memory, the per-iteration schedule (k_t, eta_t), the FFT plans, the NCCL
+// Owns device memory, the per-iteration schedule (k_t, eta_t), the FFT geometry, the NCCL
 // communicator and the CSR/shard indexing.  Every force evaluation is enqueued as sm_100a
 // kernels (kernels_exact.cu, kernels_fft.cu) or cuFFT on the context stream; there is no
 // host compute path.  Citations as in include/tfdp.h.
 #include <cuda_runtime.h>
-#include <cufft.h>
 #include <dlfcn.h>
 
 #include <algorithm>
@@ -35,26 +34,19 @@ enum Kind {
   K_SETUP,
   K_ZERO,
   K_SPREAD,
-  K_KGRID,
-  K_FFT_K,
-  K_FFT_FWD,
-  K_MULT,
-  K_FFT_INV,
+  K_KSPEC,
+  K_ROWS_FWD,
+  K_COLS,
+  K_ROWS_INV,
   K_GATHER_UPDATE,
   K_COMM,
   K_COUNT
 };
-const char* kKindNames[K_COUNT] = {"exact_partial", "exact_finish", "bbox",   "setup",
-                                   "zero_grid",     "spread",       "kgrid",  "cufft_r2c_kernel",
-                                   "cufft_r2c_grid", "mult",        "cufft_c2r", "gather_update",
-                                   "nccl"};
-const bool kOwnKernel[K_COUNT] = {true, true, true, true, true, true, true,
-                                  false, false, true, false, true, false};
-
-struct FftPlan {
-  int P = 0;
-  cufftHandle r2c3 = 0, r2c1 = 0, c2r3 = 0;
-};
+const char* kKindNames[K_COUNT] = {"exact_partial", "exact_finish", "bbox",     "setup",
+                                   "zero_planes",   "spread",       "kspec_rows", "rows_fwd",
+                                   "cols",          "rows_inv",     "gather_update", "nccl"};
+const bool kOwnKernel[K_COUNT] = {true, true, true, true, true, true,
+                                  true, true, true, true, true, false};
 
 }  // namespace
 
@@ -79,7 +71,7 @@ struct tfdp_ctx {
   // status words
   unsigned long long* diverge = nullptr;
   int* capped = nullptr;
-  unsigned long long* h_status = nullptr;  // pinned [2]
+  unsigned long long* h_status = nullptr;  // pinned [2 + sizeof(GridGeom)/8]
   BoxKeys* keys = nullptr;
   GridGeom* geom = nullptr;
   bool box_valid = false;
@@ -87,14 +79,15 @@ struct tfdp_ctx {
   int nint_cap = 0;
   int P_of_k[4] = {0, 0, 0, 0};
   int cap_of_k[4] = {0, 0, 0, 0};
-  std::map<int, FftPlan> plans;
-  int64_t P_alloc = 0;
-  int grid_pitch = 0;  // P the charge planes were last laid out with (0 = not zeroed)
-  float* grid = nullptr;
-  float* phi = nullptr;
-  float* kreal = nullptr;
-  float2* khat = nullptr;
-  float2* chat = nullptr;
+  int cpitch = 0;        // pitch of the compact [3][M][M] charge / potential planes
+  int ca_pitch = 0;      // row pitch of the half-spectra CA[3][P/2+1][.] (even)
+  int64_t alloc_planes = 0, alloc_ca = 0, alloc_ka = 0;
+  float* grid = nullptr;  // charges C (spread target)
+  float* phi = nullptr;   // potentials Phi (gather source)
+  float2* ca = nullptr;   // row half-spectra, transformed in place by the column pass
+  float* ka = nullptr;    // kernel row spectra KA[q][dy]
+  float2* tw[4] = {nullptr, nullptr, nullptr, nullptr};  // twiddles per k (length P_k)
+  int tw_P[4] = {0, 0, 0, 0};
   // schedule
   int t = 0;
   std::vector<int32_t> ksched;
@@ -140,14 +133,6 @@ tfdp_status fail(tfdp_ctx* c, tfdp_status s, const char* fmt, ...) {
     if (e_ != cudaSuccess)                                                                 \
       return fail(c, e_ == cudaErrorMemoryAllocation ? TFDP_ERR_OOM : TFDP_ERR_CUDA,       \
                   "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__);    \
-  } while (0)
-
-#define CUFFT_TRY(c, call)                                                        \
-  do {                                                                            \
-    cufftResult r_ = (call);                                                      \
-    if (r_ != CUFFT_SUCCESS)                                                      \
-      return fail(c, r_ == CUFFT_ALLOC_FAILED ? TFDP_ERR_OOM : TFDP_ERR_CUDA,     \
-                  "%s: cufft error %d (%s:%d)", #call, (int)r_, __FILE__, __LINE__); \
   } while (0)
 
 #define NCCL_TRY(c, call)                                                                  \
@@ -219,14 +204,20 @@ void prof_collect(tfdp_ctx* c) {
 }
 
 // ---------------------------------------------------------------- helpers
+// Largest FFT the shared-memory kernels hold (cols pass: 24 P bytes <= 227 KB).
+constexpr int kMaxFftSize = 9216;
+
+// Smallest even m >= target of the form 2^a 3^b 5^c with b <= 2, c <= 1 (the radices of
+// kernels_fftconv.cu, few odd stages).
 int nice_fft_size(int64_t target) {
-  // smallest even m >= target with only factors 2,3,5,7 (fast cuFFT radices)
   for (int64_t m = std::max<int64_t>(target, 2);; ++m) {
     if (m & 1) continue;
     int64_t r = m;
-    for (int f : {2, 3, 5, 7})
-      while (r % f == 0) r /= f;
-    if (r == 1) return (int)m;
+    int b = 0, c5 = 0;
+    while (r % 2 == 0) r /= 2;
+    while (r % 3 == 0) { r /= 3; ++b; }
+    while (r % 5 == 0) { r /= 5; ++c5; }
+    if (r == 1 && b <= 2 && c5 <= 1) return (int)m;
   }
 }
 
@@ -348,80 +339,97 @@ void host_box(const float* xy, int64_t n, float* L) {
 }
 
 // ---------------------------------------------------------------- FFT resources
-tfdp_status plan_for(tfdp_ctx* c, int P, FftPlan** out) {
-  auto it = c->plans.find(P);
-  if (it != c->plans.end()) {
-    *out = &it->second;
-    return TFDP_OK;
-  }
-  FftPlan fp;
-  fp.P = P;
-  int dims[2] = {P, P};
-  CUFFT_TRY(c, cufftPlanMany(&fp.r2c3, 2, dims, nullptr, 1, 0, nullptr, 1, 0, CUFFT_R2C, 3));
-  CUFFT_TRY(c, cufftPlanMany(&fp.r2c1, 2, dims, nullptr, 1, 0, nullptr, 1, 0, CUFFT_R2C, 1));
-  CUFFT_TRY(c, cufftPlanMany(&fp.c2r3, 2, dims, nullptr, 1, 0, nullptr, 1, 0, CUFFT_C2R, 3));
-  CUFFT_TRY(c, cufftSetStream(fp.r2c3, c->stream));
-  CUFFT_TRY(c, cufftSetStream(fp.r2c1, c->stream));
-  CUFFT_TRY(c, cufftSetStream(fp.c2r3, c->stream));
-  c->plans[P] = fp;
-  *out = &c->plans[P];
-  return TFDP_OK;
-}
-
 void free_fft_buffers(tfdp_ctx* c) {
   cudaFree(c->grid);
   cudaFree(c->phi);
-  cudaFree(c->kreal);
-  cudaFree(c->khat);
-  cudaFree(c->chat);
-  c->grid = c->phi = c->kreal = nullptr;
-  c->khat = c->chat = nullptr;
-  c->P_alloc = 0;
+  cudaFree(c->ca);
+  cudaFree(c->ka);
+  c->grid = c->phi = c->ka = nullptr;
+  c->ca = nullptr;
+  c->alloc_planes = c->alloc_ca = c->alloc_ka = 0;
+  for (int k = 0; k < 4; ++k) {
+    cudaFree(c->tw[k]);
+    c->tw[k] = nullptr;
+    c->tw_P[k] = 0;
+  }
 }
 
-// Grid cap + FFT size per k from a box side L: N_int cap with
-// 25% headroom over the rule, P_k = smallest 2^a3^b5^c7^d >= 2 N_cap k - 1 (R9).
+bool k_used(const tfdp_ctx* c, int k) { return c->p.k == 0 || c->p.k == k; }
+
+// Grid sizing: N_need = ceil(L) + 8 (or the forced N_int);
+// P_k = smallest 2^a3^b5^c >= 2 N_need k - 1 (R9: any such P is exact); the grid then
+// holds N_int <= cap_k = floor((P_k + 1) / 2k).  Re-planned when the layout outgrows it.
 tfdp_status configure_fft(tfdp_ctx* c, float L) {
   const tfdp_params& p = c->p;
-  int cap;
-  if (p.n_int_fixed > 0) {
-    cap = p.n_int_fixed;
-  } else {
-    const double want = std::max<double>(p.n_int_min, std::ceil((double)L * 1.25) + 8.0);
-    cap = (int)std::min(want, 20000.0);
-  }
-  c->nint_cap = cap;
-  int64_t Pmax = 0;
+  int need;
+  if (p.n_int_fixed > 0) need = p.n_int_fixed;
+  else need = std::max<int>(p.n_int_min, (int)std::min<double>(std::ceil((double)L) + 8.0, 1e6));
+  int mcap = 0;
   for (int k = 1; k <= 3; ++k) {
-    int P;
-    if (p.fft_size > 0) {
-      P = p.fft_size;
-      const int capk = (P + 1) / (2 * k);
-      if (p.n_int_fixed > 0 && capk < cap) {
-        if (p.k == 0 || p.k == k)
-          return fail(c, TFDP_ERR_ARG, "fft_size %d < 2*N_int*k-1 = %d (k=%d)", P,
-                      2 * cap * k - 1, k);
-      }
-      c->cap_of_k[k] = std::min(cap, capk);
-    } else {
-      P = nice_fft_size(2LL * cap * k - 1);
-      c->cap_of_k[k] = cap;
+    int P = p.fft_size > 0 ? p.fft_size : nice_fft_size(2LL * need * k - 1);
+    if (P > kMaxFftSize && p.fft_size == 0) P = kMaxFftSize;  // grid capped (warning bit)
+    int cap = (P + 1) / (2 * k);
+    if (p.n_int_fixed > 0 && k_used(c, k)) {
+      if (cap < p.n_int_fixed)
+        return fail(c, TFDP_ERR_ARG, "fft_size %d < 2*N_int*k-1 = %d (k=%d)", P,
+                    2 * p.n_int_fixed * k - 1, k);
+      cap = p.n_int_fixed;
+    }
+    if (P % 2 || P > kMaxFftSize)
+      return fail(c, TFDP_ERR_UNSUPPORTED, "FFT size %d unsupported (even, <= %d)", P, kMaxFftSize);
+    {
+      int r = P;
+      while (r % 2 == 0) r /= 2;
+      while (r % 3 == 0) r /= 3;
+      while (r % 5 == 0) r /= 5;
+      if (r != 1) return fail(c, TFDP_ERR_UNSUPPORTED, "FFT size %d must be 2^a 3^b 5^c", P);
     }
     c->P_of_k[k] = P;
-    if (p.k == 0 || p.k == k) Pmax = std::max<int64_t>(Pmax, P);
+    c->cap_of_k[k] = cap;
+    if (k_used(c, k)) mcap = std::max(mcap, cap * k);
   }
-  if (Pmax > c->P_alloc) {
-    free_fft_buffers(c);
-    const size_t pp = (size_t)Pmax * Pmax;
-    const size_t pc = (size_t)Pmax * (Pmax / 2 + 1);
-    CUDA_TRY(c, cudaMalloc(&c->grid, 3 * pp * sizeof(float)));
-    CUDA_TRY(c, cudaMalloc(&c->phi, 3 * pp * sizeof(float)));
-    CUDA_TRY(c, cudaMalloc(&c->kreal, pp * sizeof(float)));
-    CUDA_TRY(c, cudaMalloc(&c->khat, pc * sizeof(float2)));
-    CUDA_TRY(c, cudaMalloc(&c->chat, 3 * pc * sizeof(float2)));
-    c->P_alloc = Pmax;
-    c->grid_pitch = 0;  // fresh buffers: padding must be zeroed before first use
+  c->nint_cap = need;
+  const int cpitch = mcap;
+  const int capitch = (mcap + 1) & ~1;
+  int64_t planes = 3LL * cpitch * cpitch, ca = 0, ka = 0;
+  for (int k = 1; k <= 3; ++k) {
+    if (!k_used(c, k)) continue;
+    ca = std::max<int64_t>(ca, 3LL * (c->P_of_k[k] / 2 + 1) * capitch);
+    ka = std::max<int64_t>(ka, (int64_t)(c->P_of_k[k] / 2 + 1) * cpitch);
   }
+  if (planes > c->alloc_planes || ca > c->alloc_ca || ka > c->alloc_ka) {
+    cudaStreamSynchronize(c->stream);
+    cudaFree(c->grid);
+    cudaFree(c->phi);
+    cudaFree(c->ca);
+    cudaFree(c->ka);
+    c->grid = c->phi = c->ka = nullptr;
+    c->ca = nullptr;
+    CUDA_TRY(c, cudaMalloc(&c->grid, planes * sizeof(float)));
+    CUDA_TRY(c, cudaMalloc(&c->phi, planes * sizeof(float)));
+    CUDA_TRY(c, cudaMalloc(&c->ca, ca * sizeof(float2)));
+    CUDA_TRY(c, cudaMalloc(&c->ka, ka * sizeof(float)));
+    c->alloc_planes = planes;
+    c->alloc_ca = ca;
+    c->alloc_ka = ka;
+  }
+  c->cpitch = cpitch;
+  c->ca_pitch = capitch;
+  int Pmax = 0;
+  for (int k = 1; k <= 3; ++k) {
+    if (!k_used(c, k)) continue;
+    const int P = c->P_of_k[k];
+    Pmax = std::max(Pmax, P);
+    if (c->tw_P[k] != P) {
+      cudaFree(c->tw[k]);
+      c->tw[k] = nullptr;
+      CUDA_TRY(c, cudaMalloc(&c->tw[k], (size_t)P * sizeof(float2)));
+      tfdp::launch_twiddles(c->tw[k], P, c->stream);
+      c->tw_P[k] = P;
+    }
+  }
+  CUDA_TRY(c, tfdp::fftconv_prepare(Pmax));
+  CUDA_TRY(c, cudaGetLastError());
   return TFDP_OK;
 }
 
@@ -464,32 +472,21 @@ tfdp_status evaluate(tfdp_ctx* c, int update, float eta, int k) {
     }
   } else {
     const int P = c->P_of_k[k];
-    FftPlan* fp = nullptr;
-    TRY(plan_for(c, P, &fp));
+    const int mcap = c->cap_of_k[k] * k;
+    const float2* tw = c->tw[k];
     if (!c->box_valid || c->world > 1) {
-      {
-        Scope sc(c, K_BBOX);
-        tfdp::launch_reset_keys(c->keys, c->stream);
-        tfdp::launch_bbox(xy, c->n, c->keys, c->stream);
-      }
+      Scope sc(c, K_BBOX);
+      tfdp::launch_reset_keys(c->keys, c->stream);
+      tfdp::launch_bbox(xy, c->n, c->keys, c->stream);
     }
     {
       Scope sc(c, K_SETUP);
       tfdp::launch_setup(c->keys, c->geom, k, c->p.n_int_min, c->p.n_int_fixed, c->cap_of_k[k],
-                         P, c->capped, c->stream);
+                         P, c->cpitch, c->capped, c->stream);
     }
     {
       Scope sc(c, K_ZERO);
-      if (c->grid_pitch != P) {
-        // New buffers, or k changed the FFT size: charges written under the old row pitch
-        // can sit anywhere in the padding, so clear all planes once.  Afterwards only the
-        // M_cap x M_cap corner is ever written, and only that corner is cleared per call.
-        CUDA_TRY(c, cudaMemsetAsync(c->grid, 0, (size_t)3 * c->P_alloc * c->P_alloc * sizeof(float),
-                                    c->stream));
-        c->grid_pitch = P;
-      } else {
-        tfdp::launch_zero_grid(c->grid, P, std::min(c->cap_of_k[k] * k, P), c->stream);
-      }
+      tfdp::launch_zero_planes(c->geom, c->grid, c->cpitch, mcap, c->stream);
     }
     const bool allreduce = c->world > 1 && c->p.dist_mode == TFDP_DIST_GRID_ALLREDUCE;
     {
@@ -503,28 +500,30 @@ tfdp_status evaluate(tfdp_ctx* c, int update, float eta, int k) {
       if (!c->comm)
         return fail(c, TFDP_ERR_UNSUPPORTED, "grid all-reduce needs an NCCL communicator");
       Scope sc(c, K_COMM);
-      NCCL_TRY(c, c->nccl->AllReduce(c->grid, c->grid, (size_t)3 * P * P, ncclFloat, ncclSum,
-                                     c->comm, c->stream));
+      // rows [0, M_cap) of each plane (the charges live in [0, M) x [0, M))
+      NCCL_TRY(c, c->nccl->GroupStart());
+      for (int ch = 0; ch < 3; ++ch) {
+        float* pl = c->grid + (size_t)ch * c->cpitch * c->cpitch;
+        NCCL_TRY(c, c->nccl->AllReduce(pl, pl, (size_t)mcap * c->cpitch, ncclFloat, ncclSum,
+                                       c->comm, c->stream));
+      }
+      NCCL_TRY(c, c->nccl->GroupEnd());
     }
     {
-      Scope sc(c, K_KGRID);
-      tfdp::launch_kgrid(c->geom, P, c->fa, c->kreal, c->stream);
+      Scope sc(c, K_KSPEC);
+      tfdp::launch_kspec_rows(c->geom, P, mcap, c->fa, tw, c->ka, c->cpitch, c->stream);
     }
     {
-      Scope sc(c, K_FFT_K);
-      CUFFT_TRY(c, cufftExecR2C(fp->r2c1, c->kreal, reinterpret_cast<cufftComplex*>(c->khat)));
+      Scope sc(c, K_ROWS_FWD);
+      tfdp::launch_rows_fwd(c->geom, c->grid, c->cpitch, P, mcap, tw, c->ca, c->ca_pitch, c->stream);
     }
     {
-      Scope sc(c, K_FFT_FWD);
-      CUFFT_TRY(c, cufftExecR2C(fp->r2c3, c->grid, reinterpret_cast<cufftComplex*>(c->chat)));
+      Scope sc(c, K_COLS);
+      tfdp::launch_cols(c->geom, c->ca, c->ca_pitch, c->ka, c->cpitch, P, tw, c->stream);
     }
     {
-      Scope sc(c, K_MULT);
-      tfdp::launch_mult(c->chat, c->khat, P, c->stream);
-    }
-    {
-      Scope sc(c, K_FFT_INV);
-      CUFFT_TRY(c, cufftExecC2R(fp->c2r3, reinterpret_cast<cufftComplex*>(c->chat), c->phi));
+      Scope sc(c, K_ROWS_INV);
+      tfdp::launch_rows_inv(c->geom, c->ca, c->ca_pitch, P, mcap, tw, c->phi, c->cpitch, c->stream);
     }
     {
       Scope sc(c, K_GATHER_UPDATE);
@@ -549,12 +548,16 @@ int k_at(const tfdp_ctx* c, int t) {
   return c->ksched[std::min(std::max(t, 0), T - 1)];
 }
 
-// Reads the divergence word and the grid-cap flag (the only host sync of a step call).
+// Reads the divergence word, the grid-cap flag and the last grid geometry (the only host
+// sync of a step call).
 tfdp_status check_status(tfdp_ctx* c, bool* capped) {
   CUDA_TRY(c, cudaMemcpyAsync(c->h_status, c->diverge, sizeof(unsigned long long),
                               cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaMemcpyAsync(c->h_status + 1, c->capped, sizeof(int), cudaMemcpyDeviceToHost,
                               c->stream));
+  if (c->p.solver == TFDP_IBFFT)
+    CUDA_TRY(c, cudaMemcpyAsync(c->h_status + 2, c->geom, sizeof(GridGeom), cudaMemcpyDeviceToHost,
+                                c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   const unsigned long long d = c->h_status[0];
   *capped = (int)(c->h_status[1] & 0xffffffffu) != 0;
@@ -566,10 +569,22 @@ tfdp_status check_status(tfdp_ctx* c, bool* capped) {
   return TFDP_OK;
 }
 
-tfdp_status replan_after_cap(tfdp_ctx* c) {
-  // The rule wanted more intervals than the grid holds: warn, re-size from the current box.
-  c->warnings |= TFDP_WARN_NINT_CAPPED;
-  CUDA_TRY(c, cudaMemsetAsync(c->capped, 0, sizeof(int), c->stream));
+// Re-sizes the grid when an iteration ran capped, or when the last N_int came within 4
+// intervals of the cap (so the next block of iterations does not run capped).
+tfdp_status maybe_replan(tfdp_ctx* c, bool capped) {
+  if (c->p.solver != TFDP_IBFFT) return TFDP_OK;
+  if (capped) {
+    c->warnings |= TFDP_WARN_NINT_CAPPED;
+    CUDA_TRY(c, cudaMemsetAsync(c->capped, 0, sizeof(int), c->stream));
+  }
+  if (c->p.n_int_fixed > 0) return TFDP_OK;
+  GridGeom last;
+  memcpy(&last, c->h_status + 2, sizeof last);
+  int mincap = INT32_MAX;
+  for (int k = 1; k <= 3; ++k)
+    if (k_used(c, k)) mincap = std::min(mincap, c->cap_of_k[k]);
+  if (!capped && last.n_int + 4 <= mincap) return TFDP_OK;
+  if (!capped && c->P_of_k[3] >= kMaxFftSize) return TFDP_OK;  // already at the largest grid
   tfdp::launch_reset_keys(c->keys, c->stream);
   tfdp::launch_bbox(c->xy[c->cur], c->n, c->keys, c->stream);
   c->launches += 2;
@@ -583,7 +598,7 @@ tfdp_status replan_after_cap(tfdp_ctx* c) {
     return f;
   };
   const float L = std::max(k2f(hk.maxx) - k2f(hk.minx), k2f(hk.maxy) - k2f(hk.miny));
-  c->box_valid = true;
+  c->box_valid = c->world == 1;
   return configure_fft(c, L);
 }
 
@@ -741,7 +756,8 @@ tfdp_status tfdp_init(tfdp_ctx** out, int64_t n, const int64_t* row_ptr, const i
   ALLOC(c->capped, sizeof(int));
   ALLOC(c->keys, sizeof(BoxKeys));
   ALLOC(c->geom, sizeof(GridGeom));
-  if (cudaMallocHost((void**)&c->h_status, 2 * sizeof(unsigned long long)) != cudaSuccess)
+  if (cudaMallocHost((void**)&c->h_status, 2 * sizeof(unsigned long long) + sizeof(GridGeom)) !=
+      cudaSuccess)
     return bail(fail(c, TFDP_ERR_OOM, "cudaMallocHost failed"));
   if (p.solver == TFDP_EXACT) {
     // source chunks depend on n only (bitwise-identical results for any shard count, R15)
@@ -820,7 +836,7 @@ tfdp_status tfdp_step(tfdp_ctx* c, int32_t n_iters) {
     done += block;
     bool capped = false;
     TRY(check_status(c, &capped));
-    if (capped && c->p.solver == TFDP_IBFFT) TRY(replan_after_cap(c));
+    TRY(maybe_replan(c, capped));
   }
   return TFDP_OK;
 }
@@ -847,10 +863,8 @@ tfdp_status tfdp_forces(tfdp_ctx* c, float* rep_xy, float* att_xy) {
   }
   bool capped = false;
   TRY(check_status(c, &capped));
-  if (capped && c->p.solver == TFDP_IBFFT) {
-    TRY(replan_after_cap(c));
-    c->box_valid = false;
-  }
+  TRY(maybe_replan(c, capped));
+  c->box_valid = false;
   (void)host_out;
   return TFDP_OK;
 }
@@ -975,11 +989,6 @@ void tfdp_destroy(tfdp_ctx* c) {
     cudaEventDestroy(q.b);
   }
   for (auto e : c->ev_pool) cudaEventDestroy(e);
-  for (auto& kv : c->plans) {
-    cufftDestroy(kv.second.r2c3);
-    cufftDestroy(kv.second.r2c1);
-    cufftDestroy(kv.second.c2r3);
-  }
   free_fft_buffers(c);
   cudaFree(c->xy[0]);
   cudaFree(c->xy[1]);

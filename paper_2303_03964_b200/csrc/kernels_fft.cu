@@ -1,14 +1,11 @@
 // ibFFT path kernels — sm_100a.
 //   bbox          exact fp32 min/max of the positions (ordered-uint atomics)
 //   setup         box -> (lo, L, N_int, w, h, centre) on the device, no host sync (R5/R6/R19)
-//   zero_grid     clears the M_cap x M_cap corner of the 3 zero-padded P x P charge planes
 //   spread        step 1: Lagrange charges {1, x~, y~} onto the k x k nodes of each
 //                 node's own interval; fp32 atomics into L2
-//   kgrid         kernel samples K(h da, h db) / P^2 on the circulant embedding (R9)
-//   mult          step 2 in frequency space: C^_v *= K^ (K real and even => K^ real)
 //   gather_update step 3 + assemble + attraction + update,
 //                 fused bbox of the new positions for the next iteration
-// The FFTs themselves are cuFFT R2C/C2R (library call).
+// The grid convolution (step 2) is kernels_fftconv.cu.
 #include <algorithm>
 
 #include "device_math.cuh"
@@ -61,7 +58,7 @@ void launch_bbox(const float2* xy, int64_t n, BoxKeys* keys, cudaStream_t s) {
 
 // ------------------------------------------------------------------ setup
 __global__ void setup_kernel(BoxKeys* keys, GridGeom* geom, int k, int n_int_min,
-                             int n_int_fixed, int n_int_cap, int P, int* capped_flag) {
+                             int n_int_fixed, int n_int_cap, int P, int pitch, int* capped_flag) {
   const float mnx = key2f(keys->minx), mny = key2f(keys->miny);
   const float mxx = key2f(keys->maxx), mxy = key2f(keys->maxy);
   // R6: bounding square anchored at (min x, min y), side L = max(span_x, span_y) (fp32, R19)
@@ -102,7 +99,7 @@ __global__ void setup_kernel(BoxKeys* keys, GridGeom* geom, int k, int n_int_min
   g.M = nint * k;
   g.P = P;
   g.capped = capped;
-  g.pad = 0;
+  g.pitch = pitch;
   *geom = g;
   if (capped) atomicOr(capped_flag, 1);
   // consumed: reset for the bbox fused into this iteration's update
@@ -111,22 +108,9 @@ __global__ void setup_kernel(BoxKeys* keys, GridGeom* geom, int k, int n_int_min
 }
 
 void launch_setup(BoxKeys* keys, GridGeom* geom, int k, int n_int_min, int n_int_fixed,
-                  int n_int_cap, int P, int* capped_flag, cudaStream_t s) {
-  setup_kernel<<<1, 1, 0, s>>>(keys, geom, k, n_int_min, n_int_fixed, n_int_cap, P, capped_flag);
-}
-
-// ------------------------------------------------------------------ zero
-__global__ void zero_grid_kernel(float* __restrict__ grid, int P, int Mcap) {
-  // rows [0, Mcap) x columns [0, Mcap) of each of the 3 planes (blockIdx.z)
-  float* base = grid + ((int64_t)blockIdx.z * P + blockIdx.y) * P;
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < Mcap; c += gridDim.x * blockDim.x)
-    base[c] = 0.0f;
-}
-
-void launch_zero_grid(float* grid, int P, int Mcap, cudaStream_t s) {
-  const int threads = 256;
-  dim3 g((unsigned)max(1, min(8, (Mcap + threads - 1) / threads)), (unsigned)Mcap, 3);
-  zero_grid_kernel<<<g, threads, 0, s>>>(grid, P, Mcap);
+                  int n_int_cap, int P, int pitch, int* capped_flag, cudaStream_t s) {
+  setup_kernel<<<1, 1, 0, s>>>(keys, geom, k, n_int_min, n_int_fixed, n_int_cap, P, pitch,
+                               capped_flag);
 }
 
 // ------------------------------------------------------------------ interval coords
@@ -162,10 +146,10 @@ spread_kernel(const float2* __restrict__ xy, int64_t lo, int64_t cnt,
   lagrange<K>(c.ux, lx);
   lagrange<K>(c.uy, ly);
   const float xt = p.x - g.cx, yt = p.y - g.cy;  // box-centred channels (R11)
-  const int64_t plane = (int64_t)g.P * g.P;
+  const int64_t plane = (int64_t)g.pitch * g.pitch;
 #pragma unroll
   for (int b = 0; b < K; ++b) {
-    const int64_t row = (int64_t)(c.by * K + b) * g.P;
+    const int64_t row = (int64_t)(c.by * K + b) * g.pitch;
 #pragma unroll
     for (int a = 0; a < K; ++a) {
       const int64_t idx = row + c.bx * K + a;
@@ -184,62 +168,6 @@ void launch_spread(const float2* xy, int64_t lo, int64_t cnt, const GridGeom* ge
   if (k == 1) spread_kernel<1><<<blocks, kNodeThreads, 0, s>>>(xy, lo, cnt, geom, grid);
   else if (k == 2) spread_kernel<2><<<blocks, kNodeThreads, 0, s>>>(xy, lo, cnt, geom, grid);
   else spread_kernel<3><<<blocks, kNodeThreads, 0, s>>>(xy, lo, cnt, geom, grid);
-}
-
-// ------------------------------------------------------------------ kernel grid
-template <int G>
-__global__ void __launch_bounds__(256)
-kgrid_kernel(const GridGeom* __restrict__ geom, int P, float neg_gamma, float* __restrict__ kreal) {
-  const int i1 = blockIdx.x * blockDim.x + threadIdx.x;  // x offset index
-  const int i0 = blockIdx.y;                             // y offset index
-  if (i1 >= P) return;
-  const GridGeom g = *geom;
-  const int M = g.M;
-  // circulant embedding of the offsets -(M-1)..(M-1) (linear convolution, R9)
-  const int dx = (i1 <= M - 1) ? i1 : ((i1 >= P - (M - 1)) ? i1 - P : INT32_MAX);
-  const int dy = (i0 <= M - 1) ? i0 : ((i0 >= P - (M - 1)) ? i0 - P : INT32_MAX);
-  float v = 0.0f;
-  if (dx != INT32_MAX && dy != INT32_MAX) {
-    const float d2 = (float)(dx * dx + dy * dy);  // exact integer < 2^24
-    const float s = fmaf(g.h * g.h, d2, 1.0f);
-    v = pow_neg<G>(s, neg_gamma) * (1.0f / ((float)P * (float)P));  // 1/P^2 of the C2R
-  }
-  kreal[(int64_t)i0 * P + i1] = v;
-}
-
-void launch_kgrid(const GridGeom* geom, int P, ForceArgs fa, float* kreal, cudaStream_t s) {
-  dim3 grid((unsigned)((P + 255) / 256), (unsigned)P);
-  const float ng = -fa.gamma;
-  switch (fa.gamma_int) {
-    case 1: kgrid_kernel<1><<<grid, 256, 0, s>>>(geom, P, ng, kreal); break;
-    case 2: kgrid_kernel<2><<<grid, 256, 0, s>>>(geom, P, ng, kreal); break;
-    case 3: kgrid_kernel<3><<<grid, 256, 0, s>>>(geom, P, ng, kreal); break;
-    case 4: kgrid_kernel<4><<<grid, 256, 0, s>>>(geom, P, ng, kreal); break;
-    case 8: kgrid_kernel<8><<<grid, 256, 0, s>>>(geom, P, ng, kreal); break;
-    default: kgrid_kernel<0><<<grid, 256, 0, s>>>(geom, P, ng, kreal); break;
-  }
-}
-
-// ------------------------------------------------------------------ spectral multiply
-__global__ void __launch_bounds__(256)
-mult_kernel(float2* __restrict__ chat, const float2* __restrict__ khat, int64_t ncplx) {
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < ncplx;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const float kr = khat[e].x;  // K even in both axes => K^ real (imaginary part = rounding)
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      float2 v = chat[c * ncplx + e];
-      v.x *= kr;
-      v.y *= kr;
-      chat[c * ncplx + e] = v;
-    }
-  }
-}
-
-void launch_mult(float2* chat, const float2* khat, int P, cudaStream_t s) {
-  const int64_t ncplx = (int64_t)P * (P / 2 + 1);
-  const int blocks = (int)std::min<int64_t>((ncplx + 255) / 256, 148 * 16);
-  mult_kernel<<<blocks, 256, 0, s>>>(chat, khat, ncplx);
 }
 
 // ------------------------------------------------------------------ gather + update
@@ -262,11 +190,11 @@ gather_update_kernel(const float2* __restrict__ xy, float2* __restrict__ xy_next
     float lx[K], ly[K];
     lagrange<K>(c.ux, lx);
     lagrange<K>(c.uy, ly);
-    const int64_t plane = (int64_t)g.P * g.P;
+    const int64_t plane = (int64_t)g.pitch * g.pitch;
     float psi0 = 0.f, psi1 = 0.f, psi2 = 0.f;
 #pragma unroll
     for (int b = 0; b < K; ++b) {
-      const int64_t row = (int64_t)(c.by * K + b) * g.P;
+      const int64_t row = (int64_t)(c.by * K + b) * g.pitch;
 #pragma unroll
       for (int a = 0; a < K; ++a) {
         const int64_t idx = row + c.bx * K + a;

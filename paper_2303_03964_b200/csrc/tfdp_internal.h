@@ -25,7 +25,7 @@ struct GridGeom {
   int M;             // grid points per axis = n_int * k
   int P;             // FFT size (>= 2M - 1, R9)
   int capped;        // 1 if n_int was clamped to the allocated grid (warning)
-  int pad;
+  int pitch;         // row pitch (floats) of the compact charge / potential planes
 };
 
 // Box as order-preserving uint keys so atomicMin/atomicMax give the exact fp32 min/max.
@@ -54,12 +54,22 @@ void launch_exact_finish(const float2* xy, float2* xy_next, int64_t lo, int64_t 
 // ibFFT path
 void launch_bbox(const float2* xy, int64_t n, BoxKeys* keys, cudaStream_t s);
 void launch_setup(BoxKeys* keys, GridGeom* geom, int k, int n_int_min, int n_int_fixed,
-                  int n_int_cap, int P, int* capped_flag, cudaStream_t s);
-void launch_zero_grid(float* grid, int P, int Mcap, cudaStream_t s);
+                  int n_int_cap, int P, int pitch, int* capped_flag, cudaStream_t s);
 void launch_spread(const float2* xy, int64_t lo, int64_t cnt, const GridGeom* geom, int k,
                    float* grid, cudaStream_t s);
-void launch_kgrid(const GridGeom* geom, int P, ForceArgs fa, float* kreal, cudaStream_t s);
-void launch_mult(float2* chat, const float2* khat, int P, cudaStream_t s);
+
+// hand-written FFT convolution (kernels_fftconv.cu)
+cudaError_t fftconv_prepare(int P);
+void launch_twiddles(float2* tw, int P, cudaStream_t s);
+void launch_zero_planes(const GridGeom* geom, float* C, int cpitch, int Mcap, cudaStream_t s);
+void launch_kspec_rows(const GridGeom* geom, int P, int Mcap, ForceArgs fa, const float2* tw,
+                       float* KA, int ka_pitch, cudaStream_t s);
+void launch_rows_fwd(const GridGeom* geom, const float* C, int cpitch, int P, int Mcap,
+                     const float2* tw, float2* CA, int ca_pitch, cudaStream_t s);
+void launch_cols(const GridGeom* geom, float2* CA, int ca_pitch, const float* KA, int ka_pitch,
+                 int P, const float2* tw, cudaStream_t s);
+void launch_rows_inv(const GridGeom* geom, const float2* CA, int ca_pitch, int P, int Mcap,
+                     const float2* tw, float* Phi, int cpitch, cudaStream_t s);
 void launch_gather_update(const float2* xy, float2* xy_next, int64_t lo, int64_t n_local,
                           const GridGeom* geom, int k, const float* phi,
                           const int64_t* row_ptr, const int32_t* col, ForceArgs fa,
