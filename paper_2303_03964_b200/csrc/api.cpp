@@ -72,7 +72,9 @@ struct tfdp_ctx {
   unsigned long long* diverge = nullptr;
   int* capped = nullptr;
   unsigned long long* h_status = nullptr;  // pinned [2 + sizeof(GridGeom)/8]
-  BoxKeys* keys = nullptr;
+  BoxKeys* keys = nullptr;      // reduced box of the last geometry setup
+  BoxKeys* box_part = nullptr;  // per-block partial boxes (bbox / fused update epilogue)
+  int n_part = 0;               // partials written by the last producer
   GridGeom* geom = nullptr;
   bool box_valid = false;
   // ibFFT
@@ -476,12 +478,12 @@ tfdp_status evaluate(tfdp_ctx* c, int update, float eta, int k) {
     const float2* tw = c->tw[k];
     if (!c->box_valid || c->world > 1) {
       Scope sc(c, K_BBOX);
-      tfdp::launch_reset_keys(c->keys, c->stream);
-      tfdp::launch_bbox(xy, c->n, c->keys, c->stream);
+      c->n_part = tfdp::launch_bbox(xy, c->n, c->box_part, c->stream);
     }
     {
       Scope sc(c, K_SETUP);
-      tfdp::launch_setup(c->keys, c->geom, k, c->p.n_int_min, c->p.n_int_fixed, c->cap_of_k[k],
+      tfdp::launch_setup(c->box_part, c->n_part, c->keys, c->geom, k, c->p.n_int_min,
+                         c->p.n_int_fixed, c->cap_of_k[k],
                          P, c->cpitch, c->capped, c->stream);
     }
     {
@@ -527,7 +529,8 @@ tfdp_status evaluate(tfdp_ctx* c, int update, float eta, int k) {
     }
     {
       Scope sc(c, K_GATHER_UPDATE);
-      BoxKeys* nk = (update && c->world == 1) ? c->keys : nullptr;
+      BoxKeys* nk = (update && c->world == 1) ? c->box_part : nullptr;
+      if (nk) c->n_part = (int)((n_local + tfdp::kNodeThreads - 1) / tfdp::kNodeThreads);
       tfdp::launch_gather_update(xy, xyn, c->lo, n_local, c->geom, k, c->phi, c->row_ptr, c->col,
                                  c->fa, eta, c->t, update, c->rep, c->att, c->diverge, nk,
                                  c->stream);
@@ -585,8 +588,8 @@ tfdp_status maybe_replan(tfdp_ctx* c, bool capped) {
     if (k_used(c, k)) mincap = std::min(mincap, c->cap_of_k[k]);
   if (!capped && last.n_int + 4 <= mincap) return TFDP_OK;
   if (!capped && c->P_of_k[3] >= kMaxFftSize) return TFDP_OK;  // already at the largest grid
-  tfdp::launch_reset_keys(c->keys, c->stream);
-  tfdp::launch_bbox(c->xy[c->cur], c->n, c->keys, c->stream);
+  c->n_part = tfdp::launch_bbox(c->xy[c->cur], c->n, c->box_part, c->stream);
+  tfdp::launch_box_reduce(c->box_part, c->n_part, c->keys, c->stream);
   c->launches += 2;
   BoxKeys hk;
   CUDA_TRY(c, cudaMemcpyAsync(&hk, c->keys, sizeof hk, cudaMemcpyDeviceToHost, c->stream));
@@ -755,6 +758,9 @@ tfdp_status tfdp_init(tfdp_ctx** out, int64_t n, const int64_t* row_ptr, const i
   ALLOC(c->diverge, sizeof(unsigned long long));
   ALLOC(c->capped, sizeof(int));
   ALLOC(c->keys, sizeof(BoxKeys));
+  ALLOC(c->box_part, std::max<int64_t>(tfdp::bbox_blocks(n),
+                                       (n_local + tfdp::kNodeThreads - 1) / tfdp::kNodeThreads) *
+                         sizeof(BoxKeys));
   ALLOC(c->geom, sizeof(GridGeom));
   if (cudaMallocHost((void**)&c->h_status, 2 * sizeof(unsigned long long) + sizeof(GridGeom)) !=
       cudaSuccess)
@@ -780,8 +786,8 @@ tfdp_status tfdp_init(tfdp_ctx** out, int64_t n, const int64_t* row_ptr, const i
     return bail(fail(c, TFDP_ERR_CUDA, "initial copies failed: %s", cudaGetErrorString(cudaGetLastError())));
   if (p.solver == TFDP_IBFFT) {
     if (xy_dev) {  // box of a device layout: one bbox pass
-      tfdp::launch_reset_keys(c->keys, s);
-      tfdp::launch_bbox(c->xy[0], n, c->keys, s);
+      c->n_part = tfdp::launch_bbox(c->xy[0], n, c->box_part, s);
+      tfdp::launch_box_reduce(c->box_part, c->n_part, c->keys, s);
       BoxKeys hk;
       cudaMemcpyAsync(&hk, c->keys, sizeof hk, cudaMemcpyDeviceToHost, s);
       cudaStreamSynchronize(s);
@@ -1000,6 +1006,7 @@ void tfdp_destroy(tfdp_ctx* c) {
   cudaFree(c->diverge);
   cudaFree(c->capped);
   cudaFree(c->keys);
+  cudaFree(c->box_part);
   cudaFree(c->geom);
   if (c->h_status) cudaFreeHost(c->h_status);
   if (c->comm && c->nccl) c->nccl->CommDestroy(c->comm);

@@ -1,5 +1,5 @@
 // ibFFT path kernels — sm_100a.
-//   bbox          exact fp32 min/max of the positions (ordered-uint atomics)
+//   bbox          exact fp32 min/max of the positions (ordered-uint keys, block partials)
 //   setup         box -> (lo, L, N_int, w, h, centre) on the device, no host sync (R5/R6/R19)
 //   spread        step 1: Lagrange charges {1, x~, y~} onto the k x k nodes of each
 //                 node's own interval; fp32 atomics into L2
@@ -14,22 +14,74 @@
 namespace tfdp {
 
 // ------------------------------------------------------------------ bbox
-__device__ __forceinline__ void box_reduce_commit(unsigned kx0, unsigned ky0, unsigned kx1,
-                                                  unsigned ky1, BoxKeys* keys) {
+// Two-level exact min/max: every block reduces its keys (warp __reduce + smem) and writes
+// one BoxKeys partial; the consumer (setup / box_reduce, one block) reduces the partials.
+// No same-address atomics (those serialise in one L2 slice).
+__device__ __forceinline__ void block_box_commit(unsigned kx0, unsigned ky0, unsigned kx1,
+                                                 unsigned ky1, BoxKeys* part) {
+  __shared__ unsigned s[4][32];
   kx0 = __reduce_min_sync(0xffffffffu, kx0);
   ky0 = __reduce_min_sync(0xffffffffu, ky0);
   kx1 = __reduce_max_sync(0xffffffffu, kx1);
   ky1 = __reduce_max_sync(0xffffffffu, ky1);
-  if ((threadIdx.x & 31) == 0) {
-    atomicMin(&keys->minx, kx0);
-    atomicMin(&keys->miny, ky0);
-    atomicMax(&keys->maxx, kx1);
-    atomicMax(&keys->maxy, ky1);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) {
+    s[0][warp] = kx0;
+    s[1][warp] = ky0;
+    s[2][warp] = kx1;
+    s[3][warp] = ky1;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = (blockDim.x + 31) >> 5;
+    const bool v = lane < nw;
+    kx0 = __reduce_min_sync(0xffffffffu, v ? s[0][lane] : 0xffffffffu);
+    ky0 = __reduce_min_sync(0xffffffffu, v ? s[1][lane] : 0xffffffffu);
+    kx1 = __reduce_max_sync(0xffffffffu, v ? s[2][lane] : 0u);
+    ky1 = __reduce_max_sync(0xffffffffu, v ? s[3][lane] : 0u);
+    if (lane == 0) part[blockIdx.x] = BoxKeys{kx0, ky0, kx1, ky1};
   }
 }
 
+// One block reduces n_part partials; result in *out (all threads return it).
+__device__ BoxKeys block_reduce_partials(const BoxKeys* __restrict__ part, int n_part) {
+  unsigned kx0 = 0xffffffffu, ky0 = 0xffffffffu, kx1 = 0u, ky1 = 0u;
+  for (int i = threadIdx.x; i < n_part; i += blockDim.x) {
+    const BoxKeys b = part[i];
+    kx0 = min(kx0, b.minx);
+    ky0 = min(ky0, b.miny);
+    kx1 = max(kx1, b.maxx);
+    ky1 = max(ky1, b.maxy);
+  }
+  __shared__ BoxKeys r[1];
+  __shared__ unsigned s[4][32];
+  kx0 = __reduce_min_sync(0xffffffffu, kx0);
+  ky0 = __reduce_min_sync(0xffffffffu, ky0);
+  kx1 = __reduce_max_sync(0xffffffffu, kx1);
+  ky1 = __reduce_max_sync(0xffffffffu, ky1);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) {
+    s[0][warp] = kx0;
+    s[1][warp] = ky0;
+    s[2][warp] = kx1;
+    s[3][warp] = ky1;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = (blockDim.x + 31) >> 5;
+    const bool v = lane < nw;
+    kx0 = __reduce_min_sync(0xffffffffu, v ? s[0][lane] : 0xffffffffu);
+    ky0 = __reduce_min_sync(0xffffffffu, v ? s[1][lane] : 0xffffffffu);
+    kx1 = __reduce_max_sync(0xffffffffu, v ? s[2][lane] : 0u);
+    ky1 = __reduce_max_sync(0xffffffffu, v ? s[3][lane] : 0u);
+    if (lane == 0) r[0] = BoxKeys{kx0, ky0, kx1, ky1};
+  }
+  __syncthreads();
+  return r[0];
+}
+
 __global__ void __launch_bounds__(kNodeThreads)
-bbox_kernel(const float2* __restrict__ xy, int64_t n, BoxKeys* keys) {
+bbox_kernel(const float2* __restrict__ xy, int64_t n, BoxKeys* part) {
   unsigned kx0 = 0xffffffffu, ky0 = 0xffffffffu, kx1 = 0u, ky1 = 0u;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -40,27 +92,37 @@ bbox_kernel(const float2* __restrict__ xy, int64_t n, BoxKeys* keys) {
     kx1 = max(kx1, a);
     ky1 = max(ky1, b);
   }
-  box_reduce_commit(kx0, ky0, kx1, ky1, keys);
+  block_box_commit(kx0, ky0, kx1, ky1, part);
 }
 
-__global__ void reset_keys_kernel(BoxKeys* keys) {
-  keys->minx = keys->miny = 0xffffffffu;
-  keys->maxx = keys->maxy = 0u;
+__global__ void __launch_bounds__(1024) box_reduce_kernel(const BoxKeys* part, int n_part, BoxKeys* keys) {
+  const BoxKeys b = block_reduce_partials(part, n_part);
+  if (threadIdx.x == 0) *keys = b;
 }
 
-void launch_reset_keys(BoxKeys* keys, cudaStream_t s) { reset_keys_kernel<<<1, 1, 0, s>>>(keys); }
+int bbox_blocks(int64_t n) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>((n + kNodeThreads - 1) / kNodeThreads, 148 * 8));
+}
 
-void launch_bbox(const float2* xy, int64_t n, BoxKeys* keys, cudaStream_t s) {
-  int blocks = (int)std::min<int64_t>((n + kNodeThreads - 1) / kNodeThreads, 148 * 8);
-  if (blocks < 1) blocks = 1;
-  bbox_kernel<<<blocks, kNodeThreads, 0, s>>>(xy, n, keys);
+int launch_bbox(const float2* xy, int64_t n, BoxKeys* part, cudaStream_t s) {
+  const int blocks = bbox_blocks(n);
+  bbox_kernel<<<blocks, kNodeThreads, 0, s>>>(xy, n, part);
+  return blocks;
+}
+
+void launch_box_reduce(const BoxKeys* part, int n_part, BoxKeys* keys, cudaStream_t s) {
+  box_reduce_kernel<<<1, 1024, 0, s>>>(part, n_part, keys);
 }
 
 // ------------------------------------------------------------------ setup
-__global__ void setup_kernel(BoxKeys* keys, GridGeom* geom, int k, int n_int_min,
-                             int n_int_fixed, int n_int_cap, int P, int pitch, int* capped_flag) {
-  const float mnx = key2f(keys->minx), mny = key2f(keys->miny);
-  const float mxx = key2f(keys->maxx), mxy = key2f(keys->maxy);
+__global__ void __launch_bounds__(1024)
+setup_kernel(const BoxKeys* part, int n_part, BoxKeys* keys, GridGeom* geom, int k,
+             int n_int_min, int n_int_fixed, int n_int_cap, int P, int pitch, int* capped_flag) {
+  const BoxKeys kb = block_reduce_partials(part, n_part);
+  if (threadIdx.x != 0) return;
+  *keys = kb;
+  const float mnx = key2f(kb.minx), mny = key2f(kb.miny);
+  const float mxx = key2f(kb.maxx), mxy = key2f(kb.maxy);
   // R6: bounding square anchored at (min x, min y), side L = max(span_x, span_y) (fp32, R19)
   float L = fmaxf(__fsub_rn(mxx, mnx), __fsub_rn(mxy, mny));
   float lox = mnx, loy = mny;
@@ -102,15 +164,13 @@ __global__ void setup_kernel(BoxKeys* keys, GridGeom* geom, int k, int n_int_min
   g.pitch = pitch;
   *geom = g;
   if (capped) atomicOr(capped_flag, 1);
-  // consumed: reset for the bbox fused into this iteration's update
-  keys->minx = keys->miny = 0xffffffffu;
-  keys->maxx = keys->maxy = 0u;
 }
 
-void launch_setup(BoxKeys* keys, GridGeom* geom, int k, int n_int_min, int n_int_fixed,
-                  int n_int_cap, int P, int pitch, int* capped_flag, cudaStream_t s) {
-  setup_kernel<<<1, 1, 0, s>>>(keys, geom, k, n_int_min, n_int_fixed, n_int_cap, P, pitch,
-                               capped_flag);
+void launch_setup(const BoxKeys* part, int n_part, BoxKeys* keys, GridGeom* geom, int k,
+                  int n_int_min, int n_int_fixed, int n_int_cap, int P, int pitch,
+                  int* capped_flag, cudaStream_t s) {
+  setup_kernel<<<1, 1024, 0, s>>>(part, n_part, keys, geom, k, n_int_min, n_int_fixed, n_int_cap,
+                                  P, pitch, capped_flag);
 }
 
 // ------------------------------------------------------------------ interval coords
@@ -178,7 +238,7 @@ gather_update_kernel(const float2* __restrict__ xy, float2* __restrict__ xy_next
                      const float* __restrict__ phi, const int64_t* __restrict__ row_ptr,
                      const int32_t* __restrict__ col, ForceArgs fa, float eta, int iter,
                      int update, float2* __restrict__ rep_out, float2* __restrict__ att_out,
-                     unsigned long long* diverge, BoxKeys* next_keys) {
+                     unsigned long long* diverge, BoxKeys* next_part) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool active = t < n_local;
   unsigned kx0 = 0xffffffffu, ky0 = 0xffffffffu, kx1 = 0u, ky1 = 0u;
@@ -235,21 +295,21 @@ gather_update_kernel(const float2* __restrict__ xy, float2* __restrict__ xy_next
       if (att_out) att_out[t] = make_float2(ax, ay);
     }
   }
-  if (update && next_keys) box_reduce_commit(kx0, ky0, kx1, ky1, next_keys);
+  if (update && next_part) block_box_commit(kx0, ky0, kx1, ky1, next_part);
 }
 
 void launch_gather_update(const float2* xy, float2* xy_next, int64_t lo, int64_t n_local,
                           const GridGeom* geom, int k, const float* phi,
                           const int64_t* row_ptr, const int32_t* col, ForceArgs fa,
                           float eta, int iter, int update, float2* rep_out, float2* att_out,
-                          unsigned long long* diverge, BoxKeys* next_keys, cudaStream_t s) {
+                          unsigned long long* diverge, BoxKeys* next_part, cudaStream_t s) {
   if (n_local <= 0) return;
   const unsigned blocks = (unsigned)((n_local + kNodeThreads - 1) / kNodeThreads);
 #define TFDP_GU(KK)                                                                         \
   gather_update_kernel<KK><<<blocks, kNodeThreads, 0, s>>>(xy, xy_next, lo, n_local, geom,  \
                                                            phi, row_ptr, col, fa, eta, iter, \
                                                            update, rep_out, att_out, diverge,\
-                                                           next_keys)
+                                                           next_part)
   if (k == 1) TFDP_GU(1);
   else if (k == 2) TFDP_GU(2);
   else TFDP_GU(3);

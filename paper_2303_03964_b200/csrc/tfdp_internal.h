@@ -52,9 +52,13 @@ void launch_exact_finish(const float2* xy, float2* xy_next, int64_t lo, int64_t 
                          cudaStream_t s);
 
 // ibFFT path
-void launch_bbox(const float2* xy, int64_t n, BoxKeys* keys, cudaStream_t s);
-void launch_setup(BoxKeys* keys, GridGeom* geom, int k, int n_int_min, int n_int_fixed,
-                  int n_int_cap, int P, int pitch, int* capped_flag, cudaStream_t s);
+// Box: producers write one BoxKeys partial per block; consumers reduce them in one block.
+int bbox_blocks(int64_t n);
+int launch_bbox(const float2* xy, int64_t n, BoxKeys* part, cudaStream_t s);  // returns n_part
+void launch_box_reduce(const BoxKeys* part, int n_part, BoxKeys* keys, cudaStream_t s);
+void launch_setup(const BoxKeys* part, int n_part, BoxKeys* keys, GridGeom* geom, int k,
+                  int n_int_min, int n_int_fixed, int n_int_cap, int P, int pitch,
+                  int* capped_flag, cudaStream_t s);
 void launch_spread(const float2* xy, int64_t lo, int64_t cnt, const GridGeom* geom, int k,
                    float* grid, cudaStream_t s);
 
@@ -74,8 +78,7 @@ void launch_gather_update(const float2* xy, float2* xy_next, int64_t lo, int64_t
                           const GridGeom* geom, int k, const float* phi,
                           const int64_t* row_ptr, const int32_t* col, ForceArgs fa,
                           float eta, int iter, int update, float2* rep_out, float2* att_out,
-                          unsigned long long* diverge, BoxKeys* next_keys,
+                          unsigned long long* diverge, BoxKeys* next_part,
                           cudaStream_t s);
-void launch_reset_keys(BoxKeys* keys, cudaStream_t s);
 
 }  // namespace tfdp
