@@ -206,8 +206,8 @@ void prof_collect(tfdp_ctx* c) {
 }
 
 // ---------------------------------------------------------------- helpers
-// Largest FFT the shared-memory kernels hold (cols pass: 24 P bytes <= 227 KB).
-constexpr int kMaxFftSize = 9216;
+// Largest FFT the shared-memory kernels hold (cols pass: ~26 P bytes <= 227 KB).
+constexpr int kMaxFftSize = 8192;
 
 // Smallest even m >= target of the form 2^a 3^b 5^c with b <= 2, c <= 1 (the radices of
 // kernels_fftconv.cu, few odd stages).
@@ -425,7 +425,7 @@ tfdp_status configure_fft(tfdp_ctx* c, float L) {
     if (c->tw_P[k] != P) {
       cudaFree(c->tw[k]);
       c->tw[k] = nullptr;
-      CUDA_TRY(c, cudaMalloc(&c->tw[k], (size_t)P * sizeof(float2)));
+      CUDA_TRY(c, cudaMalloc(&c->tw[k], (size_t)(P + 128) * sizeof(float2)));  // >= tw_len
       tfdp::launch_twiddles(c->tw[k], P, c->stream);
       c->tw_P[k] = P;
     }

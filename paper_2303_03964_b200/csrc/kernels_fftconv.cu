@@ -105,75 +105,140 @@ __device__ __forceinline__ void dft<8>(float2 (&v)[8]) {
   v[7] = csub(e[3], o3);
 }
 
-// One Stockham autosort stage (Govindaraju et al. 2008 formulation), radix R, size N,
-// current sub-transform size Ns.  tw[t] = exp(-2 pi i t / N).
+// Shared-memory layout of one FFT buffer: one float2 of padding per 8, which makes the
+// strided Stockham stores of the first stages conflict-free.
+__device__ __forceinline__ int pad(int i) { return i + (i >> 3); }
+__host__ __device__ constexpr int padded_len(int N) { return N + (N >> 3) + 1; }
+
+// Twiddle table (fp64-generated, fp32 stored), two-level so it fits in shared memory:
+// tw[0..64) = exp(-2 pi i t / N), tw[64 + u] = exp(-2 pi i 64 u / N), u = 0..N/64; then
+// exp(-2 pi i t / N) = tw[64 + (t >> 6)] * tw[t & 63]  (one complex product, ~1.5 ulp).
+__host__ __device__ constexpr int tw_len(int N) { return 64 + N / 64 + 1; }
+
+__device__ __forceinline__ float2 tw_at(const float2* __restrict__ tw, int t) {
+  return cmul(tw[64 + (t >> 6)], tw[t & 63]);
+}
+
+// Twiddles w^r, r = 1..R-1, of one butterfly: at most three table lookups (w, w^2, w^4),
+// the rest by at most two complex products.
 template <int R>
-__device__ __forceinline__ void stage(const float2* __restrict__ in, float2* __restrict__ out,
-                                      int N, int Ns, const float2* __restrict__ tw) {
-  const int nb = N / R;
-  const int step = N / (Ns * R);
-  for (int j = threadIdx.x; j < nb; j += blockDim.x) {
-    const int k = j % Ns;
-    float2 v[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) v[r] = in[j + r * nb];
-    if (Ns > 1) {
-#pragma unroll
-      for (int r = 1; r < R; ++r) v[r] = cmul(v[r], __ldg(tw + k * r * step));
-    }
-    dft<R>(v);
-    const int d = (j - k) * R + k;
-#pragma unroll
-    for (int r = 0; r < R; ++r) out[d + r * Ns] = v[r];
+__device__ __forceinline__ void twiddles(const float2* __restrict__ tw, int base, float2 (&w)[R]) {
+  w[1] = tw_at(tw, base);
+  if constexpr (R >= 3) w[2] = tw_at(tw, 2 * base);
+  if constexpr (R >= 4) w[3] = cmul(w[1], w[2]);
+  if constexpr (R == 5) w[4] = cmul(w[2], w[2]);
+  if constexpr (R == 8) {
+    w[4] = tw_at(tw, 4 * base);
+    w[5] = cmul(w[4], w[1]);
+    w[6] = cmul(w[4], w[2]);
+    w[7] = cmul(w[4], w[3]);
   }
 }
 
-// Forward complex FFT of a[0..N) (N = 2^a 3^b 5^c) in shared memory; b is scratch.
-// Returns the buffer holding the result.  Called by the whole block; ends with a barrier.
-__device__ float2* fft_smem(float2* a, float2* b, int N, const float2* __restrict__ tw) {
-  int Ns = 1;
-  while (Ns < N) {
-    const int rem = N / Ns;
-    if (rem % 8 == 0) {
-      stage<8>(a, b, N, Ns, tw);
-      Ns *= 8;
-    } else if (rem % 4 == 0) {
-      stage<4>(a, b, N, Ns, tw);
-      Ns *= 4;
-    } else if (rem % 2 == 0) {
-      stage<2>(a, b, N, Ns, tw);
-      Ns *= 2;
-    } else if (rem % 3 == 0) {
-      stage<3>(a, b, N, Ns, tw);
-      Ns *= 3;
-    } else {
-      stage<5>(a, b, N, Ns, tw);
-      Ns *= 5;
+// In-place Stockham autosort stage (Govindaraju et al. 2008 formulation), radix R, size N,
+// current sub-transform size Ns.  Every thread first loads + transforms its butterflies
+// (registers), the block synchronises, then all results are stored: one buffer instead
+// of ping-pong, so twice the FFTs fit in shared memory.  Requires blockDim.x >= N / 8.
+template <int R>
+struct PerThread { static constexpr int value = 1; };
+template <> struct PerThread<4> { static constexpr int value = 2; };
+template <> struct PerThread<2> { static constexpr int value = 4; };
+template <> struct PerThread<3> { static constexpr int value = 3; };
+template <> struct PerThread<5> { static constexpr int value = 2; };
+
+template <int R>
+__device__ __forceinline__ void stage(float2* buf, int N, int Ns, const float2* __restrict__ tw) {
+  constexpr int MB = PerThread<R>::value;  // butterflies per thread (N/R <= MB * blockDim)
+  const int nb = N / R;
+  const int step = nb / Ns;  // N / (Ns R)
+  const bool p2 = (Ns & (Ns - 1)) == 0;
+  float2 v[MB][R];
+#pragma unroll
+  for (int b = 0; b < MB; ++b) {
+    const int j = threadIdx.x + b * blockDim.x;
+    if (j < nb) {
+      const int k = p2 ? (j & (Ns - 1)) : (j % Ns);
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[b][r] = buf[pad(j + r * nb)];
+      if (Ns > 1) {
+        float2 w[R];
+        twiddles<R>(tw, k * step, w);
+#pragma unroll
+        for (int r = 1; r < R; ++r) v[b][r] = cmul(v[b][r], w[r]);
+      }
+      dft<R>(v[b]);
     }
-    __syncthreads();
-    float2* t = a;
-    a = b;
-    b = t;
   }
-  return a;
+  __syncthreads();
+#pragma unroll
+  for (int b = 0; b < MB; ++b) {
+    const int j = threadIdx.x + b * blockDim.x;
+    if (j < nb) {
+      const int k = p2 ? (j & (Ns - 1)) : (j % Ns);
+      const int d = (j - k) * R + k;
+#pragma unroll
+      for (int r = 0; r < R; ++r) buf[pad(d + r * Ns)] = v[b][r];
+    }
+  }
+  __syncthreads();
+}
+
+// Forward complex FFT of buf[0..N) (N = 2^a 3^b 5^c, padded layout) in shared memory, in
+// place.  Power-of-two stages first (radix 8, then 4 / 2), odd radices last, so Ns is a
+// power of two wherever possible.  Called by the whole block (blockDim.x >= N/8); the
+// input must be visible (barrier) before the call; ends with a barrier.
+__device__ void fft_smem(float2* buf, int N, const float2* __restrict__ tw) {
+  int Ns = 1, rem = N;
+  while (rem % 8 == 0) {
+    stage<8>(buf, N, Ns, tw);
+    Ns *= 8;
+    rem /= 8;
+  }
+  if (rem % 4 == 0) {
+    stage<4>(buf, N, Ns, tw);
+    Ns *= 4;
+    rem /= 4;
+  }
+  if (rem % 2 == 0) {
+    stage<2>(buf, N, Ns, tw);
+    Ns *= 2;
+    rem /= 2;
+  }
+  while (rem % 3 == 0) {
+    stage<3>(buf, N, Ns, tw);
+    Ns *= 3;
+    rem /= 3;
+  }
+  while (rem % 5 == 0) {
+    stage<5>(buf, N, Ns, tw);
+    Ns *= 5;
+    rem /= 5;
+  }
 }
 
 __global__ void twiddle_kernel(float2* tw, int N) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= N) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= tw_len(N)) return;
+  const int t = i < 64 ? i : 64 * (i - 64);
   double s, c;
   sincospi(2.0 * (double)t / (double)N, &s, &c);
-  tw[t] = make_float2((float)c, (float)-s);
+  tw[i] = make_float2((float)c, (float)-s);
+}
+
+// Copies the twiddle table to shared memory (caller synchronises before use).
+__device__ __forceinline__ void load_tw(float2* dst, const float2* __restrict__ src, int N) {
+  for (int i = threadIdx.x; i < tw_len(N); i += blockDim.x) dst[i] = src[i];
 }
 
 // ---------------------------------------------------------------- K spectrum rows
 template <int G>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(1024)
 kspec_rows_kernel(const GridGeom* __restrict__ geom, int P, float neg_gamma,
                   const float2* __restrict__ tw, float* __restrict__ KA, int ka_pitch) {
   extern __shared__ float2 sm[];
   float2* a = sm;
-  float2* b = sm + P;
+  float2* tws = sm + padded_len(P);
+  load_tw(tws, tw, P);
   const GridGeom g = *geom;
   const int M = g.M;
   const int dya = 2 * blockIdx.x, dyb = dya + 1;
@@ -188,25 +253,27 @@ kspec_rows_kernel(const GridGeom* __restrict__ geom, int P, float neg_gamma,
       va = pow_neg<G>(fmaf(h2, dx2 + (float)(dya * dya), 1.0f), neg_gamma) * scale;
       if (dyb < M) vb = pow_neg<G>(fmaf(h2, dx2 + (float)(dyb * dyb), 1.0f), neg_gamma) * scale;
     }
-    a[x] = make_float2(va, vb);
+    a[pad(x)] = make_float2(va, vb);
   }
   __syncthreads();
-  const float2* r = fft_smem(a, b, P, tw);
+  fft_smem(a, P, tws);
+  const float2* r = a;
   // real-even rows -> real spectra: row a in Re, row b in Im
   for (int q = threadIdx.x; q <= P / 2; q += blockDim.x) {
-    const float2 z = r[q];
+    const float2 z = r[pad(q)];
     KA[(int64_t)q * ka_pitch + dya] = z.x;
     if (dyb < M) KA[(int64_t)q * ka_pitch + dyb] = z.y;
   }
 }
 
 // ---------------------------------------------------------------- forward rows
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(1024)
 rows_fwd_kernel(const GridGeom* __restrict__ geom, const float* __restrict__ C, int cpitch,
                 int P, const float2* __restrict__ tw, float2* __restrict__ CA, int ca_pitch) {
   extern __shared__ float2 sm[];
   float2* a = sm;
-  float2* b = sm + P;
+  float2* tws = sm + padded_len(P);
+  load_tw(tws, tw, P);
   const int M = geom->M;
   const int ra = 2 * blockIdx.x, rb = ra + 1;
   if (ra >= M) return;
@@ -220,15 +287,16 @@ rows_fwd_kernel(const GridGeom* __restrict__ geom, const float* __restrict__ C, 
       va = rowa[x];
       if (hb) vb = rowb[x];
     }
-    a[x] = make_float2(va, vb);
+    a[pad(x)] = make_float2(va, vb);
   }
   __syncthreads();
-  const float2* r = fft_smem(a, b, P, tw);
+  fft_smem(a, P, tws);
+  const float2* r = a;
   const int half = P / 2;
   float2* out = CA + (int64_t)ch * (half + 1) * ca_pitch;
   for (int q = threadIdx.x; q <= half; q += blockDim.x) {
-    const float2 z = r[q];
-    const float2 zc = conjf2(r[q == 0 ? 0 : P - q]);
+    const float2 z = r[pad(q)];
+    const float2 zc = conjf2(r[pad(q == 0 ? 0 : P - q)]);
     const float2 xa = make_float2(0.5f * (z.x + zc.x), 0.5f * (z.y + zc.y));
     const float2 xb = mul_mi(make_float2(0.5f * (z.x - zc.x), 0.5f * (z.y - zc.y)));
     float2* o = out + (int64_t)q * ca_pitch + ra;
@@ -241,13 +309,14 @@ rows_fwd_kernel(const GridGeom* __restrict__ geom, const float* __restrict__ C, 
 }
 
 // ---------------------------------------------------------------- columns
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(1024)
 cols_kernel(const GridGeom* __restrict__ geom, float2* __restrict__ CA, int ca_pitch,
             const float* __restrict__ KA, int ka_pitch, int P, const float2* __restrict__ tw) {
   extern __shared__ float2 sm[];
   float2* a = sm;
-  float2* b = sm + P;
-  float* kh = reinterpret_cast<float*>(sm + 2 * P);  // [2][P]
+  float2* tws = sm + padded_len(P);
+  float* kh = reinterpret_cast<float*>(tws + tw_len(P));  // [2][P]
+  load_tw(tws, tw, P);
   const int M = geom->M;
   const int half = P / 2;
   const int q0 = 2 * blockIdx.x, q1 = q0 + 1;
@@ -260,13 +329,14 @@ cols_kernel(const GridGeom* __restrict__ geom, float2* __restrict__ CA, int ca_p
       va = KA[(int64_t)q0 * ka_pitch + dy];
       if (h1) vb = KA[(int64_t)q1 * ka_pitch + dy];
     }
-    a[u] = make_float2(va, vb);
+    a[pad(u)] = make_float2(va, vb);
   }
   __syncthreads();
   {
-    const float2* r = fft_smem(a, b, P, tw);
+    fft_smem(a, P, tws);
+  const float2* r = a;
     for (int u = threadIdx.x; u < P; u += blockDim.x) {
-      const float2 z = r[u];
+      const float2 z = r[pad(u)];
       kh[u] = z.x;
       kh[P + u] = z.y;
     }
@@ -277,21 +347,22 @@ cols_kernel(const GridGeom* __restrict__ geom, float2* __restrict__ CA, int ca_p
       const int q = s ? q1 : q0;
       if (q > half) break;
       float2* col = CA + ((int64_t)ch * (half + 1) + q) * ca_pitch;
-      for (int u = threadIdx.x; u < P; u += blockDim.x) a[u] = (u < M) ? col[u] : make_float2(0.f, 0.f);
+      for (int u = threadIdx.x; u < P; u += blockDim.x) a[pad(u)] = (u < M) ? col[u] : make_float2(0.f, 0.f);
       __syncthreads();
-      float2* r = fft_smem(a, b, P, tw);
-      float2* o = (r == a) ? b : a;
+      fft_smem(a, P, tws);
+      float2* r = a;
       // multiply by K^ (real) and conjugate for the inverse transform
       const float* k = kh + s * P;
       for (int u = threadIdx.x; u < P; u += blockDim.x) {
-        const float2 z = r[u];
+        const float2 z = r[pad(u)];
         const float kk = k[u];
-        r[u] = make_float2(z.x * kk, -z.y * kk);
+        r[pad(u)] = make_float2(z.x * kk, -z.y * kk);
       }
       __syncthreads();
-      const float2* ri = fft_smem(r, o, P, tw);
+      fft_smem(r, P, tws);
+      const float2* ri = r;
       for (int u = threadIdx.x; u < M; u += blockDim.x) {
-        const float2 z = ri[u];
+        const float2 z = ri[pad(u)];
         col[u] = make_float2(z.x, -z.y);
       }
       __syncthreads();
@@ -300,12 +371,13 @@ cols_kernel(const GridGeom* __restrict__ geom, float2* __restrict__ CA, int ca_p
 }
 
 // ---------------------------------------------------------------- inverse rows
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(1024)
 rows_inv_kernel(const GridGeom* __restrict__ geom, const float2* __restrict__ CA, int ca_pitch,
                 int P, const float2* __restrict__ tw, float* __restrict__ Phi, int cpitch) {
   extern __shared__ float2 sm[];
   float2* a = sm;
-  float2* b = sm + P;
+  float2* tws = sm + padded_len(P);
+  load_tw(tws, tw, P);
   const int M = geom->M;
   const int ra = 2 * blockIdx.x, rb = ra + 1;
   if (ra >= M) return;
@@ -331,14 +403,15 @@ rows_inv_kernel(const GridGeom* __restrict__ geom, const float2* __restrict__ CA
       xb = conjf2(xb);
     }
     const float2 z = make_float2(xa.x - xb.y, xa.y + xb.x);  // xa + i xb
-    a[q] = conjf2(z);
+    a[pad(q)] = conjf2(z);
   }
   __syncthreads();
-  const float2* r = fft_smem(a, b, P, tw);
+  fft_smem(a, P, tws);
+  const float2* r = a;
   float* pa = Phi + ((int64_t)ch * cpitch + ra) * cpitch;
   float* pb = pa + cpitch;
   for (int x = threadIdx.x; x < M; x += blockDim.x) {
-    const float2 z = r[x];  // conj(result) = xa + i xb: xa = z.x, xb = -z.y
+    const float2 z = r[pad(x)];  // conj(result) = xa + i xb: xa = z.x, xb = -z.y
     pa[x] = z.x;
     if (hb) pb[x] = -z.y;
   }
@@ -355,17 +428,20 @@ __global__ void zero_planes_kernel(const GridGeom* __restrict__ geom, float* __r
 }  // namespace
 
 void launch_twiddles(float2* tw, int P, cudaStream_t s) {
-  twiddle_kernel<<<(P + 255) / 256, 256, 0, s>>>(tw, P);
+  twiddle_kernel<<<(tw_len(P) + 255) / 256, 256, 0, s>>>(tw, P);
 }
 
 void launch_zero_planes(const GridGeom* geom, float* C, int cpitch, int Mcap, cudaStream_t s) {
   zero_planes_kernel<<<dim3((unsigned)Mcap, 3), 256, 0, s>>>(geom, C, cpitch);
 }
 
+// Threads per FFT block: >= P/8 (one radix-8 butterfly each), multiple of 32, >= 128.
+int fft_threads(int P) { return std::min(1024, std::max(128, ((P / 8) + 31) / 32 * 32)); }
+
 size_t fftconv_smem_bytes(int P, int which) {
   // which: 0 rows (2 P float2), 1 cols (2 P float2 + 2 P float)
-  return which == 0 ? (size_t)2 * P * sizeof(float2)
-                    : (size_t)2 * P * sizeof(float2) + (size_t)2 * P * sizeof(float);
+  const size_t base = (size_t)(padded_len(P) + tw_len(P)) * sizeof(float2);
+  return which == 0 ? base : base + (size_t)2 * P * sizeof(float);
 }
 
 cudaError_t fftconv_prepare(int P) {
@@ -393,30 +469,30 @@ void launch_kspec_rows(const GridGeom* geom, int P, int Mcap, ForceArgs fa, cons
   const size_t sm = fftconv_smem_bytes(P, 0);
   const float ng = -fa.gamma;
   switch (fa.gamma_int) {
-    case 1: kspec_rows_kernel<1><<<blocks, 256, sm, s>>>(geom, P, ng, tw, KA, ka_pitch); break;
-    case 2: kspec_rows_kernel<2><<<blocks, 256, sm, s>>>(geom, P, ng, tw, KA, ka_pitch); break;
-    case 3: kspec_rows_kernel<3><<<blocks, 256, sm, s>>>(geom, P, ng, tw, KA, ka_pitch); break;
-    case 4: kspec_rows_kernel<4><<<blocks, 256, sm, s>>>(geom, P, ng, tw, KA, ka_pitch); break;
-    case 8: kspec_rows_kernel<8><<<blocks, 256, sm, s>>>(geom, P, ng, tw, KA, ka_pitch); break;
-    default: kspec_rows_kernel<0><<<blocks, 256, sm, s>>>(geom, P, ng, tw, KA, ka_pitch); break;
+    case 1: kspec_rows_kernel<1><<<blocks, fft_threads(P), sm, s>>>(geom, P, ng, tw, KA, ka_pitch); break;
+    case 2: kspec_rows_kernel<2><<<blocks, fft_threads(P), sm, s>>>(geom, P, ng, tw, KA, ka_pitch); break;
+    case 3: kspec_rows_kernel<3><<<blocks, fft_threads(P), sm, s>>>(geom, P, ng, tw, KA, ka_pitch); break;
+    case 4: kspec_rows_kernel<4><<<blocks, fft_threads(P), sm, s>>>(geom, P, ng, tw, KA, ka_pitch); break;
+    case 8: kspec_rows_kernel<8><<<blocks, fft_threads(P), sm, s>>>(geom, P, ng, tw, KA, ka_pitch); break;
+    default: kspec_rows_kernel<0><<<blocks, fft_threads(P), sm, s>>>(geom, P, ng, tw, KA, ka_pitch); break;
   }
 }
 
 void launch_rows_fwd(const GridGeom* geom, const float* C, int cpitch, int P, int Mcap,
                      const float2* tw, float2* CA, int ca_pitch, cudaStream_t s) {
-  rows_fwd_kernel<<<dim3((unsigned)((Mcap + 1) / 2), 3), 256, fftconv_smem_bytes(P, 0), s>>>(
+  rows_fwd_kernel<<<dim3((unsigned)((Mcap + 1) / 2), 3), fft_threads(P), fftconv_smem_bytes(P, 0), s>>>(
       geom, C, cpitch, P, tw, CA, ca_pitch);
 }
 
 void launch_cols(const GridGeom* geom, float2* CA, int ca_pitch, const float* KA, int ka_pitch,
                  int P, const float2* tw, cudaStream_t s) {
   const unsigned blocks = (unsigned)((P / 2 + 1 + 1) / 2);
-  cols_kernel<<<blocks, 256, fftconv_smem_bytes(P, 1), s>>>(geom, CA, ca_pitch, KA, ka_pitch, P, tw);
+  cols_kernel<<<blocks, fft_threads(P), fftconv_smem_bytes(P, 1), s>>>(geom, CA, ca_pitch, KA, ka_pitch, P, tw);
 }
 
 void launch_rows_inv(const GridGeom* geom, const float2* CA, int ca_pitch, int P, int Mcap,
                      const float2* tw, float* Phi, int cpitch, cudaStream_t s) {
-  rows_inv_kernel<<<dim3((unsigned)((Mcap + 1) / 2), 3), 256, fftconv_smem_bytes(P, 0), s>>>(
+  rows_inv_kernel<<<dim3((unsigned)((Mcap + 1) / 2), 3), fft_threads(P), fftconv_smem_bytes(P, 0), s>>>(
       geom, CA, ca_pitch, P, tw, Phi, cpitch);
 }
 
