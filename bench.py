@@ -156,28 +156,15 @@ def barrier(world):
 
 
 def max_over_ranks(x: float, world: int) -> float:
-    if world == 1:
-        return x
-    import torch
-    import torch.distributed as dist
+    from paper_2303_03964_b200 import dist as D
 
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+    return D.max_over_ranks(x) if world > 1 else x
 
 
 def make_dist(rank, world, local):
-    import paper_2303_03964_b200 as P
+    from paper_2303_03964_b200 import dist as D
 
-    if world == 1:
-        return None
-    import torch
-    import torch.distributed as dist
-
-    uid = P.nccl_unique_id() if rank == 0 else bytes(128)
-    t = torch.tensor(list(uid), dtype=torch.uint8, device="cuda")
-    dist.broadcast(t, src=0)
-    return P.Dist(rank, world, local, bytes(t.cpu().tolist()))
+    return D.bootstrap(device=local) if world > 1 else None
 
 
 # ---------------------------------------------------------------------------- GPU arm
