@@ -88,6 +88,8 @@ struct tfdp_ctx {
   float* phi = nullptr;   // potentials Phi (gather source)
   float2* ca = nullptr;   // row half-spectra, transformed in place by the column pass
   float* ka = nullptr;    // kernel row spectra KA[q][dy]
+  float* kh = nullptr;    // kernel spectrum columns KH[q][u] (real)
+  int64_t alloc_kh = 0;
   float2* tw[4] = {nullptr, nullptr, nullptr, nullptr};  // twiddles per k (length P_k)
   int tw_P[4] = {0, 0, 0, 0};
   // schedule
@@ -206,14 +208,13 @@ void prof_collect(tfdp_ctx* c) {
 }
 
 // ---------------------------------------------------------------- helpers
-// Largest FFT the shared-memory kernels hold (cols pass: ~26 P bytes <= 227 KB).
+// Largest FFT of the shared-memory kernels (512 threads, one radix-16 butterfly each).
 constexpr int kMaxFftSize = 8192;
 
-// Smallest even m >= target of the form 2^a 3^b 5^c with b <= 2, c <= 1 (the radices of
-// kernels_fftconv.cu, few odd stages).
+// Smallest m >= target with m % 256 == 0 and m = 2^a 3^b 5^c, b <= 2, c <= 1 (the radices
+// of kernels_fftconv.cu; the first two stages are radix 16, all strides multiples of 16).
 int nice_fft_size(int64_t target) {
-  for (int64_t m = std::max<int64_t>(target, 2);; ++m) {
-    if (m & 1) continue;
+  for (int64_t m = std::max<int64_t>((target + 255) / 256 * 256, 256);; m += 256) {
     int64_t r = m;
     int b = 0, c5 = 0;
     while (r % 2 == 0) r /= 2;
@@ -346,9 +347,10 @@ void free_fft_buffers(tfdp_ctx* c) {
   cudaFree(c->phi);
   cudaFree(c->ca);
   cudaFree(c->ka);
-  c->grid = c->phi = c->ka = nullptr;
+  cudaFree(c->kh);
+  c->grid = c->phi = c->ka = c->kh = nullptr;
   c->ca = nullptr;
-  c->alloc_planes = c->alloc_ca = c->alloc_ka = 0;
+  c->alloc_planes = c->alloc_ca = c->alloc_ka = c->alloc_kh = 0;
   for (int k = 0; k < 4; ++k) {
     cudaFree(c->tw[k]);
     c->tw[k] = nullptr;
@@ -377,8 +379,9 @@ tfdp_status configure_fft(tfdp_ctx* c, float L) {
                     2 * p.n_int_fixed * k - 1, k);
       cap = p.n_int_fixed;
     }
-    if (P % 2 || P > kMaxFftSize)
-      return fail(c, TFDP_ERR_UNSUPPORTED, "FFT size %d unsupported (even, <= %d)", P, kMaxFftSize);
+    if (P % 256 || P > kMaxFftSize)
+      return fail(c, TFDP_ERR_UNSUPPORTED, "FFT size %d unsupported (multiple of 256, <= %d)", P,
+                  kMaxFftSize);
     {
       int r = P;
       while (r % 2 == 0) r /= 2;
@@ -393,27 +396,33 @@ tfdp_status configure_fft(tfdp_ctx* c, float L) {
   c->nint_cap = need;
   const int cpitch = mcap;
   const int capitch = (mcap + 1) & ~1;
-  int64_t planes = 3LL * cpitch * cpitch, ca = 0, ka = 0;
+  int64_t planes = 3LL * cpitch * cpitch, ca = 0, ka = 0, kh = 0;
   for (int k = 1; k <= 3; ++k) {
     if (!k_used(c, k)) continue;
     ca = std::max<int64_t>(ca, 3LL * (c->P_of_k[k] / 2 + 1) * capitch);
     ka = std::max<int64_t>(ka, (int64_t)(c->P_of_k[k] / 2 + 1) * cpitch);
+    kh = std::max<int64_t>(kh, (int64_t)(c->P_of_k[k] / 2 + 2) * c->P_of_k[k]);
   }
-  if (planes > c->alloc_planes || ca > c->alloc_ca || ka > c->alloc_ka) {
+  if (planes > c->alloc_planes || ca > c->alloc_ca || ka > c->alloc_ka || kh > c->alloc_kh) {
     cudaStreamSynchronize(c->stream);
     cudaFree(c->grid);
     cudaFree(c->phi);
     cudaFree(c->ca);
     cudaFree(c->ka);
-    c->grid = c->phi = c->ka = nullptr;
+    cudaFree(c->kh);
+    c->grid = c->phi = c->ka = c->kh = nullptr;
     c->ca = nullptr;
     CUDA_TRY(c, cudaMalloc(&c->grid, planes * sizeof(float)));
+    // invariant: the charge planes are zero between iterations (rows_fwd re-zeroes)
+    CUDA_TRY(c, cudaMemsetAsync(c->grid, 0, planes * sizeof(float), c->stream));
     CUDA_TRY(c, cudaMalloc(&c->phi, planes * sizeof(float)));
     CUDA_TRY(c, cudaMalloc(&c->ca, ca * sizeof(float2)));
     CUDA_TRY(c, cudaMalloc(&c->ka, ka * sizeof(float)));
+    CUDA_TRY(c, cudaMalloc(&c->kh, kh * sizeof(float)));
     c->alloc_planes = planes;
     c->alloc_ca = ca;
     c->alloc_ka = ka;
+    c->alloc_kh = kh;
   }
   c->cpitch = cpitch;
   c->ca_pitch = capitch;
@@ -430,7 +439,8 @@ tfdp_status configure_fft(tfdp_ctx* c, float L) {
       c->tw_P[k] = P;
     }
   }
-  CUDA_TRY(c, tfdp::fftconv_prepare(Pmax));
+  for (int k = 1; k <= 3; ++k)
+    if (k_used(c, k)) CUDA_TRY(c, tfdp::fftconv_prepare(c->P_of_k[k]));
   CUDA_TRY(c, cudaGetLastError());
   return TFDP_OK;
 }
@@ -478,6 +488,7 @@ tfdp_status evaluate(tfdp_ctx* c, int update, float eta, int k) {
     const float2* tw = c->tw[k];
     if (!c->box_valid || c->world > 1) {
       Scope sc(c, K_BBOX);
+      tfdp::launch_reset_slots(c->box_part, c->stream);
       c->n_part = tfdp::launch_bbox(xy, c->n, c->box_part, c->stream);
     }
     {
@@ -486,10 +497,8 @@ tfdp_status evaluate(tfdp_ctx* c, int update, float eta, int k) {
                          c->p.n_int_fixed, c->cap_of_k[k],
                          P, c->cpitch, c->capped, c->stream);
     }
-    {
-      Scope sc(c, K_ZERO);
-      tfdp::launch_zero_planes(c->geom, c->grid, c->cpitch, mcap, c->stream);
-    }
+    // The charge planes are all-zero here: they start zeroed and rows_fwd clears every row
+    // it consumes (no separate zeroing pass).
     const bool allreduce = c->world > 1 && c->p.dist_mode == TFDP_DIST_GRID_ALLREDUCE;
     {
       Scope sc(c, K_SPREAD);
@@ -513,7 +522,7 @@ tfdp_status evaluate(tfdp_ctx* c, int update, float eta, int k) {
     }
     {
       Scope sc(c, K_KSPEC);
-      tfdp::launch_kspec_rows(c->geom, P, mcap, c->fa, tw, c->ka, c->cpitch, c->stream);
+      tfdp::launch_kspec(c->geom, P, mcap, c->fa, tw, c->ka, c->cpitch, c->kh, c->stream);
     }
     {
       Scope sc(c, K_ROWS_FWD);
@@ -521,7 +530,7 @@ tfdp_status evaluate(tfdp_ctx* c, int update, float eta, int k) {
     }
     {
       Scope sc(c, K_COLS);
-      tfdp::launch_cols(c->geom, c->ca, c->ca_pitch, c->ka, c->cpitch, P, tw, c->stream);
+      tfdp::launch_cols(c->geom, c->ca, c->ca_pitch, c->kh, P, tw, c->stream);
     }
     {
       Scope sc(c, K_ROWS_INV);
@@ -530,7 +539,7 @@ tfdp_status evaluate(tfdp_ctx* c, int update, float eta, int k) {
     {
       Scope sc(c, K_GATHER_UPDATE);
       BoxKeys* nk = (update && c->world == 1) ? c->box_part : nullptr;
-      if (nk) c->n_part = (int)((n_local + tfdp::kNodeThreads - 1) / tfdp::kNodeThreads);
+      if (nk) c->n_part = tfdp::kBoxSlots;
       tfdp::launch_gather_update(xy, xyn, c->lo, n_local, c->geom, k, c->phi, c->row_ptr, c->col,
                                  c->fa, eta, c->t, update, c->rep, c->att, c->diverge, nk,
                                  c->stream);
@@ -588,6 +597,7 @@ tfdp_status maybe_replan(tfdp_ctx* c, bool capped) {
     if (k_used(c, k)) mincap = std::min(mincap, c->cap_of_k[k]);
   if (!capped && last.n_int + 4 <= mincap) return TFDP_OK;
   if (!capped && c->P_of_k[3] >= kMaxFftSize) return TFDP_OK;  // already at the largest grid
+  tfdp::launch_reset_slots(c->box_part, c->stream);
   c->n_part = tfdp::launch_bbox(c->xy[c->cur], c->n, c->box_part, c->stream);
   tfdp::launch_box_reduce(c->box_part, c->n_part, c->keys, c->stream);
   c->launches += 2;
@@ -758,9 +768,7 @@ tfdp_status tfdp_init(tfdp_ctx** out, int64_t n, const int64_t* row_ptr, const i
   ALLOC(c->diverge, sizeof(unsigned long long));
   ALLOC(c->capped, sizeof(int));
   ALLOC(c->keys, sizeof(BoxKeys));
-  ALLOC(c->box_part, std::max<int64_t>(tfdp::bbox_blocks(n),
-                                       (n_local + tfdp::kNodeThreads - 1) / tfdp::kNodeThreads) *
-                         sizeof(BoxKeys));
+  ALLOC(c->box_part, tfdp::kBoxSlots * sizeof(BoxKeys));
   ALLOC(c->geom, sizeof(GridGeom));
   if (cudaMallocHost((void**)&c->h_status, 2 * sizeof(unsigned long long) + sizeof(GridGeom)) !=
       cudaSuccess)
@@ -784,6 +792,7 @@ tfdp_status tfdp_init(tfdp_ctx** out, int64_t n, const int64_t* row_ptr, const i
       cudaMemsetAsync(c->diverge, 0xff, sizeof(unsigned long long), s) != cudaSuccess ||
       cudaMemsetAsync(c->capped, 0, sizeof(int), s) != cudaSuccess)
     return bail(fail(c, TFDP_ERR_CUDA, "initial copies failed: %s", cudaGetErrorString(cudaGetLastError())));
+  tfdp::launch_reset_slots(c->box_part, s);
   if (p.solver == TFDP_IBFFT) {
     if (xy_dev) {  // box of a device layout: one bbox pass
       c->n_part = tfdp::launch_bbox(c->xy[0], n, c->box_part, s);
@@ -1005,6 +1014,7 @@ void tfdp_destroy(tfdp_ctx* c) {
   cudaFree(c->att);
   cudaFree(c->diverge);
   cudaFree(c->capped);
+  cudaFree(c->kh);
   cudaFree(c->keys);
   cudaFree(c->box_part);
   cudaFree(c->geom);

@@ -52,6 +52,37 @@ __device__ __forceinline__ float key2f(unsigned int k) {
   return __uint_as_float(u);
 }
 
+// Attraction of one CSR row (P:286-288 Eq. newforce, phi = 1 t-force term R17), without
+// the -alpha factor: sum_j (1 + beta / (1 + d^2)) (x_i - x_j).  Four edges per round: all
+// column indices, then all neighbour positions are loaded before any arithmetic, so a
+// thread keeps up to 8 independent loads in flight (the row walk is latency-bound).
+__device__ __forceinline__ float2 attraction_sum(const float2* __restrict__ xy, float2 xi,
+                                                 const int64_t* __restrict__ row_ptr,
+                                                 const int32_t* __restrict__ col, int64_t i,
+                                                 float beta) {
+  float sx = 0.f, sy = 0.f;
+  int64_t e = row_ptr[i];
+  const int64_t e1 = row_ptr[i + 1];
+  auto term = [&](float2 xj) {
+    const float dx = xi.x - xj.x, dy = xi.y - xj.y;
+    const float s = fmaf(dx, dx, fmaf(dy, dy, 1.0f));
+    const float c = fmaf(beta, rcp_approx(s), 1.0f);
+    sx = fmaf(c, dx, sx);
+    sy = fmaf(c, dy, sy);
+  };
+  for (; e + 4 <= e1; e += 4) {
+    const int j0 = __ldg(col + e), j1 = __ldg(col + e + 1), j2 = __ldg(col + e + 2),
+              j3 = __ldg(col + e + 3);
+    const float2 x0 = __ldg(xy + j0), x1 = __ldg(xy + j1), x2 = __ldg(xy + j2), x3 = __ldg(xy + j3);
+    term(x0);
+    term(x1);
+    term(x2);
+    term(x3);
+  }
+  for (; e < e1; ++e) term(__ldg(xy + __ldg(col + e)));
+  return make_float2(sx, sy);
+}
+
 // Lagrange basis on K equispaced nodes t_c = (c + 1/2)/K of [0, 1] (R8):
 // l_c(u) = prod_{c' != c} (u - t_c') / (t_c - t_c').  Constants fold at compile time.
 template <int K>

@@ -92,17 +92,8 @@ __device__ __forceinline__ float2 attraction_row(const float2* __restrict__ xy, 
                                                  const int64_t* __restrict__ row_ptr,
                                                  const int32_t* __restrict__ col, int64_t i,
                                                  float alpha, float beta) {
-  float sx = 0.f, sy = 0.f;
-  const int64_t e1 = row_ptr[i + 1];
-  for (int64_t e = row_ptr[i]; e < e1; ++e) {
-    const float2 xj = xy[col[e]];
-    const float dx = xi.x - xj.x, dy = xi.y - xj.y;
-    const float s = fmaf(dx, dx, fmaf(dy, dy, 1.0f));
-    const float c = fmaf(beta, rcp_approx(s), 1.0f);  // 1 + beta / s  (phi = 1 t-force, R17)
-    sx = fmaf(c, dx, sx);
-    sy = fmaf(c, dy, sy);
-  }
-  return make_float2(-alpha * sx, -alpha * sy);
+  const float2 s = attraction_sum(xy, xi, row_ptr, col, i, beta);
+  return make_float2(-alpha * s.x, -alpha * s.y);
 }
 
 __global__ void __launch_bounds__(kNodeThreads)

@@ -14,11 +14,12 @@
 namespace tfdp {
 
 // ------------------------------------------------------------------ bbox
-// Two-level exact min/max: every block reduces its keys (warp __reduce + smem) and writes
-// one BoxKeys partial; the consumer (setup / box_reduce, one block) reduces the partials.
-// No same-address atomics (those serialise in one L2 slice).
+// Two-level exact min/max: every block reduces its keys (warp __reduce + smem) and merges
+// them with atomicMin/Max into one of kBoxSlots slots (block % kBoxSlots: ~60 blocks per
+// slot, so no single-address hot spot); the consumer (setup / box_reduce, one block) reduces
+// the slots and resets them to the identity for the next producer.
 __device__ __forceinline__ void block_box_commit(unsigned kx0, unsigned ky0, unsigned kx1,
-                                                 unsigned ky1, BoxKeys* part) {
+                                                 unsigned ky1, BoxKeys* slots) {
   __shared__ unsigned s[4][32];
   kx0 = __reduce_min_sync(0xffffffffu, kx0);
   ky0 = __reduce_min_sync(0xffffffffu, ky0);
@@ -39,12 +40,23 @@ __device__ __forceinline__ void block_box_commit(unsigned kx0, unsigned ky0, uns
     ky0 = __reduce_min_sync(0xffffffffu, v ? s[1][lane] : 0xffffffffu);
     kx1 = __reduce_max_sync(0xffffffffu, v ? s[2][lane] : 0u);
     ky1 = __reduce_max_sync(0xffffffffu, v ? s[3][lane] : 0u);
-    if (lane == 0) part[blockIdx.x] = BoxKeys{kx0, ky0, kx1, ky1};
+    if (lane == 0) {
+      BoxKeys* sl = slots + (blockIdx.x % kBoxSlots);
+      atomicMin(&sl->minx, kx0);
+      atomicMin(&sl->miny, ky0);
+      atomicMax(&sl->maxx, kx1);
+      atomicMax(&sl->maxy, ky1);
+    }
   }
 }
 
-// One block reduces n_part partials; result in *out (all threads return it).
-__device__ BoxKeys block_reduce_partials(const BoxKeys* __restrict__ part, int n_part) {
+__device__ __forceinline__ void reset_slots(BoxKeys* slots) {
+  for (int i = threadIdx.x; i < kBoxSlots; i += blockDim.x)
+    slots[i] = BoxKeys{0xffffffffu, 0xffffffffu, 0u, 0u};
+}
+
+// One block reduces the n_part slots, then resets them (all threads return the result).
+__device__ BoxKeys block_reduce_partials(BoxKeys* part, int n_part) {
   unsigned kx0 = 0xffffffffu, ky0 = 0xffffffffu, kx1 = 0u, ky1 = 0u;
   for (int i = threadIdx.x; i < n_part; i += blockDim.x) {
     const BoxKeys b = part[i];
@@ -76,7 +88,8 @@ __device__ BoxKeys block_reduce_partials(const BoxKeys* __restrict__ part, int n
     ky1 = __reduce_max_sync(0xffffffffu, v ? s[3][lane] : 0u);
     if (lane == 0) r[0] = BoxKeys{kx0, ky0, kx1, ky1};
   }
-  __syncthreads();
+  __syncthreads();  // all slot reads are done
+  reset_slots(part);
   return r[0];
 }
 
@@ -95,28 +108,31 @@ bbox_kernel(const float2* __restrict__ xy, int64_t n, BoxKeys* part) {
   block_box_commit(kx0, ky0, kx1, ky1, part);
 }
 
-__global__ void __launch_bounds__(1024) box_reduce_kernel(const BoxKeys* part, int n_part, BoxKeys* keys) {
+__global__ void __launch_bounds__(64) box_reduce_kernel(BoxKeys* part, int n_part, BoxKeys* keys) {
   const BoxKeys b = block_reduce_partials(part, n_part);
   if (threadIdx.x == 0) *keys = b;
 }
+
+__global__ void __launch_bounds__(64) reset_slots_kernel(BoxKeys* slots) { reset_slots(slots); }
 
 int bbox_blocks(int64_t n) {
   return (int)std::max<int64_t>(1, std::min<int64_t>((n + kNodeThreads - 1) / kNodeThreads, 148 * 8));
 }
 
+void launch_reset_slots(BoxKeys* slots, cudaStream_t s) { reset_slots_kernel<<<1, 64, 0, s>>>(slots); }
+
 int launch_bbox(const float2* xy, int64_t n, BoxKeys* part, cudaStream_t s) {
-  const int blocks = bbox_blocks(n);
-  bbox_kernel<<<blocks, kNodeThreads, 0, s>>>(xy, n, part);
-  return blocks;
+  bbox_kernel<<<bbox_blocks(n), kNodeThreads, 0, s>>>(xy, n, part);
+  return kBoxSlots;
 }
 
-void launch_box_reduce(const BoxKeys* part, int n_part, BoxKeys* keys, cudaStream_t s) {
-  box_reduce_kernel<<<1, 1024, 0, s>>>(part, n_part, keys);
+void launch_box_reduce(BoxKeys* part, int n_part, BoxKeys* keys, cudaStream_t s) {
+  box_reduce_kernel<<<1, 64, 0, s>>>(part, n_part, keys);
 }
 
 // ------------------------------------------------------------------ setup
-__global__ void __launch_bounds__(1024)
-setup_kernel(const BoxKeys* part, int n_part, BoxKeys* keys, GridGeom* geom, int k,
+__global__ void __launch_bounds__(64)
+setup_kernel(BoxKeys* part, int n_part, BoxKeys* keys, GridGeom* geom, int k,
              int n_int_min, int n_int_fixed, int n_int_cap, int P, int pitch, int* capped_flag) {
   const BoxKeys kb = block_reduce_partials(part, n_part);
   if (threadIdx.x != 0) return;
@@ -166,11 +182,11 @@ setup_kernel(const BoxKeys* part, int n_part, BoxKeys* keys, GridGeom* geom, int
   if (capped) atomicOr(capped_flag, 1);
 }
 
-void launch_setup(const BoxKeys* part, int n_part, BoxKeys* keys, GridGeom* geom, int k,
+void launch_setup(BoxKeys* part, int n_part, BoxKeys* keys, GridGeom* geom, int k,
                   int n_int_min, int n_int_fixed, int n_int_cap, int P, int pitch,
                   int* capped_flag, cudaStream_t s) {
-  setup_kernel<<<1, 1024, 0, s>>>(part, n_part, keys, geom, k, n_int_min, n_int_fixed, n_int_cap,
-                                  P, pitch, capped_flag);
+  setup_kernel<<<1, 64, 0, s>>>(part, n_part, keys, geom, k, n_int_min, n_int_fixed, n_int_cap,
+                                P, pitch, capped_flag);
 }
 
 // ------------------------------------------------------------------ interval coords
@@ -268,18 +284,8 @@ gather_update_kernel(const float2* __restrict__ xy, float2* __restrict__ xy_next
     // F^r = x~ psi_1 - psi_x~  (Eqs. Fr1/Fr2); fused to limit cancellation (R11)
     const float Rx = fa.rho * fmaf(xt, psi0, -psi1);
     const float Ry = fa.rho * fmaf(yt, psi0, -psi2);
-    float ax = 0.f, ay = 0.f;
-    const int64_t e1 = row_ptr[i + 1];
-    for (int64_t e = row_ptr[i]; e < e1; ++e) {
-      const float2 xj = xy[col[e]];
-      const float dx = p.x - xj.x, dy = p.y - xj.y;
-      const float s = fmaf(dx, dx, fmaf(dy, dy, 1.0f));
-      const float cc = fmaf(fa.beta, rcp_approx(s), 1.0f);
-      ax = fmaf(cc, dx, ax);
-      ay = fmaf(cc, dy, ay);
-    }
-    ax *= -fa.alpha;
-    ay *= -fa.alpha;
+    const float2 as = attraction_sum(xy, p, row_ptr, col, i, fa.beta);
+    const float ax = -fa.alpha * as.x, ay = -fa.alpha * as.y;
     if (update) {
       const float nx = fmaf(eta, Rx + ax, p.x);
       const float ny = fmaf(eta, Ry + ay, p.y);

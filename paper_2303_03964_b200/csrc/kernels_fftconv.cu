@@ -1,17 +1,20 @@
 // Hand-written FFT convolution of the ibFFT grid step (R9) — sm_100a.
 //
-// Replaces a zero-padded P x P 2-D R2C -> x K^ -> C2R (cuFFT) by four passes that never
-// touch the zero padding and never write outputs that are discarded:
-//   kspec_rows  K rows dy = 0..M-1, generated on the fly (K even in x and y, so each row
-//               FFT is real): KA[q][dy], q = 0..P/2                        (1 x M FFTs)
-//   rows_fwd    each pair of charge rows (a + i b) -> one complex FFT, untangled into
-//               the half spectra of rows a and b: CA[c][q][row]            (3M/2 FFTs)
-//   cols        per pair of columns q: K^ columns (one packed real-even FFT), then for
-//               each channel FFT -> x K^ -> inverse FFT, keeping rows 0..M-1 (13 FFTs)
-//   rows_inv    Hermitian rows -> one complex inverse FFT per row pair, keep 0..M-1
-// Rows beyond M are zero and never loaded; outputs beyond M are never stored.  All FFTs
-// are power-of-two Stockham radix-8/4/2 in shared memory with an fp64-generated twiddle
-// table.  The 1/P^2 of the inverse is folded into the kernel samples.
+// Replaces a zero-padded P x P 2-D R2C -> x K^ -> C2R by five passes that never transform
+// the zero padding and never store outputs that are discarded:
+//   kspec_rows  K rows dy = 0..M-1 generated on the fly (K is even in x and y, so each row
+//               spectrum is real), two rows per complex FFT: KA[q][dy], q = 0..P/2
+//   kspec_cols  two K^ columns per packed real-even FFT: KH[q][u] (real), u = 0..P-1
+//   rows_fwd    two charge rows (a + i b) per complex FFT, untangled into the half
+//               spectra of rows a and b: CA[c][q][row]
+//   cols        one (channel, column) per block: FFT -> x K^ -> inverse FFT, rows 0..M-1 kept
+//   rows_inv    Hermitian rows, two rows per complex inverse FFT, columns 0..M-1 kept
+// The inputs of every forward FFT are zero beyond P/2 (M <= P/2), so the first radix-8
+// stage skips those loads; every inverse FFT keeps only outputs below P/2, so its last
+// stage stores half.  FFTs are in-place Stockham stages (radix 8, 4, 2, then 3, 5) in
+// shared memory, P % 64 == 0, one float2 of padding per 8 (conflict-free strided stores,
+// address = base + r * stride).  Twiddles come from a two-level fp64-generated table in
+// shared memory (w) and short product chains (w^2 ... w^7).  1/P^2 is folded into K.
 #include <algorithm>
 
 #include "device_math.cuh"
@@ -27,8 +30,7 @@ __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
 __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
 __device__ __forceinline__ float2 conjf2(float2 a) { return make_float2(a.x, -a.y); }
-// multiply by -i
-__device__ __forceinline__ float2 mul_mi(float2 a) { return make_float2(a.y, -a.x); }
+__device__ __forceinline__ float2 mul_mi(float2 a) { return make_float2(a.y, -a.x); }  // * (-i)
 
 template <int R>
 __device__ __forceinline__ void dft(float2 (&v)[R]);
@@ -54,7 +56,6 @@ __device__ __forceinline__ void dft<3>(float2 (&v)[3]) {
 
 template <>
 __device__ __forceinline__ void dft<5>(float2 (&v)[5]) {
-  // direct 5-point DFT with the standard real/imag split
   const float c1 = 0.30901699437494742f, c2 = -0.80901699437494742f;
   const float s1 = -0.95105651629515357f, s2 = -0.58778525229247313f;
   const float2 a1 = cadd(v[1], v[4]), b1 = csub(v[1], v[4]);
@@ -62,7 +63,6 @@ __device__ __forceinline__ void dft<5>(float2 (&v)[5]) {
   const float2 x0 = v[0];
   const float2 m1 = make_float2(x0.x + c1 * a1.x + c2 * a2.x, x0.y + c1 * a1.y + c2 * a2.y);
   const float2 m2 = make_float2(x0.x + c2 * a1.x + c1 * a2.x, x0.y + c2 * a1.y + c1 * a2.y);
-  // i*(s1 b1 + s2 b2), i*(s2 b1 - s1 b2)
   const float2 n1 = make_float2(-(s1 * b1.y + s2 * b2.y), s1 * b1.x + s2 * b2.x);
   const float2 n2 = make_float2(-(s2 * b1.y - s1 * b2.y), s2 * b1.x - s1 * b2.x);
   v[0] = cadd(x0, cadd(a1, a2));
@@ -74,7 +74,6 @@ __device__ __forceinline__ void dft<5>(float2 (&v)[5]) {
 
 template <>
 __device__ __forceinline__ void dft<4>(float2 (&v)[4]) {
-  // forward DFT-4: X_s = sum_r v_r (-i)^{rs}
   const float2 s02 = cadd(v[0], v[2]), d02 = csub(v[0], v[2]);
   const float2 s13 = cadd(v[1], v[3]), d13 = mul_mi(csub(v[1], v[3]));
   v[0] = cadd(s02, s13);
@@ -85,16 +84,14 @@ __device__ __forceinline__ void dft<4>(float2 (&v)[4]) {
 
 template <>
 __device__ __forceinline__ void dft<8>(float2 (&v)[8]) {
-  // radix-2 x radix-4: even/odd DFT-4s combined with W8^s
   float2 e[4] = {v[0], v[2], v[4], v[6]};
   float2 o[4] = {v[1], v[3], v[5], v[7]};
   dft<4>(e);
   dft<4>(o);
   const float h = 0.70710678118654752f;
-  // W8^1 = (1 - i)/sqrt2, W8^2 = -i, W8^3 = (-1 - i)/sqrt2
-  const float2 o1 = make_float2(h * (o[1].x + o[1].y), h * (o[1].y - o[1].x));
-  const float2 o2 = mul_mi(o[2]);
-  const float2 o3 = make_float2(h * (o[3].y - o[3].x), -h * (o[3].x + o[3].y));
+  const float2 o1 = make_float2(h * (o[1].x + o[1].y), h * (o[1].y - o[1].x));  // W8
+  const float2 o2 = mul_mi(o[2]);                                               // W8^2
+  const float2 o3 = make_float2(h * (o[3].y - o[3].x), -h * (o[3].x + o[3].y)); // W8^3
   v[0] = cadd(e[0], o[0]);
   v[4] = csub(e[0], o[0]);
   v[1] = cadd(e[1], o1);
@@ -105,62 +102,112 @@ __device__ __forceinline__ void dft<8>(float2 (&v)[8]) {
   v[7] = csub(e[3], o3);
 }
 
-// Shared-memory layout of one FFT buffer: one float2 of padding per 8, which makes the
-// strided Stockham stores of the first stages conflict-free.
-__device__ __forceinline__ int pad(int i) { return i + (i >> 3); }
-__host__ __device__ constexpr int padded_len(int N) { return N + (N >> 3) + 1; }
+// DFT-16 as 4 x 4 (Cooley-Tukey, r = 4 r1 + r2, s = s1 + 4 s2): DFT-4 over r1, twiddle
+// W16^(r2 s1), DFT-4 over r2; outputs written back in natural order.
+template <>
+__device__ __forceinline__ void dft<16>(float2 (&v)[16]) {
+  float2 y[4][4];  // y[r2][s1]
+#pragma unroll
+  for (int r2 = 0; r2 < 4; ++r2) {
+    float2 t[4] = {v[r2], v[r2 + 4], v[r2 + 8], v[r2 + 12]};
+    dft<4>(t);
+#pragma unroll
+    for (int s1 = 0; s1 < 4; ++s1) y[r2][s1] = t[s1];
+  }
+  const float h = 0.70710678118654752f;
+  const float c1 = 0.92387953251128674f, s1_ = 0.38268343236508978f;  // cos, sin(pi/8)
+  // W16^e = exp(-2 pi i e / 16) for the products e = r2 * s1
+  const float2 W1 = make_float2(c1, -s1_), W2 = make_float2(h, -h), W3 = make_float2(s1_, -c1);
+  const float2 W6 = make_float2(-h, -h), W9 = make_float2(-c1, s1_);
+  y[1][1] = cmul(y[1][1], W1);
+  y[1][2] = cmul(y[1][2], W2);
+  y[1][3] = cmul(y[1][3], W3);
+  y[2][1] = cmul(y[2][1], W2);
+  y[2][2] = mul_mi(y[2][2]);  // W16^4 = -i
+  y[2][3] = cmul(y[2][3], W6);
+  y[3][1] = cmul(y[3][1], W3);
+  y[3][2] = cmul(y[3][2], W6);
+  y[3][3] = cmul(y[3][3], W9);
+#pragma unroll
+  for (int s1 = 0; s1 < 4; ++s1) {
+    float2 t[4] = {y[0][s1], y[1][s1], y[2][s1], y[3][s1]};
+    dft<4>(t);
+#pragma unroll
+    for (int s2 = 0; s2 < 4; ++s2) v[s1 + 4 * s2] = t[s2];
+  }
+}
 
-// Twiddle table (fp64-generated, fp32 stored), two-level so it fits in shared memory:
-// tw[0..64) = exp(-2 pi i t / N), tw[64 + u] = exp(-2 pi i 64 u / N), u = 0..N/64; then
-// exp(-2 pi i t / N) = tw[64 + (t >> 6)] * tw[t & 63]  (one complex product, ~1.5 ulp).
+// Shared-memory layout: one float2 of padding per 16 (pad(i) = i + i/16): the strided
+// Stockham stores of the first stages become conflict-free and, since every stride is a
+// multiple of 16 (P % 256 == 0), address(r) = base + r * padded_stride.
+__device__ __forceinline__ int pad(int i) { return i + (i >> 4); }
+__host__ __device__ constexpr int padded_len(int N) { return N + (N >> 4) + 1; }
+
+// Two-level twiddle table: tw[0..64) = exp(-2 pi i t / N), tw[64 + u] = exp(-2 pi i 64u / N),
+// exp(-2 pi i t / N) = tw[64 + t/64] * tw[t % 64].
 __host__ __device__ constexpr int tw_len(int N) { return 64 + N / 64 + 1; }
-
 __device__ __forceinline__ float2 tw_at(const float2* __restrict__ tw, int t) {
   return cmul(tw[64 + (t >> 6)], tw[t & 63]);
 }
 
-// Twiddles w^r, r = 1..R-1, of one butterfly: at most three table lookups (w, w^2, w^4),
-// the rest by at most two complex products.
+// w^r for r = 1..R-1 from one table lookup and a product chain of depth <= 3.
 template <int R>
 __device__ __forceinline__ void twiddles(const float2* __restrict__ tw, int base, float2 (&w)[R]) {
   w[1] = tw_at(tw, base);
-  if constexpr (R >= 3) w[2] = tw_at(tw, 2 * base);
-  if constexpr (R >= 4) w[3] = cmul(w[1], w[2]);
-  if constexpr (R == 5) w[4] = cmul(w[2], w[2]);
-  if constexpr (R == 8) {
-    w[4] = tw_at(tw, 4 * base);
+  if constexpr (R >= 3) w[2] = cmul(w[1], w[1]);
+  if constexpr (R >= 4) w[3] = cmul(w[2], w[1]);
+  if constexpr (R >= 5) w[4] = cmul(w[2], w[2]);
+  if constexpr (R >= 8) {
     w[5] = cmul(w[4], w[1]);
     w[6] = cmul(w[4], w[2]);
     w[7] = cmul(w[4], w[3]);
   }
+  if constexpr (R == 16) {  // second lookup keeps the product chains at depth <= 3
+    w[8] = tw_at(tw, 8 * base);
+#pragma unroll
+    for (int r = 1; r < 8; ++r) w[8 + r] = cmul(w[8], w[r]);
+  }
 }
 
-// In-place Stockham autosort stage (Govindaraju et al. 2008 formulation), radix R, size N,
-// current sub-transform size Ns.  Every thread first loads + transforms its butterflies
-// (registers), the block synchronises, then all results are stored: one buffer instead
-// of ping-pong, so twice the FFTs fit in shared memory.  Requires blockDim.x >= N / 8.
-template <int R>
-struct PerThread { static constexpr int value = 1; };
-template <> struct PerThread<4> { static constexpr int value = 2; };
-template <> struct PerThread<2> { static constexpr int value = 4; };
-template <> struct PerThread<3> { static constexpr int value = 3; };
-template <> struct PerThread<5> { static constexpr int value = 2; };
+// Butterflies per thread of a radix-R stage when blockDim.x >= N / 16.
+template <int R> struct PerThread { static constexpr int value = 16 / R; };
+template <> struct PerThread<3> { static constexpr int value = 6; };
+template <> struct PerThread<5> { static constexpr int value = 4; };
 
-template <int R>
-__device__ __forceinline__ void stage(float2* buf, int N, int Ns, const float2* __restrict__ tw) {
-  constexpr int MB = PerThread<R>::value;  // butterflies per thread (N/R <= MB * blockDim)
+// Register cap via min blocks per SM: 64 registers per thread (every non-inlined stage fits
+// in 64 without spills, measured with ptxas), i.e. 1024 threads of FFT work per SM.
+template <int T>
+constexpr int kMinBlocks = T <= 512 ? 1024 / T : 1;
+
+// FFT flags: inputs zero at index >= N/2 (first stage skips them); only outputs < N/2 needed
+// (last stage stores half).
+enum { kZeroUpper = 1, kLowOut = 2 };
+
+// In-place Stockham autosort stage (Govindaraju et al. 2008 formulation): radix R, size N,
+// sub-transform size Ns (1 for the first stage, else a multiple of 16 since N % 256 == 0 and
+// the first stage is radix 16).  Loads + butterflies into registers, barrier, stores, barrier.
+// Not inlined: each stage needs < 100 registers; inlining the runtime-radix chain costs more.
+template <int T, int R, bool ZERO_UPPER, bool LOW_OUT>
+__device__ __noinline__ void stage(float2* buf, int N, int Ns, const float2* __restrict__ tw) {
+  constexpr int MB = PerThread<R>::value;
   const int nb = N / R;
-  const int step = nb / Ns;  // N / (Ns R)
+  const int step = nb / Ns;                 // N / (Ns R)
+  const int sin_ = nb + (nb >> 4);          // pad stride of the loads (nb % 16 == 0)
+  const int sout = Ns == 1 ? 1 : Ns + (Ns >> 4);
   const bool p2 = (Ns & (Ns - 1)) == 0;
   float2 v[MB][R];
 #pragma unroll
   for (int b = 0; b < MB; ++b) {
-    const int j = threadIdx.x + b * blockDim.x;
+    const int j = threadIdx.x + b * T;
     if (j < nb) {
-      const int k = p2 ? (j & (Ns - 1)) : (j % Ns);
+      const int pj = j + (j >> 4);
 #pragma unroll
-      for (int r = 0; r < R; ++r) v[b][r] = buf[pad(j + r * nb)];
+      for (int r = 0; r < R; ++r) {
+        if (ZERO_UPPER && 2 * r >= R) v[b][r] = make_float2(0.f, 0.f);
+        else v[b][r] = buf[pj + r * sin_];
+      }
       if (Ns > 1) {
+        const int k = p2 ? (j & (Ns - 1)) : (j % Ns);
         float2 w[R];
         twiddles<R>(tw, k * step, w);
 #pragma unroll
@@ -172,47 +219,46 @@ __device__ __forceinline__ void stage(float2* buf, int N, int Ns, const float2* 
   __syncthreads();
 #pragma unroll
   for (int b = 0; b < MB; ++b) {
-    const int j = threadIdx.x + b * blockDim.x;
+    const int j = threadIdx.x + b * T;
     if (j < nb) {
-      const int k = p2 ? (j & (Ns - 1)) : (j % Ns);
+      const int k = Ns == 1 ? 0 : (p2 ? (j & (Ns - 1)) : (j % Ns));
       const int d = (j - k) * R + k;
+      const int pd = d + (d >> 4);
 #pragma unroll
-      for (int r = 0; r < R; ++r) buf[pad(d + r * Ns)] = v[b][r];
+      for (int r = 0; r < R; ++r)
+        if (!LOW_OUT || 2 * r < R) buf[pd + r * sout] = v[b][r];
     }
   }
   __syncthreads();
 }
 
-// Forward complex FFT of buf[0..N) (N = 2^a 3^b 5^c, padded layout) in shared memory, in
-// place.  Power-of-two stages first (radix 8, then 4 / 2), odd radices last, so Ns is a
-// power of two wherever possible.  Called by the whole block (blockDim.x >= N/8); the
-// input must be visible (barrier) before the call; ends with a barrier.
+template <int T, bool LOW>
+__device__ __forceinline__ void stage_any(int R, float2* buf, int N, int Ns,
+                                          const float2* __restrict__ tw) {
+  switch (R) {
+    case 16: stage<T, 16, false, LOW>(buf, N, Ns, tw); break;
+    case 8: stage<T, 8, false, LOW>(buf, N, Ns, tw); break;
+    case 4: stage<T, 4, false, LOW>(buf, N, Ns, tw); break;
+    case 2: stage<T, 2, false, LOW>(buf, N, Ns, tw); break;
+    case 3: stage<T, 3, false, false>(buf, N, Ns, tw); break;  // odd radix: store all
+    default: stage<T, 5, false, false>(buf, N, Ns, tw); break;
+  }
+}
+
+// Forward complex FFT of buf[0..N) in place (padded layout), N = 2^a 3^b 5^c, N % 256 == 0.
+// Radix 16 first (so Ns is a multiple of 16 afterwards), then 16/8/4/2, then 3, 5.  Called
+// by the whole block (T >= N/16 threads) after a barrier; ends with a barrier.
+template <int T, int FLAGS>
 __device__ void fft_smem(float2* buf, int N, const float2* __restrict__ tw) {
-  int Ns = 1, rem = N;
-  while (rem % 8 == 0) {
-    stage<8>(buf, N, Ns, tw);
-    Ns *= 8;
-    rem /= 8;
-  }
-  if (rem % 4 == 0) {
-    stage<4>(buf, N, Ns, tw);
-    Ns *= 4;
-    rem /= 4;
-  }
-  if (rem % 2 == 0) {
-    stage<2>(buf, N, Ns, tw);
-    Ns *= 2;
-    rem /= 2;
-  }
-  while (rem % 3 == 0) {
-    stage<3>(buf, N, Ns, tw);
-    Ns *= 3;
-    rem /= 3;
-  }
-  while (rem % 5 == 0) {
-    stage<5>(buf, N, Ns, tw);
-    Ns *= 5;
-    rem /= 5;
+  stage<T, 16, (FLAGS & kZeroUpper) != 0, false>(buf, N, 1, tw);
+  int Ns = 16, rem = N / 16;
+  while (rem > 1) {
+    const int R = (rem % 16 == 0) ? 16 : (rem % 8 == 0) ? 8 : (rem % 4 == 0) ? 4
+                : (rem % 2 == 0) ? 2 : (rem % 3 == 0) ? 3 : 5;
+    if (rem == R && (FLAGS & kLowOut)) stage_any<T, true>(R, buf, N, Ns, tw);
+    else stage_any<T, false>(R, buf, N, Ns, tw);
+    Ns *= R;
+    rem /= R;
   }
 }
 
@@ -225,15 +271,26 @@ __global__ void twiddle_kernel(float2* tw, int N) {
   tw[i] = make_float2((float)c, (float)-s);
 }
 
-// Copies the twiddle table to shared memory (caller synchronises before use).
 __device__ __forceinline__ void load_tw(float2* dst, const float2* __restrict__ src, int N) {
   for (int i = threadIdx.x; i < tw_len(N); i += blockDim.x) dst[i] = src[i];
 }
 
-// ---------------------------------------------------------------- K spectrum rows
-template <int G>
-__global__ void __launch_bounds__(1024)
-kspec_rows_kernel(const GridGeom* __restrict__ geom, int P, float neg_gamma,
+// t-kernel sample (1 + d^2)^-gamma with the integer-gamma fast paths (uniform branch).
+__device__ __forceinline__ float ksample(float s, float neg_gamma, int gi) {
+  switch (gi) {
+    case 1: return pow_neg<1>(s, neg_gamma);
+    case 2: return pow_neg<2>(s, neg_gamma);
+    case 3: return pow_neg<3>(s, neg_gamma);
+    case 4: return pow_neg<4>(s, neg_gamma);
+    case 8: return pow_neg<8>(s, neg_gamma);
+    default: return pow_neg<0>(s, neg_gamma);
+  }
+}
+
+// ---------------------------------------------------------------- K spectrum: rows
+template <int T>
+__global__ void __launch_bounds__(T, kMinBlocks<T>)
+kspec_rows_kernel(const GridGeom* __restrict__ geom, int P, float neg_gamma, int gi,
                   const float2* __restrict__ tw, float* __restrict__ KA, int ka_pitch) {
   extern __shared__ float2 sm[];
   float2* a = sm;
@@ -245,84 +302,39 @@ kspec_rows_kernel(const GridGeom* __restrict__ geom, int P, float neg_gamma,
   if (dya >= M) return;
   const float h2 = g.h * g.h;
   const float scale = 1.0f / ((float)P * (float)P);
-  for (int x = threadIdx.x; x < P; x += blockDim.x) {
+  for (int x = threadIdx.x; x < P; x += T) {
     const int dx = (x <= M - 1) ? x : ((x >= P - (M - 1)) ? x - P : INT32_MAX);
     float va = 0.f, vb = 0.f;
     if (dx != INT32_MAX) {
       const float dx2 = (float)(dx * dx);
-      va = pow_neg<G>(fmaf(h2, dx2 + (float)(dya * dya), 1.0f), neg_gamma) * scale;
-      if (dyb < M) vb = pow_neg<G>(fmaf(h2, dx2 + (float)(dyb * dyb), 1.0f), neg_gamma) * scale;
+      va = ksample(fmaf(h2, dx2 + (float)(dya * dya), 1.0f), neg_gamma, gi) * scale;
+      if (dyb < M) vb = ksample(fmaf(h2, dx2 + (float)(dyb * dyb), 1.0f), neg_gamma, gi) * scale;
     }
     a[pad(x)] = make_float2(va, vb);
   }
   __syncthreads();
-  fft_smem(a, P, tws);
-  const float2* r = a;
-  // real-even rows -> real spectra: row a in Re, row b in Im
-  for (int q = threadIdx.x; q <= P / 2; q += blockDim.x) {
-    const float2 z = r[pad(q)];
+  fft_smem<T, 0>(a, P, tws);
+  for (int q = threadIdx.x; q <= P / 2; q += T) {  // real-even rows: row a in Re, b in Im
+    const float2 z = a[pad(q)];
     KA[(int64_t)q * ka_pitch + dya] = z.x;
     if (dyb < M) KA[(int64_t)q * ka_pitch + dyb] = z.y;
   }
 }
 
-// ---------------------------------------------------------------- forward rows
-__global__ void __launch_bounds__(1024)
-rows_fwd_kernel(const GridGeom* __restrict__ geom, const float* __restrict__ C, int cpitch,
-                int P, const float2* __restrict__ tw, float2* __restrict__ CA, int ca_pitch) {
+// ---------------------------------------------------------------- K spectrum: columns
+template <int T>
+__global__ void __launch_bounds__(T, kMinBlocks<T>)
+kspec_cols_kernel(const GridGeom* __restrict__ geom, const float* __restrict__ KA, int ka_pitch,
+                  int P, const float2* __restrict__ tw, float* __restrict__ KH) {
   extern __shared__ float2 sm[];
   float2* a = sm;
   float2* tws = sm + padded_len(P);
-  load_tw(tws, tw, P);
-  const int M = geom->M;
-  const int ra = 2 * blockIdx.x, rb = ra + 1;
-  if (ra >= M) return;
-  const int ch = blockIdx.y;
-  const float* rowa = C + ((int64_t)ch * cpitch + ra) * cpitch;
-  const float* rowb = rowa + cpitch;
-  const bool hb = rb < M;
-  for (int x = threadIdx.x; x < P; x += blockDim.x) {
-    float va = 0.f, vb = 0.f;
-    if (x < M) {
-      va = rowa[x];
-      if (hb) vb = rowb[x];
-    }
-    a[pad(x)] = make_float2(va, vb);
-  }
-  __syncthreads();
-  fft_smem(a, P, tws);
-  const float2* r = a;
-  const int half = P / 2;
-  float2* out = CA + (int64_t)ch * (half + 1) * ca_pitch;
-  for (int q = threadIdx.x; q <= half; q += blockDim.x) {
-    const float2 z = r[pad(q)];
-    const float2 zc = conjf2(r[pad(q == 0 ? 0 : P - q)]);
-    const float2 xa = make_float2(0.5f * (z.x + zc.x), 0.5f * (z.y + zc.y));
-    const float2 xb = mul_mi(make_float2(0.5f * (z.x - zc.x), 0.5f * (z.y - zc.y)));
-    float2* o = out + (int64_t)q * ca_pitch + ra;
-    if (hb) {
-      *reinterpret_cast<float4*>(o) = make_float4(xa.x, xa.y, xb.x, xb.y);
-    } else {
-      *o = xa;
-    }
-  }
-}
-
-// ---------------------------------------------------------------- columns
-__global__ void __launch_bounds__(1024)
-cols_kernel(const GridGeom* __restrict__ geom, float2* __restrict__ CA, int ca_pitch,
-            const float* __restrict__ KA, int ka_pitch, int P, const float2* __restrict__ tw) {
-  extern __shared__ float2 sm[];
-  float2* a = sm;
-  float2* tws = sm + padded_len(P);
-  float* kh = reinterpret_cast<float*>(tws + tw_len(P));  // [2][P]
   load_tw(tws, tw, P);
   const int M = geom->M;
   const int half = P / 2;
   const int q0 = 2 * blockIdx.x, q1 = q0 + 1;
   const bool h1 = q1 <= half;
-  // K^ columns q0, q1: real-even columns (mirror of dy = 0..M-1) packed as re/im
-  for (int u = threadIdx.x; u < P; u += blockDim.x) {
+  for (int u = threadIdx.x; u < P; u += T) {  // mirror of dy = 0..M-1 (real even)
     const int dy = (u <= M - 1) ? u : ((u >= P - (M - 1)) ? P - u : -1);
     float va = 0.f, vb = 0.f;
     if (dy >= 0) {
@@ -332,46 +344,91 @@ cols_kernel(const GridGeom* __restrict__ geom, float2* __restrict__ CA, int ca_p
     a[pad(u)] = make_float2(va, vb);
   }
   __syncthreads();
-  {
-    fft_smem(a, P, tws);
-  const float2* r = a;
-    for (int u = threadIdx.x; u < P; u += blockDim.x) {
-      const float2 z = r[pad(u)];
-      kh[u] = z.x;
-      kh[P + u] = z.y;
-    }
-    __syncthreads();
+  fft_smem<T, 0>(a, P, tws);
+  for (int u = threadIdx.x; u < P; u += T) {
+    const float2 z = a[pad(u)];
+    KH[(int64_t)q0 * P + u] = z.x;
+    if (h1) KH[(int64_t)q1 * P + u] = z.y;
   }
-  for (int ch = 0; ch < 3; ++ch) {
-    for (int s = 0; s < 2; ++s) {
-      const int q = s ? q1 : q0;
-      if (q > half) break;
-      float2* col = CA + ((int64_t)ch * (half + 1) + q) * ca_pitch;
-      for (int u = threadIdx.x; u < P; u += blockDim.x) a[pad(u)] = (u < M) ? col[u] : make_float2(0.f, 0.f);
-      __syncthreads();
-      fft_smem(a, P, tws);
-      float2* r = a;
-      // multiply by K^ (real) and conjugate for the inverse transform
-      const float* k = kh + s * P;
-      for (int u = threadIdx.x; u < P; u += blockDim.x) {
-        const float2 z = r[pad(u)];
-        const float kk = k[u];
-        r[pad(u)] = make_float2(z.x * kk, -z.y * kk);
-      }
-      __syncthreads();
-      fft_smem(r, P, tws);
-      const float2* ri = r;
-      for (int u = threadIdx.x; u < M; u += blockDim.x) {
-        const float2 z = ri[pad(u)];
-        col[u] = make_float2(z.x, -z.y);
-      }
-      __syncthreads();
+}
+
+// ---------------------------------------------------------------- forward rows
+template <int T>
+__global__ void __launch_bounds__(T, kMinBlocks<T>)
+rows_fwd_kernel(const GridGeom* __restrict__ geom, float* __restrict__ C, int cpitch,
+                int P, const float2* __restrict__ tw, float2* __restrict__ CA, int ca_pitch) {
+  extern __shared__ float2 sm[];
+  float2* a = sm;
+  float2* tws = sm + padded_len(P);
+  load_tw(tws, tw, P);
+  const int M = geom->M;
+  const int ra = 2 * blockIdx.x, rb = ra + 1;
+  if (ra >= M) return;
+  const int ch = blockIdx.y;
+  float* rowa = C + ((int64_t)ch * cpitch + ra) * cpitch;
+  float* rowb = rowa + cpitch;
+  const bool hb = rb < M;
+  const int half = P / 2;
+  for (int x = threadIdx.x; x < half; x += T) {  // [P/2, P) is zero and never read
+    float va = 0.f, vb = 0.f;
+    if (x < M) {
+      va = __ldcs(rowa + x);  // read once: evict-first
+      if (hb) vb = __ldcs(rowb + x);
     }
+    a[pad(x)] = make_float2(va, vb);
+  }
+  // consumed: leave the planes zero for the next spread (stores issued after all loads)
+  for (int x = threadIdx.x; x < M; x += T) {
+    rowa[x] = 0.f;
+    if (hb) rowb[x] = 0.f;
+  }
+  __syncthreads();
+  fft_smem<T, kZeroUpper>(a, P, tws);
+  float2* out = CA + (int64_t)ch * (half + 1) * ca_pitch;
+  for (int q = threadIdx.x; q <= half; q += T) {
+    const float2 z = a[pad(q)];
+    const float2 zc = conjf2(a[pad(q == 0 ? 0 : P - q)]);
+    const float2 xa = make_float2(0.5f * (z.x + zc.x), 0.5f * (z.y + zc.y));
+    const float2 xb = mul_mi(make_float2(0.5f * (z.x - zc.x), 0.5f * (z.y - zc.y)));
+    float2* o = out + (int64_t)q * ca_pitch + ra;
+    if (hb) *reinterpret_cast<float4*>(o) = make_float4(xa.x, xa.y, xb.x, xb.y);
+    else *o = xa;
+  }
+}
+
+// ---------------------------------------------------------------- columns
+template <int T>
+__global__ void __launch_bounds__(T, kMinBlocks<T>)
+cols_kernel(const GridGeom* __restrict__ geom, float2* __restrict__ CA, int ca_pitch,
+            const float* __restrict__ KH, int P, const float2* __restrict__ tw) {
+  extern __shared__ float2 sm[];
+  float2* a = sm;
+  float2* tws = sm + padded_len(P);
+  load_tw(tws, tw, P);
+  const int M = geom->M;
+  const int half = P / 2;
+  const int q = blockIdx.x, ch = blockIdx.y;
+  float2* col = CA + ((int64_t)ch * (half + 1) + q) * ca_pitch;
+  for (int u = threadIdx.x; u < half; u += T) a[pad(u)] = (u < M) ? col[u] : make_float2(0.f, 0.f);
+  __syncthreads();
+  fft_smem<T, kZeroUpper>(a, P, tws);
+  const float* kh = KH + (int64_t)q * P;
+  for (int u = threadIdx.x; u < P; u += T) {  // x K^ (real), conjugated for the inverse
+    const float2 z = a[pad(u)];
+    const float kk = __ldg(kh + u);
+    a[pad(u)] = make_float2(z.x * kk, -z.y * kk);
+  }
+  __syncthreads();
+  fft_smem<T, kLowOut>(a, P, tws);
+  for (int u = threadIdx.x; u < M; u += T) {
+    const float2 z = a[pad(u)];
+    col[u] = make_float2(z.x, -z.y);
   }
 }
 
 // ---------------------------------------------------------------- inverse rows
-__global__ void __launch_bounds__(1024)
+template <int T>
+__global__ void __launch_bounds__(T, kMinBlocks<T>)
 rows_inv_kernel(const GridGeom* __restrict__ geom, const float2* __restrict__ CA, int ca_pitch,
                 int P, const float2* __restrict__ tw, float* __restrict__ Phi, int cpitch) {
   extern __shared__ float2 sm[];
@@ -385,9 +442,9 @@ rows_inv_kernel(const GridGeom* __restrict__ geom, const float2* __restrict__ CA
   const bool hb = rb < M;
   const int half = P / 2;
   const float2* in = CA + (int64_t)ch * (half + 1) * ca_pitch;
-  // Z[q] = Xa[q] + i Xb[q] over the full circle (Hermitian extension); stored conjugated
-  // so that a forward FFT computes the inverse transform.
-  for (int q = threadIdx.x; q < P; q += blockDim.x) {
+  // Z[q] = Xa[q] + i Xb[q] over the full circle (Hermitian extension), stored conjugated so
+  // that the forward FFT computes the inverse.
+  for (int q = threadIdx.x; q < P; q += T) {
     const int qq = (q <= half) ? q : P - q;
     float2 xa, xb = make_float2(0.f, 0.f);
     const float2* p = in + (int64_t)qq * ca_pitch + ra;
@@ -402,16 +459,14 @@ rows_inv_kernel(const GridGeom* __restrict__ geom, const float2* __restrict__ CA
       xa = conjf2(xa);
       xb = conjf2(xb);
     }
-    const float2 z = make_float2(xa.x - xb.y, xa.y + xb.x);  // xa + i xb
-    a[pad(q)] = conjf2(z);
+    a[pad(q)] = conjf2(make_float2(xa.x - xb.y, xa.y + xb.x));  // conj(xa + i xb)
   }
   __syncthreads();
-  fft_smem(a, P, tws);
-  const float2* r = a;
+  fft_smem<T, kLowOut>(a, P, tws);
   float* pa = Phi + ((int64_t)ch * cpitch + ra) * cpitch;
   float* pb = pa + cpitch;
-  for (int x = threadIdx.x; x < M; x += blockDim.x) {
-    const float2 z = r[pad(x)];  // conj(result) = xa + i xb: xa = z.x, xb = -z.y
+  for (int x = threadIdx.x; x < M; x += T) {
+    const float2 z = a[pad(x)];  // conj(result) = xa + i xb
     pa[x] = z.x;
     if (hb) pb[x] = -z.y;
   }
@@ -427,6 +482,43 @@ __global__ void zero_planes_kernel(const GridGeom* __restrict__ geom, float* __r
 
 }  // namespace
 
+// Threads per FFT block: the smallest of {128, 256, 384, 512, 768, 1024} >= P/16 (one
+// radix-16 butterfly per thread).
+int fft_threads(int P) {
+  for (int t : {128, 256, 384, 512, 768, 1024})
+    if (t * 16 >= P) return t;
+  return 1024;
+}
+
+size_t fftconv_smem_bytes(int P) { return (size_t)(padded_len(P) + tw_len(P)) * sizeof(float2); }
+
+#define TFDP_FOR_T(P_, CALL)                               \
+  switch (fft_threads(P_)) {                               \
+    case 128: { constexpr int TT = 128; CALL; } break;     \
+    case 256: { constexpr int TT = 256; CALL; } break;     \
+    case 384: { constexpr int TT = 384; CALL; } break;     \
+    case 512: { constexpr int TT = 512; CALL; } break;     \
+    case 768: { constexpr int TT = 768; CALL; } break;     \
+    default: { constexpr int TT = 1024; CALL; } break;     \
+  }
+
+cudaError_t fftconv_prepare(int P) {
+  const int b = (int)fftconv_smem_bytes(P);
+  cudaError_t e = cudaSuccess;
+#define TFDP_ATTR(fn) \
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+#define TFDP_ATTR_ALL(TT)           \
+  TFDP_ATTR(kspec_rows_kernel<TT>); \
+  TFDP_ATTR(kspec_cols_kernel<TT>); \
+  TFDP_ATTR(rows_fwd_kernel<TT>);   \
+  TFDP_ATTR(cols_kernel<TT>);       \
+  TFDP_ATTR(rows_inv_kernel<TT>);
+  TFDP_FOR_T(P, TFDP_ATTR_ALL(TT));
+#undef TFDP_ATTR_ALL
+#undef TFDP_ATTR
+  return e;
+}
+
 void launch_twiddles(float2* tw, int P, cudaStream_t s) {
   twiddle_kernel<<<(tw_len(P) + 255) / 256, 256, 0, s>>>(tw, P);
 }
@@ -435,65 +527,36 @@ void launch_zero_planes(const GridGeom* geom, float* C, int cpitch, int Mcap, cu
   zero_planes_kernel<<<dim3((unsigned)Mcap, 3), 256, 0, s>>>(geom, C, cpitch);
 }
 
-// Threads per FFT block: >= P/8 (one radix-8 butterfly each), multiple of 32, >= 128.
-int fft_threads(int P) { return std::min(1024, std::max(128, ((P / 8) + 31) / 32 * 32)); }
-
-size_t fftconv_smem_bytes(int P, int which) {
-  // which: 0 rows (2 P float2), 1 cols (2 P float2 + 2 P float)
-  const size_t base = (size_t)(padded_len(P) + tw_len(P)) * sizeof(float2);
-  return which == 0 ? base : base + (size_t)2 * P * sizeof(float);
+void launch_kspec(const GridGeom* geom, int P, int Mcap, ForceArgs fa, const float2* tw,
+                  float* KA, int ka_pitch, float* KH, cudaStream_t s) {
+  const size_t sm = fftconv_smem_bytes(P);
+  TFDP_FOR_T(P, (kspec_rows_kernel<TT><<<(unsigned)((Mcap + 1) / 2), TT, sm, s>>>(
+                    geom, P, -fa.gamma, fa.gamma_int, tw, KA, ka_pitch)));
+  TFDP_FOR_T(P, (kspec_cols_kernel<TT><<<(unsigned)((P / 2 + 2) / 2), TT, sm, s>>>(
+                    geom, KA, ka_pitch, P, tw, KH)));
 }
 
-cudaError_t fftconv_prepare(int P) {
-  const int r = (int)fftconv_smem_bytes(P, 0), c = (int)fftconv_smem_bytes(P, 1);
-  cudaError_t e;
-#define TFDP_ATTR(fn, bytes)                                                              \
-  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (bytes));     \
-  if (e != cudaSuccess) return e;
-  TFDP_ATTR(kspec_rows_kernel<0>, r);
-  TFDP_ATTR(kspec_rows_kernel<1>, r);
-  TFDP_ATTR(kspec_rows_kernel<2>, r);
-  TFDP_ATTR(kspec_rows_kernel<3>, r);
-  TFDP_ATTR(kspec_rows_kernel<4>, r);
-  TFDP_ATTR(kspec_rows_kernel<8>, r);
-  TFDP_ATTR(rows_fwd_kernel, r);
-  TFDP_ATTR(rows_inv_kernel, r);
-  TFDP_ATTR(cols_kernel, c);
-#undef TFDP_ATTR
-  return cudaSuccess;
-}
-
-void launch_kspec_rows(const GridGeom* geom, int P, int Mcap, ForceArgs fa, const float2* tw,
-                       float* KA, int ka_pitch, cudaStream_t s) {
-  const unsigned blocks = (unsigned)((Mcap + 1) / 2);
-  const size_t sm = fftconv_smem_bytes(P, 0);
-  const float ng = -fa.gamma;
-  switch (fa.gamma_int) {
-    case 1: kspec_rows_kernel<1><<<blocks, fft_threads(P), sm, s>>>(geom, P, ng, tw, KA, ka_pitch); break;
-    case 2: kspec_rows_kernel<2><<<blocks, fft_threads(P), sm, s>>>(geom, P, ng, tw, KA, ka_pitch); break;
-    case 3: kspec_rows_kernel<3><<<blocks, fft_threads(P), sm, s>>>(geom, P, ng, tw, KA, ka_pitch); break;
-    case 4: kspec_rows_kernel<4><<<blocks, fft_threads(P), sm, s>>>(geom, P, ng, tw, KA, ka_pitch); break;
-    case 8: kspec_rows_kernel<8><<<blocks, fft_threads(P), sm, s>>>(geom, P, ng, tw, KA, ka_pitch); break;
-    default: kspec_rows_kernel<0><<<blocks, fft_threads(P), sm, s>>>(geom, P, ng, tw, KA, ka_pitch); break;
-  }
-}
-
-void launch_rows_fwd(const GridGeom* geom, const float* C, int cpitch, int P, int Mcap,
+void launch_rows_fwd(const GridGeom* geom, float* C, int cpitch, int P, int Mcap,
                      const float2* tw, float2* CA, int ca_pitch, cudaStream_t s) {
-  rows_fwd_kernel<<<dim3((unsigned)((Mcap + 1) / 2), 3), fft_threads(P), fftconv_smem_bytes(P, 0), s>>>(
-      geom, C, cpitch, P, tw, CA, ca_pitch);
+  const size_t sm = fftconv_smem_bytes(P);
+  TFDP_FOR_T(P, (rows_fwd_kernel<TT><<<dim3((unsigned)((Mcap + 1) / 2), 3), TT, sm, s>>>(
+                    geom, C, cpitch, P, tw, CA, ca_pitch)));
 }
 
-void launch_cols(const GridGeom* geom, float2* CA, int ca_pitch, const float* KA, int ka_pitch,
-                 int P, const float2* tw, cudaStream_t s) {
-  const unsigned blocks = (unsigned)((P / 2 + 1 + 1) / 2);
-  cols_kernel<<<blocks, fft_threads(P), fftconv_smem_bytes(P, 1), s>>>(geom, CA, ca_pitch, KA, ka_pitch, P, tw);
+void launch_cols(const GridGeom* geom, float2* CA, int ca_pitch, const float* KH, int P,
+                 const float2* tw, cudaStream_t s) {
+  const size_t sm = fftconv_smem_bytes(P);
+  TFDP_FOR_T(P, (cols_kernel<TT><<<dim3((unsigned)(P / 2 + 1), 3), TT, sm, s>>>(
+                    geom, CA, ca_pitch, KH, P, tw)));
 }
 
 void launch_rows_inv(const GridGeom* geom, const float2* CA, int ca_pitch, int P, int Mcap,
                      const float2* tw, float* Phi, int cpitch, cudaStream_t s) {
-  rows_inv_kernel<<<dim3((unsigned)((Mcap + 1) / 2), 3), fft_threads(P), fftconv_smem_bytes(P, 0), s>>>(
-      geom, CA, ca_pitch, P, tw, Phi, cpitch);
+  const size_t sm = fftconv_smem_bytes(P);
+  TFDP_FOR_T(P, (rows_inv_kernel<TT><<<dim3((unsigned)((Mcap + 1) / 2), 3), TT, sm, s>>>(
+                    geom, CA, ca_pitch, P, tw, Phi, cpitch)));
 }
+
+#undef TFDP_FOR_T
 
 }  // namespace tfdp

@@ -52,11 +52,14 @@ void launch_exact_finish(const float2* xy, float2* xy_next, int64_t lo, int64_t 
                          cudaStream_t s);
 
 // ibFFT path
-// Box: producers write one BoxKeys partial per block; consumers reduce them in one block.
+// Box: producers merge one block-reduced BoxKeys per block into kBoxSlots slots (atomic
+// min/max); the consumer (one block) reduces the slots and resets them to the identity.
+constexpr int kBoxSlots = 64;
 int bbox_blocks(int64_t n);
-int launch_bbox(const float2* xy, int64_t n, BoxKeys* part, cudaStream_t s);  // returns n_part
-void launch_box_reduce(const BoxKeys* part, int n_part, BoxKeys* keys, cudaStream_t s);
-void launch_setup(const BoxKeys* part, int n_part, BoxKeys* keys, GridGeom* geom, int k,
+void launch_reset_slots(BoxKeys* slots, cudaStream_t s);
+int launch_bbox(const float2* xy, int64_t n, BoxKeys* slots, cudaStream_t s);  // -> n_part
+void launch_box_reduce(BoxKeys* slots, int n_part, BoxKeys* keys, cudaStream_t s);
+void launch_setup(BoxKeys* slots, int n_part, BoxKeys* keys, GridGeom* geom, int k,
                   int n_int_min, int n_int_fixed, int n_int_cap, int P, int pitch,
                   int* capped_flag, cudaStream_t s);
 void launch_spread(const float2* xy, int64_t lo, int64_t cnt, const GridGeom* geom, int k,
@@ -66,12 +69,12 @@ void launch_spread(const float2* xy, int64_t lo, int64_t cnt, const GridGeom* ge
 cudaError_t fftconv_prepare(int P);
 void launch_twiddles(float2* tw, int P, cudaStream_t s);
 void launch_zero_planes(const GridGeom* geom, float* C, int cpitch, int Mcap, cudaStream_t s);
-void launch_kspec_rows(const GridGeom* geom, int P, int Mcap, ForceArgs fa, const float2* tw,
-                       float* KA, int ka_pitch, cudaStream_t s);
-void launch_rows_fwd(const GridGeom* geom, const float* C, int cpitch, int P, int Mcap,
+void launch_kspec(const GridGeom* geom, int P, int Mcap, ForceArgs fa, const float2* tw,
+                  float* KA, int ka_pitch, float* KH, cudaStream_t s);
+void launch_rows_fwd(const GridGeom* geom, float* C, int cpitch, int P, int Mcap,
                      const float2* tw, float2* CA, int ca_pitch, cudaStream_t s);
-void launch_cols(const GridGeom* geom, float2* CA, int ca_pitch, const float* KA, int ka_pitch,
-                 int P, const float2* tw, cudaStream_t s);
+void launch_cols(const GridGeom* geom, float2* CA, int ca_pitch, const float* KH, int P,
+                 const float2* tw, cudaStream_t s);
 void launch_rows_inv(const GridGeom* geom, const float2* CA, int ca_pitch, int P, int Mcap,
                      const float2* tw, float* Phi, int cpitch, cudaStream_t s);
 void launch_gather_update(const float2* xy, float2* xy_next, int64_t lo, int64_t n_local,

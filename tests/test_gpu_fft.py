@@ -56,7 +56,7 @@ def test_fixed_grid_and_fft_size(k):
     rp, col = P.csr_build(n, u, v)
     Ro = O.repulsion_ibfft(X.astype(np.float64), k, n_int_fixed=64)
     outs = []
-    for P_ in (0, {1: 160, 2: 288, 3: 400}[k]):
+    for P_ in (0, {1: 512, 2: 768, 3: 1280}[k]):
         R, _, geo = _fft_forces(n, rp, col, X, k, n_int_fixed=64, fft_size=P_)
         assert geo["n_int"] == 64
         outs.append(R)
