@@ -379,16 +379,10 @@ tfdp_status configure_fft(tfdp_ctx* c, float L) {
                     2 * p.n_int_fixed * k - 1, k);
       cap = p.n_int_fixed;
     }
-    if (P % 256 || P > kMaxFftSize)
-      return fail(c, TFDP_ERR_UNSUPPORTED, "FFT size %d unsupported (multiple of 256, <= %d)", P,
+    if (!tfdp::fft_size_supported(P))
+      return fail(c, TFDP_ERR_UNSUPPORTED,
+                  "FFT size %d unsupported (256 q, q = 2^a 3^b 5^c, b <= 2, c <= 1, <= %d)", P,
                   kMaxFftSize);
-    {
-      int r = P;
-      while (r % 2 == 0) r /= 2;
-      while (r % 3 == 0) r /= 3;
-      while (r % 5 == 0) r /= 5;
-      if (r != 1) return fail(c, TFDP_ERR_UNSUPPORTED, "FFT size %d must be 2^a 3^b 5^c", P);
-    }
     c->P_of_k[k] = P;
     c->cap_of_k[k] = cap;
     if (k_used(c, k)) mcap = std::max(mcap, cap * k);

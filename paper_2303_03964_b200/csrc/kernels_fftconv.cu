@@ -6,15 +6,16 @@
 //               spectrum is real), two rows per complex FFT: KA[q][dy], q = 0..P/2
 //   kspec_cols  two K^ columns per packed real-even FFT: KH[q][u] (real), u = 0..P-1
 //   rows_fwd    two charge rows (a + i b) per complex FFT, untangled into the half
-//               spectra of rows a and b: CA[c][q][row]
+//               spectra of rows a and b: CA[c][q][row]; the consumed rows are re-zeroed
 //   cols        one (channel, column) per block: FFT -> x K^ -> inverse FFT, rows 0..M-1 kept
 //   rows_inv    Hermitian rows, two rows per complex inverse FFT, columns 0..M-1 kept
-// The inputs of every forward FFT are zero beyond P/2 (M <= P/2), so the first radix-8
-// stage skips those loads; every inverse FFT keeps only outputs below P/2, so its last
-// stage stores half.  FFTs are in-place Stockham stages (radix 8, 4, 2, then 3, 5) in
-// shared memory, P % 64 == 0, one float2 of padding per 8 (conflict-free strided stores,
-// address = base + r * stride).  Twiddles come from a two-level fp64-generated table in
-// shared memory (w) and short product chains (w^2 ... w^7).  1/P^2 is folded into K.
+// The inputs of every forward FFT are zero beyond P/2 (M <= P/2), so the first stage skips
+// those loads; every inverse FFT keeps only outputs below P/2, so its last stage stores half.
+// FFTs are in-place Stockham stages (radix 16, then 16/8/4/2, then 3, 5) in shared memory,
+// fully specialised at compile time for each supported P (P % 256 == 0, 2^a 3^b 5^c): every
+// index, stride and loop bound is a constant.  One float2 of padding per 16 makes the
+// strided stores conflict-free.  Twiddles come from a two-level fp64-generated table in
+// shared memory and short product chains.  1/P^2 is folded into the kernel samples.
 #include <algorithm>
 
 #include "device_math.cuh"
@@ -23,6 +24,7 @@
 namespace tfdp {
 
 namespace {
+
 
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
   return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
@@ -169,13 +171,13 @@ __device__ __forceinline__ void twiddles(const float2* __restrict__ tw, int base
   }
 }
 
-// Butterflies per thread of a radix-R stage when blockDim.x >= N / 16.
-template <int R> struct PerThread { static constexpr int value = 16 / R; };
-template <> struct PerThread<3> { static constexpr int value = 6; };
-template <> struct PerThread<5> { static constexpr int value = 4; };
+// Threads per FFT block: the smallest of {128, 256, 384, 512} >= P/16 (one radix-16
+// butterfly per thread).
+__host__ __device__ constexpr int fft_threads_c(int P) {
+  return P <= 2048 ? 128 : P <= 4096 ? 256 : P <= 6144 ? 384 : 512;
+}
 
-// Register cap via min blocks per SM: 64 registers per thread (every non-inlined stage fits
-// in 64 without spills, measured with ptxas), i.e. 1024 threads of FFT work per SM.
+// Register cap via min blocks per SM: 64 registers per thread for blocks of <= 512 threads.
 template <int T>
 constexpr int kMinBlocks = T <= 512 ? 1024 / T : 1;
 
@@ -186,27 +188,26 @@ enum { kZeroUpper = 1, kLowOut = 2 };
 // In-place Stockham autosort stage (Govindaraju et al. 2008 formulation): radix R, size N,
 // sub-transform size Ns (1 for the first stage, else a multiple of 16 since N % 256 == 0 and
 // the first stage is radix 16).  Loads + butterflies into registers, barrier, stores, barrier.
-// Not inlined: each stage needs < 100 registers; inlining the runtime-radix chain costs more.
-template <int T, int R, bool ZERO_UPPER, bool LOW_OUT>
-__device__ __noinline__ void stage(float2* buf, int N, int Ns, const float2* __restrict__ tw) {
-  constexpr int MB = PerThread<R>::value;
-  const int nb = N / R;
-  const int step = nb / Ns;                 // N / (Ns R)
-  const int sin_ = nb + (nb >> 4);          // pad stride of the loads (nb % 16 == 0)
-  const int sout = Ns == 1 ? 1 : Ns + (Ns >> 4);
-  const bool p2 = (Ns & (Ns - 1)) == 0;
+template <int T, int R, int N, int Ns, bool ZERO_UPPER, bool LOW_OUT>
+__device__ __forceinline__ void stage(float2* buf, const float2* __restrict__ tw) {
+  constexpr int nb = N / R;
+  constexpr int MB = (nb + T - 1) / T;  // butterflies per thread
+  constexpr int step = nb / Ns;         // N / (Ns R)
+  constexpr int sin_ = nb + (nb >> 4);  // padded stride of the loads (nb % 16 == 0)
+  constexpr int sout = Ns == 1 ? 1 : Ns + (Ns >> 4);
+  constexpr bool p2 = (Ns & (Ns - 1)) == 0;
   float2 v[MB][R];
 #pragma unroll
   for (int b = 0; b < MB; ++b) {
     const int j = threadIdx.x + b * T;
-    if (j < nb) {
+    if (nb % T == 0 || j < nb) {
       const int pj = j + (j >> 4);
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         if (ZERO_UPPER && 2 * r >= R) v[b][r] = make_float2(0.f, 0.f);
         else v[b][r] = buf[pj + r * sin_];
       }
-      if (Ns > 1) {
+      if constexpr (Ns > 1) {
         const int k = p2 ? (j & (Ns - 1)) : (j % Ns);
         float2 w[R];
         twiddles<R>(tw, k * step, w);
@@ -220,7 +221,7 @@ __device__ __noinline__ void stage(float2* buf, int N, int Ns, const float2* __r
 #pragma unroll
   for (int b = 0; b < MB; ++b) {
     const int j = threadIdx.x + b * T;
-    if (j < nb) {
+    if (nb % T == 0 || j < nb) {
       const int k = Ns == 1 ? 0 : (p2 ? (j & (Ns - 1)) : (j % Ns));
       const int d = (j - k) * R + k;
       const int pd = d + (d >> 4);
@@ -232,34 +233,29 @@ __device__ __noinline__ void stage(float2* buf, int N, int Ns, const float2* __r
   __syncthreads();
 }
 
-template <int T, bool LOW>
-__device__ __forceinline__ void stage_any(int R, float2* buf, int N, int Ns,
-                                          const float2* __restrict__ tw) {
-  switch (R) {
-    case 16: stage<T, 16, false, LOW>(buf, N, Ns, tw); break;
-    case 8: stage<T, 8, false, LOW>(buf, N, Ns, tw); break;
-    case 4: stage<T, 4, false, LOW>(buf, N, Ns, tw); break;
-    case 2: stage<T, 2, false, LOW>(buf, N, Ns, tw); break;
-    case 3: stage<T, 3, false, false>(buf, N, Ns, tw); break;  // odd radix: store all
-    default: stage<T, 5, false, false>(buf, N, Ns, tw); break;
+__host__ __device__ constexpr int next_radix(int rem) {
+  return rem % 16 == 0 ? 16 : rem % 8 == 0 ? 8 : rem % 4 == 0 ? 4 : rem % 2 == 0 ? 2
+       : rem % 3 == 0 ? 3 : 5;
+}
+
+template <int T, int N, int FLAGS, int Ns, int REM>
+__device__ __forceinline__ void fft_rec(float2* buf, const float2* __restrict__ tw) {
+  if constexpr (REM > 1) {
+    constexpr int R = next_radix(REM);
+    constexpr bool first = Ns == 1, last = REM == R;
+    stage<T, R, N, Ns, first && (FLAGS & kZeroUpper) != 0,
+          last && (FLAGS & kLowOut) != 0 && R % 2 == 0>(buf, tw);
+    fft_rec<T, N, FLAGS, Ns * R, REM / R>(buf, tw);
   }
 }
 
 // Forward complex FFT of buf[0..N) in place (padded layout), N = 2^a 3^b 5^c, N % 256 == 0.
 // Radix 16 first (so Ns is a multiple of 16 afterwards), then 16/8/4/2, then 3, 5.  Called
 // by the whole block (T >= N/16 threads) after a barrier; ends with a barrier.
-template <int T, int FLAGS>
-__device__ void fft_smem(float2* buf, int N, const float2* __restrict__ tw) {
-  stage<T, 16, (FLAGS & kZeroUpper) != 0, false>(buf, N, 1, tw);
-  int Ns = 16, rem = N / 16;
-  while (rem > 1) {
-    const int R = (rem % 16 == 0) ? 16 : (rem % 8 == 0) ? 8 : (rem % 4 == 0) ? 4
-                : (rem % 2 == 0) ? 2 : (rem % 3 == 0) ? 3 : 5;
-    if (rem == R && (FLAGS & kLowOut)) stage_any<T, true>(R, buf, N, Ns, tw);
-    else stage_any<T, false>(R, buf, N, Ns, tw);
-    Ns *= R;
-    rem /= R;
-  }
+template <int T, int N, int FLAGS>
+__device__ __forceinline__ void fft_smem(float2* buf, const float2* __restrict__ tw) {
+  static_assert(N % 256 == 0 && T * 16 >= N, "FFT plan");
+  fft_rec<T, N, FLAGS, 1, N>(buf, tw);
 }
 
 __global__ void twiddle_kernel(float2* tw, int N) {
@@ -287,11 +283,15 @@ __device__ __forceinline__ float ksample(float s, float neg_gamma, int gi) {
   }
 }
 
+#define TFDP_FFT_KERNEL(name) \
+  template <int P>            \
+  __global__ void __launch_bounds__(fft_threads_c(P), kMinBlocks<fft_threads_c(P)>) name
+
 // ---------------------------------------------------------------- K spectrum: rows
-template <int T>
-__global__ void __launch_bounds__(T, kMinBlocks<T>)
-kspec_rows_kernel(const GridGeom* __restrict__ geom, int P, float neg_gamma, int gi,
-                  const float2* __restrict__ tw, float* __restrict__ KA, int ka_pitch) {
+TFDP_FFT_KERNEL(kspec_rows_kernel)(const GridGeom* __restrict__ geom, float neg_gamma, int gi,
+                                   const float2* __restrict__ tw, float* __restrict__ KA,
+                                   int ka_pitch) {
+  constexpr int T = fft_threads_c(P);
   extern __shared__ float2 sm[];
   float2* a = sm;
   float2* tws = sm + padded_len(P);
@@ -313,7 +313,7 @@ kspec_rows_kernel(const GridGeom* __restrict__ geom, int P, float neg_gamma, int
     a[pad(x)] = make_float2(va, vb);
   }
   __syncthreads();
-  fft_smem<T, 0>(a, P, tws);
+  fft_smem<T, P, 0>(a, tws);
   for (int q = threadIdx.x; q <= P / 2; q += T) {  // real-even rows: row a in Re, b in Im
     const float2 z = a[pad(q)];
     KA[(int64_t)q * ka_pitch + dya] = z.x;
@@ -322,16 +322,16 @@ kspec_rows_kernel(const GridGeom* __restrict__ geom, int P, float neg_gamma, int
 }
 
 // ---------------------------------------------------------------- K spectrum: columns
-template <int T>
-__global__ void __launch_bounds__(T, kMinBlocks<T>)
-kspec_cols_kernel(const GridGeom* __restrict__ geom, const float* __restrict__ KA, int ka_pitch,
-                  int P, const float2* __restrict__ tw, float* __restrict__ KH) {
+TFDP_FFT_KERNEL(kspec_cols_kernel)(const GridGeom* __restrict__ geom,
+                                   const float* __restrict__ KA, int ka_pitch,
+                                   const float2* __restrict__ tw, float* __restrict__ KH) {
+  constexpr int T = fft_threads_c(P);
   extern __shared__ float2 sm[];
   float2* a = sm;
   float2* tws = sm + padded_len(P);
   load_tw(tws, tw, P);
   const int M = geom->M;
-  const int half = P / 2;
+  constexpr int half = P / 2;
   const int q0 = 2 * blockIdx.x, q1 = q0 + 1;
   const bool h1 = q1 <= half;
   for (int u = threadIdx.x; u < P; u += T) {  // mirror of dy = 0..M-1 (real even)
@@ -344,7 +344,7 @@ kspec_cols_kernel(const GridGeom* __restrict__ geom, const float* __restrict__ K
     a[pad(u)] = make_float2(va, vb);
   }
   __syncthreads();
-  fft_smem<T, 0>(a, P, tws);
+  fft_smem<T, P, 0>(a, tws);
   for (int u = threadIdx.x; u < P; u += T) {
     const float2 z = a[pad(u)];
     KH[(int64_t)q0 * P + u] = z.x;
@@ -353,10 +353,10 @@ kspec_cols_kernel(const GridGeom* __restrict__ geom, const float* __restrict__ K
 }
 
 // ---------------------------------------------------------------- forward rows
-template <int T>
-__global__ void __launch_bounds__(T, kMinBlocks<T>)
-rows_fwd_kernel(const GridGeom* __restrict__ geom, float* __restrict__ C, int cpitch,
-                int P, const float2* __restrict__ tw, float2* __restrict__ CA, int ca_pitch) {
+TFDP_FFT_KERNEL(rows_fwd_kernel)(const GridGeom* __restrict__ geom, float* __restrict__ C,
+                                 int cpitch, const float2* __restrict__ tw,
+                                 float2* __restrict__ CA, int ca_pitch) {
+  constexpr int T = fft_threads_c(P);
   extern __shared__ float2 sm[];
   float2* a = sm;
   float2* tws = sm + padded_len(P);
@@ -368,7 +368,7 @@ rows_fwd_kernel(const GridGeom* __restrict__ geom, float* __restrict__ C, int cp
   float* rowa = C + ((int64_t)ch * cpitch + ra) * cpitch;
   float* rowb = rowa + cpitch;
   const bool hb = rb < M;
-  const int half = P / 2;
+  constexpr int half = P / 2;
   for (int x = threadIdx.x; x < half; x += T) {  // [P/2, P) is zero and never read
     float va = 0.f, vb = 0.f;
     if (x < M) {
@@ -383,7 +383,7 @@ rows_fwd_kernel(const GridGeom* __restrict__ geom, float* __restrict__ C, int cp
     if (hb) rowb[x] = 0.f;
   }
   __syncthreads();
-  fft_smem<T, kZeroUpper>(a, P, tws);
+  fft_smem<T, P, kZeroUpper>(a, tws);
   float2* out = CA + (int64_t)ch * (half + 1) * ca_pitch;
   for (int q = threadIdx.x; q <= half; q += T) {
     const float2 z = a[pad(q)];
@@ -397,21 +397,21 @@ rows_fwd_kernel(const GridGeom* __restrict__ geom, float* __restrict__ C, int cp
 }
 
 // ---------------------------------------------------------------- columns
-template <int T>
-__global__ void __launch_bounds__(T, kMinBlocks<T>)
-cols_kernel(const GridGeom* __restrict__ geom, float2* __restrict__ CA, int ca_pitch,
-            const float* __restrict__ KH, int P, const float2* __restrict__ tw) {
+TFDP_FFT_KERNEL(cols_kernel)(const GridGeom* __restrict__ geom, float2* __restrict__ CA,
+                             int ca_pitch, const float* __restrict__ KH,
+                             const float2* __restrict__ tw) {
+  constexpr int T = fft_threads_c(P);
   extern __shared__ float2 sm[];
   float2* a = sm;
   float2* tws = sm + padded_len(P);
   load_tw(tws, tw, P);
   const int M = geom->M;
-  const int half = P / 2;
+  constexpr int half = P / 2;
   const int q = blockIdx.x, ch = blockIdx.y;
   float2* col = CA + ((int64_t)ch * (half + 1) + q) * ca_pitch;
   for (int u = threadIdx.x; u < half; u += T) a[pad(u)] = (u < M) ? col[u] : make_float2(0.f, 0.f);
   __syncthreads();
-  fft_smem<T, kZeroUpper>(a, P, tws);
+  fft_smem<T, P, kZeroUpper>(a, tws);
   const float* kh = KH + (int64_t)q * P;
   for (int u = threadIdx.x; u < P; u += T) {  // x K^ (real), conjugated for the inverse
     const float2 z = a[pad(u)];
@@ -419,7 +419,7 @@ cols_kernel(const GridGeom* __restrict__ geom, float2* __restrict__ CA, int ca_p
     a[pad(u)] = make_float2(z.x * kk, -z.y * kk);
   }
   __syncthreads();
-  fft_smem<T, kLowOut>(a, P, tws);
+  fft_smem<T, P, kLowOut>(a, tws);
   for (int u = threadIdx.x; u < M; u += T) {
     const float2 z = a[pad(u)];
     col[u] = make_float2(z.x, -z.y);
@@ -427,10 +427,11 @@ cols_kernel(const GridGeom* __restrict__ geom, float2* __restrict__ CA, int ca_p
 }
 
 // ---------------------------------------------------------------- inverse rows
-template <int T>
-__global__ void __launch_bounds__(T, kMinBlocks<T>)
-rows_inv_kernel(const GridGeom* __restrict__ geom, const float2* __restrict__ CA, int ca_pitch,
-                int P, const float2* __restrict__ tw, float* __restrict__ Phi, int cpitch) {
+TFDP_FFT_KERNEL(rows_inv_kernel)(const GridGeom* __restrict__ geom,
+                                 const float2* __restrict__ CA, int ca_pitch,
+                                 const float2* __restrict__ tw, float* __restrict__ Phi,
+                                 int cpitch) {
+  constexpr int T = fft_threads_c(P);
   extern __shared__ float2 sm[];
   float2* a = sm;
   float2* tws = sm + padded_len(P);
@@ -440,7 +441,7 @@ rows_inv_kernel(const GridGeom* __restrict__ geom, const float2* __restrict__ CA
   if (ra >= M) return;
   const int ch = blockIdx.y;
   const bool hb = rb < M;
-  const int half = P / 2;
+  constexpr int half = P / 2;
   const float2* in = CA + (int64_t)ch * (half + 1) * ca_pitch;
   // Z[q] = Xa[q] + i Xb[q] over the full circle (Hermitian extension), stored conjugated so
   // that the forward FFT computes the inverse.
@@ -462,7 +463,7 @@ rows_inv_kernel(const GridGeom* __restrict__ geom, const float2* __restrict__ CA
     a[pad(q)] = conjf2(make_float2(xa.x - xb.y, xa.y + xb.x));  // conj(xa + i xb)
   }
   __syncthreads();
-  fft_smem<T, kLowOut>(a, P, tws);
+  fft_smem<T, P, kLowOut>(a, tws);
   float* pa = Phi + ((int64_t)ch * cpitch + ra) * cpitch;
   float* pb = pa + cpitch;
   for (int x = threadIdx.x; x < M; x += T) {
@@ -472,50 +473,39 @@ rows_inv_kernel(const GridGeom* __restrict__ geom, const float2* __restrict__ CA
   }
 }
 
-__global__ void zero_planes_kernel(const GridGeom* __restrict__ geom, float* __restrict__ C, int cpitch) {
-  const int M = geom->M;
-  const int row = blockIdx.x;
-  if (row >= M) return;
-  float* p = C + ((int64_t)blockIdx.y * cpitch + row) * cpitch;
-  for (int x = threadIdx.x; x < M; x += blockDim.x) p[x] = 0.f;
-}
-
 }  // namespace
 
-// Threads per FFT block: the smallest of {128, 256, 384, 512, 768, 1024} >= P/16 (one
-// radix-16 butterfly per thread).
-int fft_threads(int P) {
-  for (int t : {128, 256, 384, 512, 768, 1024})
-    if (t * 16 >= P) return t;
-  return 1024;
+// Supported FFT sizes: P = 256 q, q = 2^a 3^b 5^c with b <= 2, c <= 1, P <= 8192.
+#define TFDP_FFT_SIZES(X) \
+  X(256) X(512) X(768) X(1024) X(1280) X(1536) X(2048) X(2304) X(2560) X(3072) X(3840) \
+  X(4096) X(4608) X(5120) X(6144) X(7680) X(8192)
+
+bool fft_size_supported(int P) {
+#define TFDP_CASE(S) if (P == S) return true;
+  TFDP_FFT_SIZES(TFDP_CASE)
+#undef TFDP_CASE
+  return false;
 }
 
 size_t fftconv_smem_bytes(int P) { return (size_t)(padded_len(P) + tw_len(P)) * sizeof(float2); }
 
-#define TFDP_FOR_T(P_, CALL)                               \
-  switch (fft_threads(P_)) {                               \
-    case 128: { constexpr int TT = 128; CALL; } break;     \
-    case 256: { constexpr int TT = 256; CALL; } break;     \
-    case 384: { constexpr int TT = 384; CALL; } break;     \
-    case 512: { constexpr int TT = 512; CALL; } break;     \
-    case 768: { constexpr int TT = 768; CALL; } break;     \
-    default: { constexpr int TT = 1024; CALL; } break;     \
-  }
-
 cudaError_t fftconv_prepare(int P) {
   const int b = (int)fftconv_smem_bytes(P);
-  cudaError_t e = cudaSuccess;
-#define TFDP_ATTR(fn) \
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
-#define TFDP_ATTR_ALL(TT)           \
-  TFDP_ATTR(kspec_rows_kernel<TT>); \
-  TFDP_ATTR(kspec_cols_kernel<TT>); \
-  TFDP_ATTR(rows_fwd_kernel<TT>);   \
-  TFDP_ATTR(cols_kernel<TT>);       \
-  TFDP_ATTR(rows_inv_kernel<TT>);
-  TFDP_FOR_T(P, TFDP_ATTR_ALL(TT));
-#undef TFDP_ATTR_ALL
-#undef TFDP_ATTR
+  cudaError_t e = cudaErrorInvalidValue;
+#define TFDP_PREP(S)                                                                          \
+  case S:                                                                                     \
+    e = cudaFuncSetAttribute(kspec_rows_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, b); \
+    if (e == cudaSuccess)                                                                     \
+      e = cudaFuncSetAttribute(kspec_cols_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, b); \
+    if (e == cudaSuccess)                                                                     \
+      e = cudaFuncSetAttribute(rows_fwd_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, b); \
+    if (e == cudaSuccess)                                                                     \
+      e = cudaFuncSetAttribute(cols_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, b); \
+    if (e == cudaSuccess)                                                                     \
+      e = cudaFuncSetAttribute(rows_inv_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, b); \
+    break;
+  switch (P) { TFDP_FFT_SIZES(TFDP_PREP) default: break; }
+#undef TFDP_PREP
   return e;
 }
 
@@ -523,40 +513,54 @@ void launch_twiddles(float2* tw, int P, cudaStream_t s) {
   twiddle_kernel<<<(tw_len(P) + 255) / 256, 256, 0, s>>>(tw, P);
 }
 
-void launch_zero_planes(const GridGeom* geom, float* C, int cpitch, int Mcap, cudaStream_t s) {
-  zero_planes_kernel<<<dim3((unsigned)Mcap, 3), 256, 0, s>>>(geom, C, cpitch);
-}
-
 void launch_kspec(const GridGeom* geom, int P, int Mcap, ForceArgs fa, const float2* tw,
                   float* KA, int ka_pitch, float* KH, cudaStream_t s) {
   const size_t sm = fftconv_smem_bytes(P);
-  TFDP_FOR_T(P, (kspec_rows_kernel<TT><<<(unsigned)((Mcap + 1) / 2), TT, sm, s>>>(
-                    geom, P, -fa.gamma, fa.gamma_int, tw, KA, ka_pitch)));
-  TFDP_FOR_T(P, (kspec_cols_kernel<TT><<<(unsigned)((P / 2 + 2) / 2), TT, sm, s>>>(
-                    geom, KA, ka_pitch, P, tw, KH)));
+#define TFDP_KS(S)                                                                          \
+  case S:                                                                                   \
+    kspec_rows_kernel<S><<<(unsigned)((Mcap + 1) / 2), fft_threads_c(S), sm, s>>>(          \
+        geom, -fa.gamma, fa.gamma_int, tw, KA, ka_pitch);                                   \
+    kspec_cols_kernel<S><<<(unsigned)((S / 2 + 2) / 2), fft_threads_c(S), sm, s>>>(         \
+        geom, KA, ka_pitch, tw, KH);                                                        \
+    break;
+  switch (P) { TFDP_FFT_SIZES(TFDP_KS) default: break; }
+#undef TFDP_KS
 }
 
 void launch_rows_fwd(const GridGeom* geom, float* C, int cpitch, int P, int Mcap,
                      const float2* tw, float2* CA, int ca_pitch, cudaStream_t s) {
   const size_t sm = fftconv_smem_bytes(P);
-  TFDP_FOR_T(P, (rows_fwd_kernel<TT><<<dim3((unsigned)((Mcap + 1) / 2), 3), TT, sm, s>>>(
-                    geom, C, cpitch, P, tw, CA, ca_pitch)));
+#define TFDP_RF(S)                                                                          \
+  case S:                                                                                   \
+    rows_fwd_kernel<S><<<dim3((unsigned)((Mcap + 1) / 2), 3), fft_threads_c(S), sm, s>>>(   \
+        geom, C, cpitch, tw, CA, ca_pitch);                                                 \
+    break;
+  switch (P) { TFDP_FFT_SIZES(TFDP_RF) default: break; }
+#undef TFDP_RF
 }
 
 void launch_cols(const GridGeom* geom, float2* CA, int ca_pitch, const float* KH, int P,
                  const float2* tw, cudaStream_t s) {
   const size_t sm = fftconv_smem_bytes(P);
-  TFDP_FOR_T(P, (cols_kernel<TT><<<dim3((unsigned)(P / 2 + 1), 3), TT, sm, s>>>(
-                    geom, CA, ca_pitch, KH, P, tw)));
+#define TFDP_CO(S)                                                                          \
+  case S:                                                                                   \
+    cols_kernel<S><<<dim3((unsigned)(S / 2 + 1), 3), fft_threads_c(S), sm, s>>>(            \
+        geom, CA, ca_pitch, KH, tw);                                                        \
+    break;
+  switch (P) { TFDP_FFT_SIZES(TFDP_CO) default: break; }
+#undef TFDP_CO
 }
 
 void launch_rows_inv(const GridGeom* geom, const float2* CA, int ca_pitch, int P, int Mcap,
                      const float2* tw, float* Phi, int cpitch, cudaStream_t s) {
   const size_t sm = fftconv_smem_bytes(P);
-  TFDP_FOR_T(P, (rows_inv_kernel<TT><<<dim3((unsigned)((Mcap + 1) / 2), 3), TT, sm, s>>>(
-                    geom, CA, ca_pitch, P, tw, Phi, cpitch)));
+#define TFDP_RI(S)                                                                          \
+  case S:                                                                                   \
+    rows_inv_kernel<S><<<dim3((unsigned)((Mcap + 1) / 2), 3), fft_threads_c(S), sm, s>>>(   \
+        geom, CA, ca_pitch, tw, Phi, cpitch);                                               \
+    break;
+  switch (P) { TFDP_FFT_SIZES(TFDP_RI) default: break; }
+#undef TFDP_RI
 }
-
-#undef TFDP_FOR_T
 
 }  // namespace tfdp

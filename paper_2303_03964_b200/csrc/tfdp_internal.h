@@ -66,9 +66,9 @@ void launch_spread(const float2* xy, int64_t lo, int64_t cnt, const GridGeom* ge
                    float* grid, cudaStream_t s);
 
 // hand-written FFT convolution (kernels_fftconv.cu)
+bool fft_size_supported(int P);  // P = 256 q, q = 2^a 3^b 5^c (b <= 2, c <= 1), P <= 8192
 cudaError_t fftconv_prepare(int P);
 void launch_twiddles(float2* tw, int P, cudaStream_t s);
-void launch_zero_planes(const GridGeom* geom, float* C, int cpitch, int Mcap, cudaStream_t s);
 void launch_kspec(const GridGeom* geom, int P, int Mcap, ForceArgs fa, const float2* tw,
                   float* KA, int ka_pitch, float* KH, cudaStream_t s);
 void launch_rows_fwd(const GridGeom* geom, float* C, int cpitch, int P, int Mcap,
