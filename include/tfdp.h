@@ -157,16 +157,20 @@ tfdp_status tfdp_fft_geometry(tfdp_ctx* ctx, float* box4, int32_t* n_int, int32_
  * the allocated grid holds at that k (TFDP_ERR_STATE unless an ibFFT context). */
 tfdp_status tfdp_fft_plan(const tfdp_ctx* ctx, int32_t k, int32_t* fft_size, int32_t* n_int_cap);
 
-/* Per-kernel device timing (CUDA events around every launch on the ctx stream).
- * tfdp_profile(ctx, 1) resets and enables, 0 disables.  tfdp_profile_read fills up to
- * cap entries: names (static strings), total milliseconds and launch counts; returns the
- * number of kernel kinds (or -1 on error).  Syncs the stream. */
+/* Per-kernel device timing (CUDA events around each launch on the ctx stream).
+ * tfdp_profile(ctx, 1) resets and times every kernel kind, 0 disables.
+ * tfdp_profile_mask(ctx, kinds) resets and times only the kinds whose bit is set (bit i =
+ * entry i of tfdp_profile_read), so a timed region can be instrumented around its dominant
+ * kernel alone.  tfdp_profile_read fills up to cap entries: names (static strings), total
+ * milliseconds and launch counts; returns the number of kernel kinds (or -1 on error).
+ * Syncs the stream. */
 tfdp_status tfdp_profile(tfdp_ctx* ctx, int32_t enable);
+tfdp_status tfdp_profile_mask(tfdp_ctx* ctx, uint32_t kinds);
 int32_t tfdp_profile_read(tfdp_ctx* ctx, const char** names, double* ms, int64_t* launches,
                           int32_t cap);
 
 /* Number of kernel launches this library has issued on the ctx (its own kernels, not
- * cuFFT/NCCL).  For the bench's gpu_launches claim. */
+ * NCCL).  For the bench's gpu_launches claim. */
 int64_t tfdp_launch_count(const tfdp_ctx* ctx);
 
 uint32_t tfdp_warnings(const tfdp_ctx* ctx);

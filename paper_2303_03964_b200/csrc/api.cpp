@@ -104,7 +104,7 @@ struct tfdp_ctx {
   const tfdp::NcclApi* nccl = nullptr;
   ncclComm_t comm = nullptr;
   // profiling
-  bool prof = false;
+  uint32_t prof_mask = 0;  // kernel kinds timed with CUDA events (bit = kind)
   struct Pend {
     int kind;
     cudaEvent_t a, b;
@@ -177,15 +177,16 @@ struct Scope {
   tfdp_ctx* c;
   int kind;
   cudaEvent_t a = nullptr;
-  Scope(tfdp_ctx* c_, int k) : c(c_), kind(k) {
-    if (c->prof) {
+  bool on;
+  Scope(tfdp_ctx* c_, int k) : c(c_), kind(k), on((c_->prof_mask >> k) & 1u) {
+    if (on) {
       a = ev_get(c);
       cudaEventRecord(a, c->stream);
     }
     if (kOwnKernel[k]) c->launches++;
   }
   ~Scope() {
-    if (c->prof) {
+    if (on) {
       cudaEvent_t b = ev_get(c);
       cudaEventRecord(b, c->stream);
       c->pend.push_back({kind, a, b});
@@ -945,13 +946,17 @@ tfdp_status tfdp_fft_plan(const tfdp_ctx* c, int32_t k, int32_t* fft_size, int32
 }
 
 tfdp_status tfdp_profile(tfdp_ctx* c, int32_t enable) {
+  return tfdp_profile_mask(c, enable ? 0xffffffffu : 0u);
+}
+
+tfdp_status tfdp_profile_mask(tfdp_ctx* c, uint32_t kinds) {
   if (!c) return TFDP_ERR_ARG;
   prof_collect(c);
   for (int i = 0; i < K_COUNT; ++i) {
     c->prof_ms[i] = 0;
     c->prof_n[i] = 0;
   }
-  c->prof = enable != 0;
+  c->prof_mask = kinds;
   return TFDP_OK;
 }
 

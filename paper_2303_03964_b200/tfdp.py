@@ -203,6 +203,21 @@ class Layout:
     def profile(self, enable: bool = True):
         check(lib().tfdp_profile(self._ctx, int(enable)), self._ctx)
 
+    def kernel_kinds(self) -> list:
+        """Names of the kernel kinds, in the bit order of profile_only()."""
+        cap = 32
+        names = (C.c_char_p * cap)()
+        k = lib().tfdp_profile_read(self._ctx, names, None, None, cap)
+        return [names[i].decode() for i in range(k)]
+
+    def profile_only(self, kinds):
+        """Time only the named kernel kinds (CUDA events around those launches alone)."""
+        order = self.kernel_kinds()
+        mask = 0
+        for name in kinds:
+            mask |= 1 << order.index(name)
+        check(lib().tfdp_profile_mask(self._ctx, mask), self._ctx)
+
     def profile_read(self) -> dict:
         cap = 32
         names = (C.c_char_p * cap)()
