@@ -49,6 +49,7 @@ typedef enum {
 enum { TFDP_EXACT = 0, TFDP_IBFFT = 1 };                 /* repulsion path (P:454 / P:488) */
 enum { TFDP_COOL_LINEAR = 0, TFDP_COOL_CONSTANT = 1 };    /* integrator readings R2 / R2'   */
 enum { TFDP_DIST_SPREAD_ALL = 0, TFDP_DIST_GRID_ALLREDUCE = 1 }; /* FFT path, p > 1 (§8(e)) */
+enum { TFDP_ORDER_AUTO = 0, TFDP_ORDER_KEEP = 1 };        /* internal node renumbering      */
 
 /* Warning bits (returned by tfdp_warnings; the call itself returns TFDP_OK). */
 enum {
@@ -75,6 +76,10 @@ typedef struct {
   int32_t cooling;     /* TFDP_COOL_LINEAR (eta_t = eta0 (1 - t/T), R2, default) |
                           TFDP_COOL_CONSTANT (eta_t = eta0, R2')                           */
   int32_t dist_mode;   /* TFDP_DIST_SPREAD_ALL (default) | TFDP_DIST_GRID_ALLREDUCE        */
+  int32_t node_order;  /* TFDP_ORDER_AUTO (default): the ibFFT path renumbers nodes internally
+                          in Morton order of the layout (single GPU, n >= 65536) at the start
+                          of each tfdp_step call; all inputs/outputs stay in the caller's
+                          order.  TFDP_ORDER_KEEP: never renumber                          */
 } tfdp_params;
 
 /* Multi-GPU description: one process per GPU.  nccl_uid = 128 bytes from

@@ -32,7 +32,7 @@ enum Kind {
   K_EXACT_FINISH,
   K_BBOX,
   K_SETUP,
-  K_ZERO,
+  K_REORDER,
   K_SPREAD,
   K_KSPEC,
   K_ROWS_FWD,
@@ -43,7 +43,7 @@ enum Kind {
   K_COUNT
 };
 const char* kKindNames[K_COUNT] = {"exact_partial", "exact_finish", "bbox",     "setup",
-                                   "zero_planes",   "spread",       "kspec_rows", "rows_fwd",
+                                   "reorder",       "spread",       "kspec_rows", "rows_fwd",
                                    "cols",          "rows_inv",     "gather_update", "nccl"};
 const bool kOwnKernel[K_COUNT] = {true, true, true, true, true, true,
                                   true, true, true, true, true, false};
@@ -105,6 +105,17 @@ struct tfdp_ctx {
   ncclComm_t comm = nullptr;
   // profiling
   uint32_t prof_mask = 0;  // kernel kinds timed with CUDA events (bit = kind)
+  // internal node order (kernels_reorder.cu): internal slot i holds caller node perm[i]
+  bool reorder = false;
+  int64_t iters_run = 0, reordered_at = -1;
+  int* perm = nullptr;
+  int* inv = nullptr;
+  int* perm2 = nullptr;
+  int* inv2 = nullptr;
+  int64_t* row_ptr_o = nullptr;  // caller-order CSR (source of every rebuild)
+  int32_t* col_o = nullptr;
+  void* rscratch = nullptr;
+  float2* iobuf = nullptr;  // n float2 staging for (un)permuted inputs / outputs
   struct Pend {
     int kind;
     cudaEvent_t a, b;
@@ -570,9 +581,54 @@ tfdp_status check_status(tfdp_ctx* c, bool* capped) {
   *capped = (int)(c->h_status[1] & 0xffffffffu) != 0;
   if (d != ~0ULL) {
     c->errored = true;
-    return fail(c, TFDP_ERR_DIVERGED, "diverged at iter %u node %u", (unsigned)(d >> 32),
-                (unsigned)(d & 0xffffffffu));
+    unsigned node = (unsigned)(d & 0xffffffffu);
+    if (c->reorder) {  // internal slot -> caller's node id
+      int orig = -1;
+      cudaMemcpy(&orig, c->perm + node, sizeof(int), cudaMemcpyDeviceToHost);
+      node = (unsigned)orig;
+    }
+    return fail(c, TFDP_ERR_DIVERGED, "diverged at iter %u node %u", (unsigned)(d >> 32), node);
   }
+  return TFDP_OK;
+}
+
+// Internal Morton renumbering of the nodes (kernels_reorder.cu): box -> keys -> counting
+// sort -> positions, permutation and CSR rebuilt in the new order.  Stream-ordered, no sync.
+tfdp_status reorder_nodes(tfdp_ctx* c) {
+  Scope sc(c, K_REORDER);
+  if (!c->box_valid) {  // else the slots already hold the box of the current positions
+    tfdp::launch_reset_slots(c->box_part, c->stream);
+    tfdp::launch_bbox(c->xy[c->cur], c->n, c->box_part, c->stream);
+    c->launches += 2;
+  }
+  // reduce without consuming: the box is permutation invariant, the next setup reuses it
+  tfdp::launch_box_reduce(c->box_part, tfdp::kBoxSlots, c->keys, c->stream, /*reset=*/false);
+  const int nk = tfdp::launch_reorder(c->xy[c->cur], c->xy[c->cur ^ 1], c->keys, c->perm, c->perm2,
+                                      c->inv2, c->row_ptr_o, c->col_o, c->row_ptr, c->col, c->n,
+                                      c->rscratch, c->stream);
+  c->launches += nk;  // (the scope counts box_reduce)
+  std::swap(c->perm, c->perm2);
+  std::swap(c->inv, c->inv2);
+  c->cur ^= 1;
+  c->box_valid = true;
+  c->n_part = tfdp::kBoxSlots;
+  CUDA_TRY(c, cudaGetLastError());
+  return TFDP_OK;
+}
+
+// Copies n_rows float2 rows from internal order (src, device) to the caller's order (dst,
+// host or device).  Without reordering this is a plain copy.
+tfdp_status copy_out(tfdp_ctx* c, const float2* src, float* dst, int64_t n_rows) {
+  const bool d = is_device_ptr(dst);
+  const float2* from = src;
+  if (c->reorder) {
+    tfdp::launch_unpermute(src, c->perm, n_rows, c->iobuf, c->stream);
+    c->launches++;
+    from = c->iobuf;
+  }
+  CUDA_TRY(c, cudaMemcpyAsync(dst, from, n_rows * sizeof(float2),
+                              d ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->stream));
+  if (!d) CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   return TFDP_OK;
 }
 
@@ -633,6 +689,7 @@ tfdp_status tfdp_params_default(tfdp_params* p) {
   p->t0 = 0;
   p->cooling = TFDP_COOL_LINEAR;
   p->dist_mode = TFDP_DIST_SPREAD_ALL;
+  p->node_order = TFDP_ORDER_AUTO;
   return TFDP_OK;
 }
 
@@ -776,6 +833,20 @@ tfdp_status tfdp_init(tfdp_ctx** out, int64_t n, const int64_t* row_ptr, const i
     c->n_chunks = (int)((n + ch - 1) / ch);
     ALLOC(c->part, (size_t)c->n_chunks * std::max<int64_t>(n_local, 1) * sizeof(double2));
   }
+  c->reorder = p.solver == TFDP_IBFFT && p.node_order == TFDP_ORDER_AUTO && c->world == 1 &&
+               n >= 65536;
+  if (c->reorder) {
+    ALLOC(c->perm, n * sizeof(int));
+    ALLOC(c->inv, n * sizeof(int));
+    ALLOC(c->perm2, n * sizeof(int));
+    ALLOC(c->inv2, n * sizeof(int));
+    ALLOC(c->row_ptr_o, (n + 1) * sizeof(int64_t));
+    ALLOC(c->col_o, std::max<int64_t>(nnz, 1) * sizeof(int32_t));
+    ALLOC(c->rscratch, tfdp::reorder_scratch_bytes(n));
+    ALLOC(c->iobuf, n * sizeof(float2));
+    tfdp::launch_iota(c->perm, c->inv, n, c->stream);
+    c->launches++;
+  }
 #undef ALLOC
   cudaStream_t s = c->stream;
   if (cudaMemcpyAsync(c->xy[0], xy0, n * sizeof(float2),
@@ -787,6 +858,12 @@ tfdp_status tfdp_init(tfdp_ctx** out, int64_t n, const int64_t* row_ptr, const i
       cudaMemsetAsync(c->diverge, 0xff, sizeof(unsigned long long), s) != cudaSuccess ||
       cudaMemsetAsync(c->capped, 0, sizeof(int), s) != cudaSuccess)
     return bail(fail(c, TFDP_ERR_CUDA, "initial copies failed: %s", cudaGetErrorString(cudaGetLastError())));
+  if (c->reorder &&
+      (cudaMemcpyAsync(c->row_ptr_o, c->row_ptr, (n + 1) * sizeof(int64_t),
+                       cudaMemcpyDeviceToDevice, s) != cudaSuccess ||
+       (nnz > 0 && cudaMemcpyAsync(c->col_o, c->col, nnz * sizeof(int32_t),
+                                   cudaMemcpyDeviceToDevice, s) != cudaSuccess)))
+    return bail(fail(c, TFDP_ERR_CUDA, "CSR copy failed"));
   tfdp::launch_reset_slots(c->box_part, s);
   if (p.solver == TFDP_IBFFT) {
     if (xy_dev) {  // box of a device layout: one bbox pass
@@ -833,6 +910,12 @@ tfdp_status tfdp_step(tfdp_ctx* c, int32_t n_iters) {
   if (c->p.cooling == TFDP_COOL_LINEAR && c->t + n_iters > T)
     return fail(c, TFDP_ERR_STATE, "iteration %d + %d exceeds T = %d under linear cooling",
                 c->t, n_iters, T);
+  // locality: renumber at the first call, then whenever 64 iterations ran since the last one
+  if (c->reorder && n_iters >= 8 && (c->reordered_at < 0 || c->iters_run - c->reordered_at >= 64)) {
+    TRY(reorder_nodes(c));
+    c->reordered_at = c->iters_run;
+  }
+  c->iters_run += n_iters;
   int done = 0;
   while (done < n_iters) {
     const int block = std::min(n_iters - done, 32);  // host check every 32 iterations
@@ -858,35 +941,19 @@ tfdp_status tfdp_forces(tfdp_ctx* c, float* rep_xy, float* att_xy) {
   TRY(evaluate(c, 0, 0.f, k_at(c, c->t)));
   c->box_valid = false;  // setup consumed the box keys without an update
   const int64_t n_local = c->hi - c->lo;
-  bool host_out = false;
-  if (rep_xy) {
-    const bool d = is_device_ptr(rep_xy);
-    host_out |= !d;
-    CUDA_TRY(c, cudaMemcpyAsync(rep_xy, c->rep, n_local * sizeof(float2),
-                                d ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->stream));
-  }
-  if (att_xy) {
-    const bool d = is_device_ptr(att_xy);
-    host_out |= !d;
-    CUDA_TRY(c, cudaMemcpyAsync(att_xy, c->att, n_local * sizeof(float2),
-                                d ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->stream));
-  }
+  if (rep_xy) TRY(copy_out(c, c->rep, rep_xy, n_local));
+  if (att_xy) TRY(copy_out(c, c->att, att_xy, n_local));
   bool capped = false;
   TRY(check_status(c, &capped));
   TRY(maybe_replan(c, capped));
   c->box_valid = false;
-  (void)host_out;
   return TFDP_OK;
 }
 
 tfdp_status tfdp_layout(tfdp_ctx* c, float* xy_out) {
   if (!c || !xy_out) return fail(c, TFDP_ERR_ARG, "NULL argument");
   cudaSetDevice(c->device);
-  const bool d = is_device_ptr(xy_out);
-  CUDA_TRY(c, cudaMemcpyAsync(xy_out, c->xy[c->cur], c->n * sizeof(float2),
-                              d ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->stream));
-  if (!d) CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-  return TFDP_OK;
+  return copy_out(c, c->xy[c->cur], xy_out, c->n);
 }
 
 tfdp_status tfdp_set_layout(tfdp_ctx* c, const float* xy) {
@@ -897,8 +964,13 @@ tfdp_status tfdp_set_layout(tfdp_ctx* c, const float* xy) {
     for (int64_t i = 0; i < 2 * c->n; ++i)
       if (!std::isfinite(xy[i]))
         return fail(c, TFDP_ERR_ARG, "layout non-finite at node %lld", (long long)(i / 2));
-  CUDA_TRY(c, cudaMemcpyAsync(c->xy[c->cur], xy, c->n * sizeof(float2),
+  float2* dst = c->reorder ? c->iobuf : c->xy[c->cur];
+  CUDA_TRY(c, cudaMemcpyAsync(dst, xy, c->n * sizeof(float2),
                               d ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->stream));
+  if (c->reorder) {  // caller order -> internal order
+    tfdp::launch_permute(c->iobuf, c->perm, c->n, c->xy[c->cur], c->stream);
+    c->launches++;
+  }
   c->box_valid = false;
   return TFDP_OK;
 }
@@ -1016,6 +1088,14 @@ void tfdp_destroy(tfdp_ctx* c) {
   cudaFree(c->kh);
   cudaFree(c->keys);
   cudaFree(c->box_part);
+  cudaFree(c->perm);
+  cudaFree(c->inv);
+  cudaFree(c->perm2);
+  cudaFree(c->inv2);
+  cudaFree(c->row_ptr_o);
+  cudaFree(c->col_o);
+  cudaFree(c->rscratch);
+  cudaFree(c->iobuf);
   cudaFree(c->geom);
   if (c->h_status) cudaFreeHost(c->h_status);
   if (c->comm && c->nccl) c->nccl->CommDestroy(c->comm);

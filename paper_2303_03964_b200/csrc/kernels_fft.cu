@@ -55,8 +55,8 @@ __device__ __forceinline__ void reset_slots(BoxKeys* slots) {
     slots[i] = BoxKeys{0xffffffffu, 0xffffffffu, 0u, 0u};
 }
 
-// One block reduces the n_part slots, then resets them (all threads return the result).
-__device__ BoxKeys block_reduce_partials(BoxKeys* part, int n_part) {
+// One block reduces the n_part slots, then (reset) resets them; all threads return the result.
+__device__ BoxKeys block_reduce_partials(BoxKeys* part, int n_part, bool reset = true) {
   unsigned kx0 = 0xffffffffu, ky0 = 0xffffffffu, kx1 = 0u, ky1 = 0u;
   for (int i = threadIdx.x; i < n_part; i += blockDim.x) {
     const BoxKeys b = part[i];
@@ -89,7 +89,7 @@ __device__ BoxKeys block_reduce_partials(BoxKeys* part, int n_part) {
     if (lane == 0) r[0] = BoxKeys{kx0, ky0, kx1, ky1};
   }
   __syncthreads();  // all slot reads are done
-  reset_slots(part);
+  if (reset) reset_slots(part);
   return r[0];
 }
 
@@ -108,8 +108,9 @@ bbox_kernel(const float2* __restrict__ xy, int64_t n, BoxKeys* part) {
   block_box_commit(kx0, ky0, kx1, ky1, part);
 }
 
-__global__ void __launch_bounds__(64) box_reduce_kernel(BoxKeys* part, int n_part, BoxKeys* keys) {
-  const BoxKeys b = block_reduce_partials(part, n_part);
+__global__ void __launch_bounds__(64)
+box_reduce_kernel(BoxKeys* part, int n_part, BoxKeys* keys, int reset) {
+  const BoxKeys b = block_reduce_partials(part, n_part, reset != 0);
   if (threadIdx.x == 0) *keys = b;
 }
 
@@ -126,8 +127,8 @@ int launch_bbox(const float2* xy, int64_t n, BoxKeys* part, cudaStream_t s) {
   return kBoxSlots;
 }
 
-void launch_box_reduce(BoxKeys* part, int n_part, BoxKeys* keys, cudaStream_t s) {
-  box_reduce_kernel<<<1, 64, 0, s>>>(part, n_part, keys);
+void launch_box_reduce(BoxKeys* part, int n_part, BoxKeys* keys, cudaStream_t s, bool reset) {
+  box_reduce_kernel<<<1, 64, 0, s>>>(part, n_part, keys, reset ? 1 : 0);
 }
 
 // ------------------------------------------------------------------ setup

@@ -58,7 +58,8 @@ constexpr int kBoxSlots = 64;
 int bbox_blocks(int64_t n);
 void launch_reset_slots(BoxKeys* slots, cudaStream_t s);
 int launch_bbox(const float2* xy, int64_t n, BoxKeys* slots, cudaStream_t s);  // -> n_part
-void launch_box_reduce(BoxKeys* slots, int n_part, BoxKeys* keys, cudaStream_t s);
+void launch_box_reduce(BoxKeys* slots, int n_part, BoxKeys* keys, cudaStream_t s,
+                       bool reset = true);
 void launch_setup(BoxKeys* slots, int n_part, BoxKeys* keys, GridGeom* geom, int k,
                   int n_int_min, int n_int_fixed, int n_int_cap, int P, int pitch,
                   int* capped_flag, cudaStream_t s);
@@ -77,6 +78,15 @@ void launch_cols(const GridGeom* geom, float2* CA, int ca_pitch, const float* KH
                  const float2* tw, cudaStream_t s);
 void launch_rows_inv(const GridGeom* geom, const float2* CA, int ca_pitch, int P, int Mcap,
                      const float2* tw, float* Phi, int cpitch, cudaStream_t s);
+// internal node renumbering (kernels_reorder.cu)
+size_t reorder_scratch_bytes(int64_t n);
+void launch_iota(int* perm, int* inv, int64_t n, cudaStream_t s);
+int launch_reorder(const float2* xy_old, float2* xy_new, const BoxKeys* box, const int* perm_old,
+                   int* perm_new, int* inv_new, const int64_t* row_ptr_o, const int32_t* col_o,
+                   int64_t* row_ptr_p, int32_t* col_p, int64_t n, void* scratch, cudaStream_t s);
+void launch_unpermute(const float2* in, const int* perm, int64_t n, float2* out, cudaStream_t s);
+void launch_permute(const float2* in, const int* perm, int64_t n, float2* out, cudaStream_t s);
+
 void launch_gather_update(const float2* xy, float2* xy_next, int64_t lo, int64_t n_local,
                           const GridGeom* geom, int k, const float* phi,
                           const int64_t* row_ptr, const int32_t* col, ForceArgs fa,

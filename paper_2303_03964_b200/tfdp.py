@@ -37,6 +37,7 @@ class Params:
     t0: int = 0
     cooling: str = "linear"  # "linear" (R2) | "constant" (R2')
     dist_mode: str = "spread_all"  # "spread_all" | "grid_allreduce"
+    node_order: str = "auto"  # "auto" (internal Morton renumbering, ibFFT) | "keep"
     dim: int = 2
 
     def to_c(self) -> _L.tfdp_params:
@@ -49,6 +50,7 @@ class Params:
         p.step0, p.iterations, p.t0 = self.step0, self.iterations, self.t0
         p.cooling = {"linear": _L.COOL_LINEAR, "constant": _L.COOL_CONSTANT}[self.cooling]
         p.dist_mode = {"spread_all": _L.DIST_SPREAD_ALL, "grid_allreduce": _L.DIST_GRID_ALLREDUCE}[self.dist_mode]
+        p.node_order = {"auto": 0, "keep": 1}[self.node_order]
         return p
 
 
