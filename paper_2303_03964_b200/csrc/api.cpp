@@ -56,6 +56,11 @@ struct tfdp_ctx {
   int rank = 0, world = 1, device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
+  // side stream: the kernel spectrum (depends only on the grid geometry) runs concurrently
+  // with spread + rows_fwd; fork/join with events, so the ctx stream order is preserved
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  bool kspec_overlap = true;  // env TFDP_KSPEC_OVERLAP=0 runs it in line (tuning / A-B)
   float2* xy[2] = {nullptr, nullptr};
   int cur = 0;
   int64_t* row_ptr = nullptr;
@@ -189,17 +194,19 @@ struct Scope {
   int kind;
   cudaEvent_t a = nullptr;
   bool on;
-  Scope(tfdp_ctx* c_, int k) : c(c_), kind(k), on((c_->prof_mask >> k) & 1u) {
+  cudaStream_t st;
+  Scope(tfdp_ctx* c_, int k, cudaStream_t s = nullptr)
+      : c(c_), kind(k), on((c_->prof_mask >> k) & 1u), st(s ? s : c_->stream) {
     if (on) {
       a = ev_get(c);
-      cudaEventRecord(a, c->stream);
+      cudaEventRecord(a, st);
     }
     if (kOwnKernel[k]) c->launches++;
   }
   ~Scope() {
     if (on) {
       cudaEvent_t b = ev_get(c);
-      cudaEventRecord(b, c->stream);
+      cudaEventRecord(b, st);
       c->pend.push_back({kind, a, b});
     }
   }
@@ -503,6 +510,21 @@ tfdp_status evaluate(tfdp_ctx* c, int update, float eta, int k) {
                          c->p.n_int_fixed, c->cap_of_k[k],
                          P, c->cpitch, c->capped, c->stream);
     }
+    // The kernel spectrum needs only the geometry: fork it onto the side stream so it overlaps
+    // spread + rows_fwd (both latency-bound); cols joins on it.
+    // (in line while kspec itself is being timed, so that its events measure the kernel
+    // rather than its wait for SMs)
+    const bool overlap = c->kspec_overlap && !((c->prof_mask >> K_KSPEC) & 1u);
+    cudaStream_t ks = overlap ? c->side : c->stream;
+    if (overlap) {
+      CUDA_TRY(c, cudaEventRecord(c->ev_fork, c->stream));
+      CUDA_TRY(c, cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+    }
+    {
+      Scope sc(c, K_KSPEC, ks);
+      tfdp::launch_kspec(c->geom, P, mcap, c->fa, tw, c->ka, c->cpitch, c->kh, ks);
+    }
+    if (overlap) CUDA_TRY(c, cudaEventRecord(c->ev_join, c->side));
     // The charge planes are all-zero here: they start zeroed and rows_fwd clears every row
     // it consumes (no separate zeroing pass).
     const bool allreduce = c->world > 1 && c->p.dist_mode == TFDP_DIST_GRID_ALLREDUCE;
@@ -527,13 +549,10 @@ tfdp_status evaluate(tfdp_ctx* c, int update, float eta, int k) {
       NCCL_TRY(c, c->nccl->GroupEnd());
     }
     {
-      Scope sc(c, K_KSPEC);
-      tfdp::launch_kspec(c->geom, P, mcap, c->fa, tw, c->ka, c->cpitch, c->kh, c->stream);
-    }
-    {
       Scope sc(c, K_ROWS_FWD);
       tfdp::launch_rows_fwd(c->geom, c->grid, c->cpitch, P, mcap, tw, c->ca, c->ca_pitch, c->stream);
     }
+    if (overlap) CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_join, 0));
     {
       Scope sc(c, K_COLS);
       tfdp::launch_cols(c->geom, c->ca, c->ca_pitch, c->kh, P, tw, c->stream);
@@ -797,6 +816,11 @@ tfdp_status tfdp_init(tfdp_ctx** out, int64_t n, const int64_t* row_ptr, const i
       return bail(fail(c, TFDP_ERR_CUDA, "cudaStreamCreate failed"));
     c->own_stream = true;
   }
+  if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess)
+    return bail(fail(c, TFDP_ERR_CUDA, "side stream / events"));
+  if (const char* e = getenv("TFDP_KSPEC_OVERLAP")) c->kspec_overlap = atoi(e) != 0;
   const bool xy_dev = is_device_ptr(xy0);
   float L0 = 1.f;
   if (!xy_dev) {
@@ -1099,6 +1123,12 @@ void tfdp_destroy(tfdp_ctx* c) {
   cudaFree(c->geom);
   if (c->h_status) cudaFreeHost(c->h_status);
   if (c->comm && c->nccl) c->nccl->CommDestroy(c->comm);
+  if (c->side) {
+    cudaStreamSynchronize(c->side);
+    cudaStreamDestroy(c->side);
+  }
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }

@@ -369,6 +369,7 @@ TFDP_FFT_KERNEL(rows_fwd_kernel)(const GridGeom* __restrict__ geom, float* __res
   float* rowb = rowa + cpitch;
   const bool hb = rb < M;
   constexpr int half = P / 2;
+#pragma unroll
   for (int x = threadIdx.x; x < half; x += T) {  // [P/2, P) is zero and never read
     float va = 0.f, vb = 0.f;
     if (x < M) {
@@ -409,10 +410,12 @@ TFDP_FFT_KERNEL(cols_kernel)(const GridGeom* __restrict__ geom, float2* __restri
   constexpr int half = P / 2;
   const int q = blockIdx.x, ch = blockIdx.y;
   float2* col = CA + ((int64_t)ch * (half + 1) + q) * ca_pitch;
+#pragma unroll
   for (int u = threadIdx.x; u < half; u += T) a[pad(u)] = (u < M) ? col[u] : make_float2(0.f, 0.f);
   __syncthreads();
   fft_smem<T, P, kZeroUpper>(a, tws);
   const float* kh = KH + (int64_t)q * P;
+#pragma unroll 4
   for (int u = threadIdx.x; u < P; u += T) {  // x K^ (real), conjugated for the inverse
     const float2 z = a[pad(u)];
     const float kk = __ldg(kh + u);
@@ -445,6 +448,7 @@ TFDP_FFT_KERNEL(rows_inv_kernel)(const GridGeom* __restrict__ geom,
   const float2* in = CA + (int64_t)ch * (half + 1) * ca_pitch;
   // Z[q] = Xa[q] + i Xb[q] over the full circle (Hermitian extension), stored conjugated so
   // that the forward FFT computes the inverse.
+#pragma unroll 8
   for (int q = threadIdx.x; q < P; q += T) {
     const int qq = (q <= half) ? q : P - q;
     float2 xa, xb = make_float2(0.f, 0.f);
