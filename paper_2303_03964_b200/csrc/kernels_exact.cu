@@ -2,65 +2,131 @@
 // + position update — sm_100a.
 //
 // exact_partial: unit of work = (block of 1024 targets, source chunk c).  Each thread
-// holds kExactTPT targets in registers; sources are staged through shared memory in
-// tiles of kExactTile float2 and read back as warp-wide broadcasts, so one LDS.64 feeds
-// kExactTPT pair evaluations.  Per pair (gamma = 2): 2 FADD, 2 FFMA (s = 1 + d^2),
-// 1 MUFU.RCP, 1 FMUL, 2 FFMA (accumulate) — the FP32/SFU-pipe bound of DESIGN.md §Kernels.
-// Sums: fp32 within a tile (<= 1024 terms), fp64 across tiles and chunks.  Source chunks
-// depend on n only, and every target sums its chunks in index order, so the forces are
-// bitwise identical for any number of target shards (R15).
+// holds kExactTPT targets in registers; sources are staged through shared memory as two
+// float arrays (x, y) and read back in pairs (j, j+1) as warp-wide LDS.64 broadcasts.  The
+// pair arithmetic runs on packed fp32x2 instructions (sm_100a FADD2 / FFMA2 / FMUL2) with
+// lanes = the two sources: per two pairs (gamma = 2) 2 FADD2 (dx, dy), 2 FFMA2 (s = 1 + d^2),
+// 2 MUFU.RCP, 1 FMUL2 (w^2), 2 FFMA2 (accumulate) = 4.5 issue slots per pair, so the kernel
+// is bound by the SFU (one MUFU.RCP per pair) — DESIGN.md §Kernels.  Sums: fp32 within a
+// tile (<= 1024 terms, even and odd sources in separate lanes), fp64 across tiles and
+// chunks.  Source chunks depend on n only, and every target sums its chunks in index order,
+// so the forces are bitwise identical for any number of target shards (R15).
 #include "device_math.cuh"
 #include "tfdp_internal.h"
 
 namespace tfdp {
 
+namespace {
+using u64 = unsigned long long;
+__device__ __forceinline__ u64 pk(float a, float b) {
+  u64 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void upk(u64 v, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ u64 fma2(u64 a, u64 b, u64 c) {
+  u64 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ u64 sub2(u64 a, u64 b) {
+  u64 d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ u64 mul2(u64 a, u64 b) {
+  u64 d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
+// (1 + d^2)^-gamma for the two lanes of s
+template <int G>
+__device__ __forceinline__ u64 weight2(u64 s, float neg_gamma) {
+  float s1, s2;
+  upk(s, s1, s2);
+  if constexpr (G == 2) {
+    const u64 w = pk(rcp_approx(s1), rcp_approx(s2));
+    return mul2(w, w);
+  } else {
+    return pk(pow_neg<G>(s1, neg_gamma), pow_neg<G>(s2, neg_gamma));
+  }
+}
+}  // namespace
+
 template <int G>
 __global__ void __launch_bounds__(kExactThreads)
 exact_partial_kernel(const float2* __restrict__ xy, int64_t n, int64_t lo, int64_t n_local,
                      int64_t chunk, float neg_gamma, double2* __restrict__ part) {
-  __shared__ float2 tile[kExactTile];
+  __shared__ __align__(16) float xs[kExactTile];
+  __shared__ __align__(16) float ys[kExactTile];
   const int c = blockIdx.y;
   const int64_t src_begin = (int64_t)c * chunk;
   const int64_t src_end = min(n, src_begin + chunk);
   const int64_t tbase = (int64_t)blockIdx.x * kExactTargetsPerBlock + threadIdx.x;
 
-  float tx[kExactTPT], ty[kExactTPT];
+  u64 tx[kExactTPT], ty[kExactTPT];  // (x_i, x_i), (y_i, y_i)
   double ax[kExactTPT], ay[kExactTPT];
 #pragma unroll
   for (int r = 0; r < kExactTPT; ++r) {
     const int64_t t = tbase + (int64_t)r * kExactThreads;
     const float2 p = (t < n_local) ? xy[lo + t] : make_float2(0.f, 0.f);
-    tx[r] = p.x;
-    ty[r] = p.y;
+    tx[r] = pk(p.x, p.x);
+    ty[r] = pk(p.y, p.y);
     ax[r] = 0.0;
     ay[r] = 0.0;
   }
+  const u64 one = pk(1.0f, 1.0f);
 
   for (int64_t base = src_begin; base < src_end; base += kExactTile) {
     const int cnt = (int)min((int64_t)kExactTile, src_end - base);
     __syncthreads();
-    for (int j = threadIdx.x; j < cnt; j += kExactThreads) tile[j] = xy[base + j];
+    for (int j = threadIdx.x; j < cnt; j += kExactThreads) {
+      const float2 p = xy[base + j];
+      xs[j] = p.x;
+      ys[j] = p.y;
+    }
     __syncthreads();
-    float fx[kExactTPT], fy[kExactTPT];
+    u64 fx[kExactTPT], fy[kExactTPT];  // lanes: even / odd sources of the tile
 #pragma unroll
-    for (int r = 0; r < kExactTPT; ++r) fx[r] = fy[r] = 0.f;
-#pragma unroll 4
-    for (int j = 0; j < cnt; ++j) {
-      const float2 q = tile[j];
+    for (int r = 0; r < kExactTPT; ++r) fx[r] = fy[r] = pk(0.f, 0.f);
+    const int cnt2 = cnt & ~1;
+#pragma unroll 2
+    for (int j = 0; j < cnt2; j += 2) {
+      const u64 qx = *reinterpret_cast<const u64*>(xs + j);  // (x_j, x_j+1)
+      const u64 qy = *reinterpret_cast<const u64*>(ys + j);
 #pragma unroll
       for (int r = 0; r < kExactTPT; ++r) {
-        const float dx = tx[r] - q.x;  // r_ij = x_i - x_j
-        const float dy = ty[r] - q.y;
-        const float s = fmaf(dx, dx, fmaf(dy, dy, 1.0f));  // 1 + |r_ij|^2
-        const float wgt = pow_neg<G>(s, neg_gamma);        // (1 + d^2)^-gamma
-        fx[r] = fmaf(wgt, dx, fx[r]);
-        fy[r] = fmaf(wgt, dy, fy[r]);
+        const u64 dx = sub2(tx[r], qx);  // r_ij = x_i - x_j
+        const u64 dy = sub2(ty[r], qy);
+        const u64 s = fma2(dy, dy, fma2(dx, dx, one));  // 1 + |r_ij|^2
+        const u64 w = weight2<G>(s, neg_gamma);         // (1 + d^2)^-gamma
+        fx[r] = fma2(w, dx, fx[r]);
+        fy[r] = fma2(w, dy, fy[r]);
+      }
+    }
+    if (cnt2 < cnt) {  // odd tail: one source in lane 0, lane 1 contributes 0
+      const u64 qx = pk(xs[cnt2], 0.f), qy = pk(ys[cnt2], 0.f);
+      const u64 lane0 = pk(1.0f, 0.0f);
+#pragma unroll
+      for (int r = 0; r < kExactTPT; ++r) {
+        const u64 dx = mul2(sub2(tx[r], qx), lane0);
+        const u64 dy = mul2(sub2(ty[r], qy), lane0);
+        const u64 s = fma2(dy, dy, fma2(dx, dx, one));
+        const u64 w = weight2<G>(s, neg_gamma);
+        fx[r] = fma2(w, dx, fx[r]);
+        fy[r] = fma2(w, dy, fy[r]);
       }
     }
 #pragma unroll
     for (int r = 0; r < kExactTPT; ++r) {
-      ax[r] += (double)fx[r];
-      ay[r] += (double)fy[r];
+      float a0, a1, b0, b1;
+      upk(fx[r], a0, a1);
+      upk(fy[r], b0, b1);
+      ax[r] += (double)a0 + (double)a1;
+      ay[r] += (double)b0 + (double)b1;
     }
   }
 #pragma unroll
