@@ -26,11 +26,16 @@ namespace tfdp {
 namespace {
 
 
+// Complex arithmetic on packed fp32x2 (sm_100a FADD2 / FMUL2 / FFMA2): a complex add is one
+// instruction, a complex product two.
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
-  return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+  return __ffma2_rn(make_float2(a.y, a.y), make_float2(-b.y, b.x),
+                    __fmul2_rn(make_float2(a.x, a.x), b));
 }
-__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) {
+  return __ffma2_rn(b, make_float2(-1.0f, -1.0f), a);
+}
 __device__ __forceinline__ float2 conjf2(float2 a) { return make_float2(a.x, -a.y); }
 __device__ __forceinline__ float2 mul_mi(float2 a) { return make_float2(a.y, -a.x); }  // * (-i)
 
@@ -408,7 +413,8 @@ TFDP_FFT_KERNEL(cols_kernel)(const GridGeom* __restrict__ geom, float2* __restri
   load_tw(tws, tw, P);
   const int M = geom->M;
   constexpr int half = P / 2;
-  const int q = blockIdx.x, ch = blockIdx.y;
+  // the three channels of one column are consecutive blocks: they share the K^ column in L2
+  const int q = blockIdx.x / 3, ch = blockIdx.x % 3;
   float2* col = CA + ((int64_t)ch * (half + 1) + q) * ca_pitch;
 #pragma unroll
   for (int u = threadIdx.x; u < half; u += T) a[pad(u)] = (u < M) ? col[u] : make_float2(0.f, 0.f);
@@ -548,7 +554,7 @@ void launch_cols(const GridGeom* geom, float2* CA, int ca_pitch, const float* KH
   const size_t sm = fftconv_smem_bytes(P);
 #define TFDP_CO(S)                                                                          \
   case S:                                                                                   \
-    cols_kernel<S><<<dim3((unsigned)(S / 2 + 1), 3), fft_threads_c(S), sm, s>>>(            \
+    cols_kernel<S><<<(unsigned)(3 * (S / 2 + 1)), fft_threads_c(S), sm, s>>>(               \
         geom, CA, ca_pitch, KH, tw);                                                        \
     break;
   switch (P) { TFDP_FFT_SIZES(TFDP_CO) default: break; }
