@@ -111,15 +111,26 @@ __device__ __forceinline__ void dft<8>(float2 (&v)[8]) {
 
 // DFT-16 as 4 x 4 (Cooley-Tukey, r = 4 r1 + r2, s = s1 + 4 s2): DFT-4 over r1, twiddle
 // W16^(r2 s1), DFT-4 over r2; outputs written back in natural order.
-template <>
-__device__ __forceinline__ void dft<16>(float2 (&v)[16]) {
+// ZU: inputs v[8..15] are zero (first stage of a zero-padded forward FFT): the first-level
+// DFT-4s of (a, b, 0, 0) reduce to (a + b, a - i b, a - b, a + i b).  (The compiler cannot
+// fold x + 0 in IEEE arithmetic, hence the explicit variant.)
+template <bool ZU = false>
+__device__ __forceinline__ void dft16(float2 (&v)[16]) {
   float2 y[4][4];  // y[r2][s1]
 #pragma unroll
   for (int r2 = 0; r2 < 4; ++r2) {
-    float2 t[4] = {v[r2], v[r2 + 4], v[r2 + 8], v[r2 + 12]};
-    dft<4>(t);
+    if constexpr (ZU) {
+      const float2 a = v[r2], b = v[r2 + 4], ib = mul_mi(b);  // -i b
+      y[r2][0] = cadd(a, b);
+      y[r2][1] = cadd(a, ib);
+      y[r2][2] = csub(a, b);
+      y[r2][3] = csub(a, ib);
+    } else {
+      float2 t[4] = {v[r2], v[r2 + 4], v[r2 + 8], v[r2 + 12]};
+      dft<4>(t);
 #pragma unroll
-    for (int s1 = 0; s1 < 4; ++s1) y[r2][s1] = t[s1];
+      for (int s1 = 0; s1 < 4; ++s1) y[r2][s1] = t[s1];
+    }
   }
   const float h = 0.70710678118654752f;
   const float c1 = 0.92387953251128674f, s1_ = 0.38268343236508978f;  // cos, sin(pi/8)
@@ -142,6 +153,11 @@ __device__ __forceinline__ void dft<16>(float2 (&v)[16]) {
 #pragma unroll
     for (int s2 = 0; s2 < 4; ++s2) v[s1 + 4 * s2] = t[s2];
   }
+}
+
+template <>
+__device__ __forceinline__ void dft<16>(float2 (&v)[16]) {
+  dft16<false>(v);
 }
 
 // Shared-memory layout: one float2 of padding per 16 (pad(i) = i + i/16): the strided
@@ -219,7 +235,8 @@ __device__ __forceinline__ void stage(float2* buf, const float2* __restrict__ tw
 #pragma unroll
         for (int r = 1; r < R; ++r) v[b][r] = cmul(v[b][r], w[r]);
       }
-      dft<R>(v[b]);
+      if constexpr (ZERO_UPPER && R == 16) dft16<true>(v[b]);
+      else dft<R>(v[b]);
     }
   }
   __syncthreads();
