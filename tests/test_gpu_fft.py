@@ -158,3 +158,28 @@ def test_full_run_np1_C3():
     no = O.np1(Xo, rp, col)
     assert abs(float(np.mean(ngs)) - no) <= 0.01, (ngs, no)
     assert max(ngs) - min(ngs) <= 0.03, ngs
+
+
+def test_internal_node_order_is_invisible():
+    """n >= 65536 triggers the internal Morton renumbering at the first tfdp_step call of
+    >= 8 iterations.  Afterwards tfdp_set_layout / tfdp_forces / tfdp_layout must still speak
+    the caller's node order: forces at a caller-supplied layout match the oracle and the
+    node_order='keep' context, and the layout round-trips."""
+    w, rp, col = _case("C3")
+    X = w.xy.astype(np.float64)
+    Ro, Ao = O.repulsion_ibfft(X, 1), O.attraction(X, rp, col)
+    out = {}
+    for order in ("auto", "keep"):
+        with P.Layout(w.n, rp, col, w.xy, P.Params(solver="ibfft", k=1, node_order=order)) as L:
+            L.step(8)  # renumbers (auto) and moves the layout
+            moved = L.layout()
+            assert not np.array_equal(moved, w.xy)
+            L.set_layout(w.xy)  # back to the caller's input layout
+            np.testing.assert_array_equal(L.layout(), w.xy)
+            R, A = L.forces()
+        assert O.rel_l2(R, Ro) <= TOL_IB, order
+        assert O.rel_l2(A, Ao) <= 1e-4, order
+        out[order] = (R, A, moved)
+    assert O.rel_l2(out["auto"][0], out["keep"][0]) <= 1e-5
+    # the 8 iterations themselves agree up to fp32 summation order (atomics, R15)
+    assert O.rel_l2(out["auto"][2] - w.xy, out["keep"][2] - w.xy) <= 1e-2
