@@ -180,6 +180,7 @@ def test_internal_node_order_is_invisible():
         assert O.rel_l2(R, Ro) <= TOL_IB, order
         assert O.rel_l2(A, Ao) <= 1e-4, order
         out[order] = (R, A, moved)
-    assert O.rel_l2(out["auto"][0], out["keep"][0]) <= 1e-5
+    # fp32 spread atomics (R15): two node_order='keep' runs already differ by ~3e-5 at C3
+    assert O.rel_l2(out["auto"][0], out["keep"][0]) <= 1e-4
     # the 8 iterations themselves agree up to fp32 summation order (atomics, R15)
     assert O.rel_l2(out["auto"][2] - w.xy, out["keep"][2] - w.xy) <= 1e-2
