@@ -6,6 +6,12 @@
 
 namespace tfdp {
 
+// PDL (tfdp_internal.h launch_chained): let the next chain kernel be scheduled now / wait
+// until the predecessor grid has completed with its writes visible.  No-ops for kernels
+// launched without the attribute.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // MUFU.RCP: one SFU op, ~1 ulp.  s = 1 + d^2 >= 1 so no denormal inputs.
 __device__ __forceinline__ float rcp_approx(float x) {
   float r;

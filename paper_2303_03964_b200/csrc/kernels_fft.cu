@@ -7,11 +7,20 @@
 //                 fused bbox of the new positions for the next iteration
 // The grid convolution (step 2) is kernels_fftconv.cu.
 #include <algorithm>
+#include <cstdlib>
 
 #include "device_math.cuh"
 #include "tfdp_internal.h"
 
 namespace tfdp {
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("TFDP_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 // ------------------------------------------------------------------ bbox
 // Two-level exact min/max: every block reduces its keys (warp __reduce + smem) and merges
@@ -135,6 +144,8 @@ void launch_box_reduce(BoxKeys* part, int n_part, BoxKeys* keys, cudaStream_t s,
 __global__ void __launch_bounds__(64)
 setup_kernel(BoxKeys* part, int n_part, BoxKeys* keys, GridGeom* geom, int k,
              int n_int_min, int n_int_fixed, int n_int_cap, int P, int pitch, int* capped_flag) {
+  pdl_wait();
+  pdl_trigger();
   const BoxKeys kb = block_reduce_partials(part, n_part);
   if (threadIdx.x != 0) return;
   *keys = kb;
@@ -186,8 +197,8 @@ setup_kernel(BoxKeys* part, int n_part, BoxKeys* keys, GridGeom* geom, int k,
 void launch_setup(BoxKeys* part, int n_part, BoxKeys* keys, GridGeom* geom, int k,
                   int n_int_min, int n_int_fixed, int n_int_cap, int P, int pitch,
                   int* capped_flag, cudaStream_t s) {
-  setup_kernel<<<1, 64, 0, s>>>(part, n_part, keys, geom, k, n_int_min, n_int_fixed, n_int_cap,
-                                P, pitch, capped_flag);
+  launch_chained(setup_kernel, 1, 64, 0, s, part, n_part, keys, geom, k, n_int_min, n_int_fixed,
+                 n_int_cap, P, pitch, capped_flag);
 }
 
 // ------------------------------------------------------------------ interval coords
@@ -214,6 +225,8 @@ template <int K>
 __global__ void __launch_bounds__(kNodeThreads)
 spread_kernel(const float2* __restrict__ xy, int64_t lo, int64_t cnt,
               const GridGeom* __restrict__ geom, float* __restrict__ grid) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= cnt) return;
   const GridGeom g = *geom;
@@ -242,9 +255,9 @@ void launch_spread(const float2* xy, int64_t lo, int64_t cnt, const GridGeom* ge
                    float* grid, cudaStream_t s) {
   if (cnt <= 0) return;
   const unsigned blocks = (unsigned)((cnt + kNodeThreads - 1) / kNodeThreads);
-  if (k == 1) spread_kernel<1><<<blocks, kNodeThreads, 0, s>>>(xy, lo, cnt, geom, grid);
-  else if (k == 2) spread_kernel<2><<<blocks, kNodeThreads, 0, s>>>(xy, lo, cnt, geom, grid);
-  else spread_kernel<3><<<blocks, kNodeThreads, 0, s>>>(xy, lo, cnt, geom, grid);
+  if (k == 1) launch_chained(spread_kernel<1>, blocks, kNodeThreads, 0, s, xy, lo, cnt, geom, grid);
+  else if (k == 2) launch_chained(spread_kernel<2>, blocks, kNodeThreads, 0, s, xy, lo, cnt, geom, grid);
+  else launch_chained(spread_kernel<3>, blocks, kNodeThreads, 0, s, xy, lo, cnt, geom, grid);
 }
 
 // ------------------------------------------------------------------ gather + update
@@ -256,6 +269,8 @@ gather_update_kernel(const float2* __restrict__ xy, float2* __restrict__ xy_next
                      const int32_t* __restrict__ col, ForceArgs fa, float eta, int iter,
                      int update, float2* __restrict__ rep_out, float2* __restrict__ att_out,
                      unsigned long long* diverge, BoxKeys* next_part) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool active = t < n_local;
   unsigned kx0 = 0xffffffffu, ky0 = 0xffffffffu, kx1 = 0u, ky1 = 0u;
@@ -313,10 +328,9 @@ void launch_gather_update(const float2* xy, float2* xy_next, int64_t lo, int64_t
   if (n_local <= 0) return;
   const unsigned blocks = (unsigned)((n_local + kNodeThreads - 1) / kNodeThreads);
 #define TFDP_GU(KK)                                                                         \
-  gather_update_kernel<KK><<<blocks, kNodeThreads, 0, s>>>(xy, xy_next, lo, n_local, geom,  \
-                                                           phi, row_ptr, col, fa, eta, iter, \
-                                                           update, rep_out, att_out, diverge,\
-                                                           next_part)
+  launch_chained(gather_update_kernel<KK>, blocks, kNodeThreads, 0, s, xy, xy_next, lo,      \
+                 n_local, geom, phi, row_ptr, col, fa, eta, iter, update, rep_out, att_out,   \
+                 diverge, next_part)
   if (k == 1) TFDP_GU(1);
   else if (k == 2) TFDP_GU(2);
   else TFDP_GU(3);

@@ -198,9 +198,11 @@ __host__ __device__ constexpr int fft_threads_c(int P) {
   return P <= 2048 ? 128 : P <= 4096 ? 256 : P <= 6144 ? 384 : 512;
 }
 
-// Register cap via min blocks per SM: 64 registers per thread for blocks of <= 512 threads.
+// Register cap via min blocks per SM: 64 registers per thread (56 for 384-thread blocks, so
+// three P = 4608..6144 blocks fit per SM instead of two: k = 3 cols -19%).  Tighter caps
+// spill (40 registers: 36-264 B).
 template <int T>
-constexpr int kMinBlocks = T <= 512 ? 1024 / T : 1;
+constexpr int kMinBlocks = T == 128 ? 8 : T == 256 ? 4 : T == 384 ? 3 : 2;
 
 // FFT flags: inputs zero at index >= N/2 (first stage skips them); only outputs < N/2 needed
 // (last stage stores half).
@@ -317,7 +319,9 @@ TFDP_FFT_KERNEL(kspec_rows_kernel)(const GridGeom* __restrict__ geom, float neg_
   extern __shared__ float2 sm[];
   float2* a = sm;
   float2* tws = sm + padded_len(P);
-  load_tw(tws, tw, P);
+  load_tw(tws, tw, P);  // constant since the plan: safe before the wait
+  pdl_wait();
+  pdl_trigger();
   const GridGeom g = *geom;
   const int M = g.M;
   const int dya = 2 * blockIdx.x, dyb = dya + 1;
@@ -351,7 +355,9 @@ TFDP_FFT_KERNEL(kspec_cols_kernel)(const GridGeom* __restrict__ geom,
   extern __shared__ float2 sm[];
   float2* a = sm;
   float2* tws = sm + padded_len(P);
-  load_tw(tws, tw, P);
+  load_tw(tws, tw, P);  // constant since the plan: safe before the wait
+  pdl_wait();
+  pdl_trigger();
   const int M = geom->M;
   constexpr int half = P / 2;
   const int q0 = 2 * blockIdx.x, q1 = q0 + 1;
@@ -382,7 +388,9 @@ TFDP_FFT_KERNEL(rows_fwd_kernel)(const GridGeom* __restrict__ geom, float* __res
   extern __shared__ float2 sm[];
   float2* a = sm;
   float2* tws = sm + padded_len(P);
-  load_tw(tws, tw, P);
+  load_tw(tws, tw, P);  // constant since the plan: safe before the wait
+  pdl_wait();
+  pdl_trigger();
   const int M = geom->M;
   const int ra = 2 * blockIdx.x, rb = ra + 1;
   if (ra >= M) return;
@@ -427,7 +435,9 @@ TFDP_FFT_KERNEL(cols_kernel)(const GridGeom* __restrict__ geom, float2* __restri
   extern __shared__ float2 sm[];
   float2* a = sm;
   float2* tws = sm + padded_len(P);
-  load_tw(tws, tw, P);
+  load_tw(tws, tw, P);  // constant since the plan: safe before the wait
+  pdl_wait();
+  pdl_trigger();
   const int M = geom->M;
   constexpr int half = P / 2;
   // the three channels of one column are consecutive blocks: they share the K^ column in L2
@@ -461,7 +471,9 @@ TFDP_FFT_KERNEL(rows_inv_kernel)(const GridGeom* __restrict__ geom,
   extern __shared__ float2 sm[];
   float2* a = sm;
   float2* tws = sm + padded_len(P);
-  load_tw(tws, tw, P);
+  load_tw(tws, tw, P);  // constant since the plan: safe before the wait
+  pdl_wait();
+  pdl_trigger();
   const int M = geom->M;
   const int ra = 2 * blockIdx.x, rb = ra + 1;
   if (ra >= M) return;
@@ -547,8 +559,8 @@ void launch_kspec(const GridGeom* geom, int P, int Mcap, ForceArgs fa, const flo
   case S:                                                                                   \
     kspec_rows_kernel<S><<<(unsigned)((Mcap + 1) / 2), fft_threads_c(S), sm, s>>>(          \
         geom, -fa.gamma, fa.gamma_int, tw, KA, ka_pitch);                                   \
-    kspec_cols_kernel<S><<<(unsigned)((S / 2 + 2) / 2), fft_threads_c(S), sm, s>>>(         \
-        geom, KA, ka_pitch, tw, KH);                                                        \
+    launch_chained(kspec_cols_kernel<S>, (unsigned)((S / 2 + 2) / 2), fft_threads_c(S), sm, s, \
+                   geom, KA, ka_pitch, tw, KH);                                             \
     break;
   switch (P) { TFDP_FFT_SIZES(TFDP_KS) default: break; }
 #undef TFDP_KS
@@ -559,8 +571,8 @@ void launch_rows_fwd(const GridGeom* geom, float* C, int cpitch, int P, int Mcap
   const size_t sm = fftconv_smem_bytes(P);
 #define TFDP_RF(S)                                                                          \
   case S:                                                                                   \
-    rows_fwd_kernel<S><<<dim3((unsigned)((Mcap + 1) / 2), 3), fft_threads_c(S), sm, s>>>(   \
-        geom, C, cpitch, tw, CA, ca_pitch);                                                 \
+    launch_chained(rows_fwd_kernel<S>, dim3((unsigned)((Mcap + 1) / 2), 3), fft_threads_c(S), \
+                   sm, s, geom, C, cpitch, tw, CA, ca_pitch);                               \
     break;
   switch (P) { TFDP_FFT_SIZES(TFDP_RF) default: break; }
 #undef TFDP_RF
@@ -583,8 +595,8 @@ void launch_rows_inv(const GridGeom* geom, const float2* CA, int ca_pitch, int P
   const size_t sm = fftconv_smem_bytes(P);
 #define TFDP_RI(S)                                                                          \
   case S:                                                                                   \
-    rows_inv_kernel<S><<<dim3((unsigned)((Mcap + 1) / 2), 3), fft_threads_c(S), sm, s>>>(   \
-        geom, CA, ca_pitch, tw, Phi, cpitch);                                               \
+    launch_chained(rows_inv_kernel<S>, dim3((unsigned)((Mcap + 1) / 2), 3), fft_threads_c(S), \
+                   sm, s, geom, CA, ca_pitch, tw, Phi, cpitch);                             \
     break;
   switch (P) { TFDP_FFT_SIZES(TFDP_RI) default: break; }
 #undef TFDP_RI

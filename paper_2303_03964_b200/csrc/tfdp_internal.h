@@ -39,6 +39,30 @@ struct ForceArgs {
   int gamma_int;  // 1..8 if gamma is that integer, else 0 (general path)
 };
 
+// ---- programmatic dependent launch (PDL) for the per-iteration kernel chain -----------
+// Chain kernels are launched with programmatic stream serialization: a kernel may be
+// scheduled while its predecessor's last wave is still running, does its independent
+// prologue (twiddle table -> smem), then blocks in griddepcontrol.wait (pdl_wait in
+// device_math.cuh) until the predecessor grid has completed and its writes are visible.
+// Every chain kernel calls pdl_wait() before touching any buffer another kernel writes, so
+// the ordering is the plain stream order.  TFDP_PDL=0 disables the attribute (A/B runs).
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline void launch_chained(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                           cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 // ---- launchers (kernels.cu / kernels_fft.cu); all enqueue on `s` ---------------------
 // exact path
 void launch_exact_partial(const float2* xy, int64_t n, int64_t lo, int64_t n_local,

@@ -169,8 +169,12 @@ def test_internal_node_order_is_invisible():
     X = w.xy.astype(np.float64)
     Ro, Ao = O.repulsion_ibfft(X, 1), O.attraction(X, rp, col)
     out = {}
+    # step0 = 1e-3: at the default 0.1 the first iterations of C3 are chaotic enough that two
+    # identical node_order='keep' runs already differ by ~2% in displacement after 8
+    # iterations (fp32 atomics, R15); a small step keeps the trajectory comparison meaningful.
     for order in ("auto", "keep"):
-        with P.Layout(w.n, rp, col, w.xy, P.Params(solver="ibfft", k=1, node_order=order)) as L:
+        prm = P.Params(solver="ibfft", k=1, node_order=order, step0=1e-3)
+        with P.Layout(w.n, rp, col, w.xy, prm) as L:
             L.step(8)  # renumbers (auto) and moves the layout
             moved = L.layout()
             assert not np.array_equal(moved, w.xy)
@@ -182,5 +186,13 @@ def test_internal_node_order_is_invisible():
         out[order] = (R, A, moved)
     # fp32 spread atomics (R15): two node_order='keep' runs already differ by ~3e-5 at C3
     assert O.rel_l2(out["auto"][0], out["keep"][0]) <= 1e-4
-    # the 8 iterations themselves agree up to fp32 summation order (atomics, R15)
-    assert O.rel_l2(out["auto"][2] - w.xy, out["keep"][2] - w.xy) <= 1e-2
+    # the 8 iterations themselves agree up to fp32 summation order (atomics, R15), and with
+    # the oracle's 8 ibFFT iterations
+    Xo = O.run(w.xy, rp, col, O.Params(), T=300, eta0=1e-3, solver="ibfft", k=1, t_end=8)
+    da, dk, do = out["auto"][2] - w.xy, out["keep"][2] - w.xy, Xo - w.xy
+    assert O.rel_l2(da, dk) <= 1e-3
+    # vs the fp64 oracle: the device keeps positions in fp32 (R14), so each of the 8 updates
+    # rounds by up to ulp(x)/2 -- at |x| ~ 100 that is ~1e-3 of these small displacements
+    ulp = np.spacing(np.maximum(np.abs(w.xy), np.abs(out["auto"][2])).astype(np.float32))
+    bound = np.linalg.norm(8 * 0.5 * ulp.astype(np.float64)) / np.linalg.norm(do)
+    assert O.rel_l2(da, do) <= bound + 1e-3, bound
