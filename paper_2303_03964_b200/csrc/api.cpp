@@ -195,13 +195,13 @@ struct Scope {
   cudaEvent_t a = nullptr;
   bool on;
   cudaStream_t st;
-  Scope(tfdp_ctx* c_, int k, cudaStream_t s = nullptr)
+  Scope(tfdp_ctx* c_, int k, cudaStream_t s = nullptr, int n_launch = 1)
       : c(c_), kind(k), on((c_->prof_mask >> k) & 1u), st(s ? s : c_->stream) {
     if (on) {
       a = ev_get(c);
       cudaEventRecord(a, st);
     }
-    if (kOwnKernel[k]) c->launches++;
+    if (kOwnKernel[k]) c->launches += n_launch;
   }
   ~Scope() {
     if (on) {
@@ -500,7 +500,7 @@ tfdp_status evaluate(tfdp_ctx* c, int update, float eta, int k) {
     const int mcap = c->cap_of_k[k] * k;
     const float2* tw = c->tw[k];
     if (!c->box_valid || c->world > 1) {
-      Scope sc(c, K_BBOX);
+      Scope sc(c, K_BBOX, nullptr, 2);  // reset_slots + bbox
       tfdp::launch_reset_slots(c->box_part, c->stream);
       c->n_part = tfdp::launch_bbox(xy, c->n, c->box_part, c->stream);
     }
@@ -521,7 +521,7 @@ tfdp_status evaluate(tfdp_ctx* c, int update, float eta, int k) {
       CUDA_TRY(c, cudaStreamWaitEvent(c->side, c->ev_fork, 0));
     }
     {
-      Scope sc(c, K_KSPEC, ks);
+      Scope sc(c, K_KSPEC, ks, 2);  // kspec_rows + kspec_cols
       tfdp::launch_kspec(c->geom, P, mcap, c->fa, tw, c->ka, c->cpitch, c->kh, ks);
     }
     if (overlap) CUDA_TRY(c, cudaEventRecord(c->ev_join, c->side));
