@@ -150,6 +150,25 @@ tfdp_status tfdp_set_layout(tfdp_ctx* ctx, const float* xy);
 tfdp_status tfdp_set_iteration(tfdp_ctx* ctx, int32_t t);
 int32_t tfdp_iteration(const tfdp_ctx* ctx);
 
+/* Replaces the parameters of a live context (the layout is kept).  Validated like tfdp_init
+ * (same errors, same warning bits, which replace the previous ones; TFDP_WARN_NINT_CAPPED
+ * is kept).  solver, dist_mode and node_order are fixed at tfdp_init (TFDP_ERR_ARG if they
+ * differ).  The iteration counter is set to p->t0 and the k schedule rebuilt for
+ * p->iterations.  On the ibFFT path a change of k, n_int_min, n_int_fixed or fft_size
+ * re-plans the grid from the current layout (one bbox pass and a sync); on failure the
+ * previous parameters stay in force.  Used by global refinement. */
+tfdp_status tfdp_set_params(tfdp_ctx* ctx, const tfdp_params* p);
+
+/* Global refinement (SPEC global_refine S:359-366): taking the current layout as
+ * the initialization, re-runs the layout loop for `iterations` iterations t = 0 .. T-1
+ * (T = iterations, schedules rebuilt for T) with repulsion exponent gamma and scale rho
+ * ("a large repulsive t-force will distribute nearby nodes evenly"; "a repulsive force
+ * with a shorter range (larger gamma)" shows the skeleton).  alpha, beta, eta0, cooling,
+ * solver and k are kept; gamma and rho stay set afterwards.  Errors: TFDP_ERR_ARG if
+ * gamma <= 1 or non-finite, rho <= 0 or non-finite, iterations < 1; otherwise the
+ * errors of tfdp_step. */
+tfdp_status tfdp_global_refine(tfdp_ctx* ctx, double gamma, double rho, int32_t iterations);
+
 /* This rank's target shard. */
 tfdp_status tfdp_shard(const tfdp_ctx* ctx, int64_t* lo, int64_t* hi);
 

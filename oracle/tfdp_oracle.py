@@ -25,7 +25,7 @@ __all__ = [
     "energy", "eta", "k_schedule", "Box", "box_rule", "interval_coords",
     "lagrange_weights", "spread", "kernel_tdist", "convolve_direct", "convolve_fft",
     "gather", "repulsion_ibfft", "forces", "step", "run", "np1", "rel_l2",
-    "equilibrium_distance",
+    "equilibrium_distance", "global_refine",
 ]
 
 
@@ -433,6 +433,19 @@ def run(X0, row_ptr, col, p: Params = Params(), T: int = 300, eta0: float = 0.1,
         if bad.any():
             raise FloatingPointError(f"diverged at iter {t} node {int(np.argmax(bad))}")
     return X
+
+
+def global_refine(X, row_ptr, col, p: Params = Params(), gamma: float | None = None,
+                  rho: float | None = None, T: int = 300, **kw):
+    """Global refinement: "Taking a t-FDP layout as initialization ... re-applying
+    t-FDP with repulsive t-forces of different values"; SPEC global_refine:
+    `run` from the given layout with gamma and/or rho overridden, t = 0 .. T-1.
+    gamma <= 1 -> ValueError (S:362)."""
+    g = p.gamma if gamma is None else float(gamma)
+    r = p.rho if rho is None else float(rho)
+    if not (g > 1.0) or not (r > 0.0):
+        raise ValueError("global refinement needs gamma > 1 and rho > 0 (S:362)")
+    return run(X, row_ptr, col, dataclasses.replace(p, gamma=g, rho=r), T=T, **kw)
 
 
 # ---------------------------------------------------------------------------------------

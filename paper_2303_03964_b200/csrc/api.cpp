@@ -651,6 +651,27 @@ tfdp_status copy_out(tfdp_ctx* c, const float2* src, float* dst, int64_t n_rows)
   return TFDP_OK;
 }
 
+// Box of the current device layout -> configure_fft.  The slots keep the box (no reset), so
+// the next setup can consume it without another bbox pass.
+tfdp_status replan_from_device(tfdp_ctx* c) {
+  tfdp::launch_reset_slots(c->box_part, c->stream);
+  c->n_part = tfdp::launch_bbox(c->xy[c->cur], c->n, c->box_part, c->stream);
+  tfdp::launch_box_reduce(c->box_part, c->n_part, c->keys, c->stream, /*reset=*/false);
+  c->launches += 3;
+  BoxKeys hk;
+  CUDA_TRY(c, cudaMemcpyAsync(&hk, c->keys, sizeof hk, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  auto k2f = [](unsigned k) {
+    unsigned u = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
+    float f;
+    memcpy(&f, &u, 4);
+    return f;
+  };
+  const float L = std::max(k2f(hk.maxx) - k2f(hk.minx), k2f(hk.maxy) - k2f(hk.miny));
+  c->box_valid = c->world == 1;
+  return configure_fft(c, L);
+}
+
 // Re-sizes the grid when an iteration ran capped, or when the last N_int came within 4
 // intervals of the cap (so the next block of iterations does not run capped).
 tfdp_status maybe_replan(tfdp_ctx* c, bool capped) {
@@ -667,22 +688,7 @@ tfdp_status maybe_replan(tfdp_ctx* c, bool capped) {
     if (k_used(c, k)) mincap = std::min(mincap, c->cap_of_k[k]);
   if (!capped && last.n_int + 4 <= mincap) return TFDP_OK;
   if (!capped && c->P_of_k[3] >= kMaxFftSize) return TFDP_OK;  // already at the largest grid
-  tfdp::launch_reset_slots(c->box_part, c->stream);
-  c->n_part = tfdp::launch_bbox(c->xy[c->cur], c->n, c->box_part, c->stream);
-  tfdp::launch_box_reduce(c->box_part, c->n_part, c->keys, c->stream);
-  c->launches += 2;
-  BoxKeys hk;
-  CUDA_TRY(c, cudaMemcpyAsync(&hk, c->keys, sizeof hk, cudaMemcpyDeviceToHost, c->stream));
-  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-  auto k2f = [](unsigned k) {
-    unsigned u = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
-    float f;
-    memcpy(&f, &u, 4);
-    return f;
-  };
-  const float L = std::max(k2f(hk.maxx) - k2f(hk.minx), k2f(hk.maxy) - k2f(hk.miny));
-  c->box_valid = c->world == 1;
-  return configure_fft(c, L);
+  return replan_from_device(c);
 }
 
 }  // namespace
@@ -1006,6 +1012,57 @@ tfdp_status tfdp_set_iteration(tfdp_ctx* c, int32_t t) {
 }
 
 int32_t tfdp_iteration(const tfdp_ctx* c) { return c ? c->t : -1; }
+
+tfdp_status tfdp_set_params(tfdp_ctx* c, const tfdp_params* p) {
+  if (!c || !p) return fail(c, TFDP_ERR_ARG, "NULL argument");
+  if (c->errored) return fail(c, TFDP_ERR_STATE, "context is errored: %s", c->err.c_str());
+  uint32_t warn = 0;
+  std::string msg;
+  tfdp_status st = validate_params(p, &warn, &msg);
+  if (st != TFDP_OK) return fail(c, st, "%s", msg.c_str());
+  if (p->solver != c->p.solver || p->dist_mode != c->p.dist_mode || p->node_order != c->p.node_order)
+    return fail(c, TFDP_ERR_ARG, "solver, dist_mode and node_order are fixed at tfdp_init");
+  cudaSetDevice(c->device);
+  const bool replan = p->solver == TFDP_IBFFT &&
+                      (p->k != c->p.k || p->n_int_min != c->p.n_int_min ||
+                       p->n_int_fixed != c->p.n_int_fixed || p->fft_size != c->p.fft_size);
+  const tfdp_params old = c->p;
+  c->p = *p;
+  if (replan) {
+    tfdp_status r = replan_from_device(c);
+    if (r != TFDP_OK) {  // keep the context usable with its previous plan
+      c->p = old;
+      const std::string m = c->err;
+      replan_from_device(c);
+      return fail(c, r, "%s", m.c_str());
+    }
+  }
+  c->warnings = (c->warnings & TFDP_WARN_NINT_CAPPED) | warn;
+  c->t = p->t0;
+  c->ksched = k_schedule(p->iterations);
+  c->fa.alpha = (float)p->alpha;
+  c->fa.beta = (float)p->beta;
+  c->fa.gamma = (float)p->gamma;
+  c->fa.rho = (float)p->rho;
+  c->fa.gamma_int = gamma_int_of(p->gamma);
+  return TFDP_OK;
+}
+
+tfdp_status tfdp_global_refine(tfdp_ctx* c, double gamma, double rho, int32_t iterations) {
+  if (!c) return fail(nullptr, TFDP_ERR_ARG, "ctx is NULL");
+  if (!std::isfinite(gamma) || gamma <= 1.0)
+    return fail(c, TFDP_ERR_ARG, "global refinement needs gamma > 1 (S:362), got %g", gamma);
+  if (!std::isfinite(rho) || rho <= 0.0)
+    return fail(c, TFDP_ERR_ARG, "global refinement needs rho > 0, got %g", rho);
+  if (iterations < 1) return fail(c, TFDP_ERR_ARG, "iterations must be >= 1");
+  tfdp_params p = c->p;
+  p.gamma = gamma;
+  p.rho = rho;
+  p.iterations = iterations;
+  p.t0 = 0;
+  TRY(tfdp_set_params(c, &p));
+  return tfdp_step(c, iterations);
+}
 
 tfdp_status tfdp_shard(const tfdp_ctx* c, int64_t* lo, int64_t* hi) {
   if (!c || !lo || !hi) return TFDP_ERR_ARG;

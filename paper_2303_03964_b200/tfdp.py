@@ -182,6 +182,22 @@ class Layout:
     def set_iteration(self, t: int):
         check(lib().tfdp_set_iteration(self._ctx, int(t)), self._ctx)
 
+    def set_params(self, params: Params):
+        """tfdp_set_params: new weights / schedule for the live layout (solver fixed)."""
+        pc = params.to_c()
+        check(lib().tfdp_set_params(self._ctx, C.byref(pc)), self._ctx)
+        self.params = params
+
+    def global_refine(self, gamma: float | None = None, rho: float | None = None,
+                      iterations: int | None = None):
+        """Global refinement (tfdp_global_refine): re-run the layout loop from the
+        current layout with repulsion exponent gamma and/or scale rho (None = unchanged)."""
+        g = self.params.gamma if gamma is None else float(gamma)
+        r = self.params.rho if rho is None else float(rho)
+        T = self.params.iterations if iterations is None else int(iterations)
+        check(lib().tfdp_global_refine(self._ctx, g, r, T), self._ctx)
+        self.params = dataclasses.replace(self.params, gamma=g, rho=r, iterations=T, t0=0)
+
     @property
     def iteration(self) -> int:
         return int(lib().tfdp_iteration(self._ctx))

@@ -15,6 +15,8 @@ from .graphs import (  # noqa: F401
     uniform_square,
     random_layout,
     random_graph,
+    path_graph,
+    two_cluster_graph,
     make_config,
     CONFIGS,
 )

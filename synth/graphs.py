@@ -150,6 +150,25 @@ def random_layout(n: int, seed: int, scale: float = 1.0) -> np.ndarray:
     return (_rng(seed).standard_normal((n, 2)) * scale).astype(np.float32)
 
 
+def path_graph(n: int):
+    """Path P_n: edges (i, i+1) (SPEC S:365 refinement example P20)."""
+    u = np.arange(n - 1, dtype=np.int32)
+    return u, u + 1
+
+
+def two_cluster_graph(n_per: int, p_in: float, p_out: float, seed: int):
+    """Two-block stochastic block model (SPEC S:366 '2-cluster synthetic graph'): nodes
+    [0, n_per) and [n_per, 2 n_per); each pair is an edge with probability p_in inside a
+    block and p_out across.  Returns (u, v, label)."""
+    g = _rng(seed)
+    n = 2 * n_per
+    iu, ju = np.triu_indices(n, 1)
+    lab = (np.arange(n) >= n_per).astype(np.int32)
+    p = np.where(lab[iu] == lab[ju], p_in, p_out)
+    keep = g.random(iu.shape[0]) < p
+    return iu[keep].astype(np.int32), ju[keep].astype(np.int32), lab
+
+
 def random_graph(n: int, m: int, seed: int):
     """Generic seeded random edge list (raw; may contain duplicates / self-loops)."""
     g = _rng(seed)
