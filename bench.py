@@ -296,6 +296,21 @@ def run_fft(args, rank, world, local):
     return res
 
 
+def run_np1(r, reps=5):
+    """NEXT-3: device NP1 of the bench layout (tfdp_np1: cell grid + warp-per-node exact kNN
+    membership).  Untimed by the contract; reported for the convergence-trace use."""
+    L = r["L"]
+    v = L.np1()  # warm-up (allocates the scratch)
+    t = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        v = L.np1()  # ends with a stream sync
+        t.append(time.perf_counter() - t0)
+    ms = 1e3 * float(np.median(t))
+    return {"workload": "C4 layout after the timed steps", "np1": v, "ms": round(ms, 3),
+            "nodes_per_s": r["n"] / (ms / 1e3), "timing": "host wall clock around the synchronous call, median of 5"}
+
+
 def run_exact(args, rank, world, local):
     import torch
 
@@ -453,6 +468,7 @@ def main():
     rank, world, local = dist_setup(args)
     torch.cuda.set_device(local)
     r = run_fft(args, rank, world, local)
+    npm = run_np1(r)
     exact = None if args.no_exact else run_exact(args, rank, world, local)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -475,7 +491,7 @@ def main():
             },
             "e2e": r["e2e"], "gpu_launches": r["launches"], "clocks": r["clocks"],
             "roofline": r["roofline"], "cpu_baseline": cpu, "kernels": r["kernels"],
-            "exact": exact,
+            "exact": exact, "np1": npm,
         }
         print(json.dumps(line), flush=True)
     r["L"].close()

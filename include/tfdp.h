@@ -169,6 +169,22 @@ tfdp_status tfdp_set_params(tfdp_ctx* ctx, const tfdp_params* p);
  * errors of tfdp_step. */
 tfdp_status tfdp_global_refine(tfdp_ctx* ctx, double gamma, double rho, int32_t iterations);
 
+/* Neighbourhood preservation NP1 of the current layout, computed on
+ * the device (NEXT-3: per-iteration convergence traces):
+ *   NP1 = (1/n) sum_i |N_G(i) ∩ N_L(i, k_i)| / |N_G(i) ∪ N_L(i, k_i)|,  k_i = deg(i),
+ * N_L(i, k) = the k nearest other nodes in the layout, equal distances broken by the lower
+ * node id; a degree-0 node contributes 1.  Distances are compared as d^2 = (dx dx) + (dy dy)
+ * with each operation rounded in IEEE fp32 (R22), so the set decisions are exact
+ * and deterministic.
+ *   np1   host double* (may be NULL): the full-graph value on every rank (NCCL sum over the
+ *         ranks); for a virtual shard (no communicator) this shard's share sum_{i in shard}/n
+ *   hits  host or device int32[hi - lo] (may be NULL): |N_G(i) ∩ N_L(i, k_i)| for the
+ *         shard's nodes in the caller's order
+ * Syncs the stream.  Cost: O(n + sum_i c_i) with c_i the nodes in the cells around i that
+ * hold its k_i nearest (uniform cell grid of ~2 nodes per cell over the bounding square).
+ * Scratch (~8 B x cells + 24 B x n) is allocated at the first call and kept. */
+tfdp_status tfdp_np1(tfdp_ctx* ctx, double* np1, int32_t* hits);
+
 /* This rank's target shard. */
 tfdp_status tfdp_shard(const tfdp_ctx* ctx, int64_t* lo, int64_t* hi);
 

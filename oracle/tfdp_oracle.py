@@ -25,7 +25,7 @@ __all__ = [
     "energy", "eta", "k_schedule", "Box", "box_rule", "interval_coords",
     "lagrange_weights", "spread", "kernel_tdist", "convolve_direct", "convolve_fft",
     "gather", "repulsion_ibfft", "forces", "step", "run", "np1", "rel_l2",
-    "equilibrium_distance", "global_refine",
+    "equilibrium_distance", "global_refine", "np1_hits", "np1_from_hits",
 ]
 
 
@@ -492,3 +492,42 @@ def np1(X, row_ptr, col, brute_max: int = 4096):
                 Lset = set(cand)
                 total += len(G & Lset) / len(G | Lset)
     return total / n
+
+
+def np1_hits(X, row_ptr, col, nodes=None, dist: str = "fp64"):
+    """Per node i: |N_G(i,1) ∩ N_L(x_i, k_i)|, k_i = deg(i), by brute force —
+    the layout kNN excludes i, ties by lower index, k_i = 0 -> 0.
+    dist = "fp64": d^2 in fp64.  dist = "fp32": the kNN decisions are taken on
+    d^2 = (dx*dx) + (dy*dy) with dx = x_j - x_i and every operation rounded to IEEE fp32
+    (the device kernel's precision; R22)."""
+    row_ptr = np.asarray(row_ptr, dtype=np.int64)
+    n = row_ptr.shape[0] - 1
+    if dist == "fp32":
+        Xc = np.asarray(X, dtype=np.float32)
+    elif dist == "fp64":
+        Xc = np.asarray(X, dtype=np.float64)
+    else:
+        raise ValueError(dist)
+    nodes = np.arange(n) if nodes is None else np.asarray(nodes, dtype=np.int64)
+    out = np.zeros(nodes.shape[0], dtype=np.int64)
+    for r, i in enumerate(nodes.tolist()):
+        ki = int(row_ptr[i + 1] - row_ptr[i])
+        if ki == 0:
+            continue
+        dx = Xc[:, 0] - Xc[i, 0]
+        dy = Xc[:, 1] - Xc[i, 1]
+        d2 = dx * dx + dy * dy  # numpy: each op rounded in the array dtype, no contraction
+        d2[i] = np.inf
+        nn = np.argsort(d2, kind="stable")[:ki]  # stable: equal distances -> lower index
+        G = set(col[row_ptr[i]:row_ptr[i + 1]].tolist())
+        out[r] = len(G & set(nn.tolist()))
+    return out
+
+
+def np1_from_hits(hits, row_ptr):
+    """NP1 = (1/n) sum_i |∩| / |∪| with |∪| = 2 k_i - |∩| (both sets have k_i elements) and
+    k_i = 0 contributing 1."""
+    deg = np.diff(np.asarray(row_ptr, dtype=np.int64))
+    h = np.asarray(hits, dtype=np.float64)
+    per = np.where(deg == 0, 1.0, h / np.maximum(2 * deg - h, 1))
+    return float(per.mean())

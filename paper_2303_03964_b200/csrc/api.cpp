@@ -121,6 +121,13 @@ struct tfdp_ctx {
   int32_t* col_o = nullptr;
   void* rscratch = nullptr;
   float2* iobuf = nullptr;  // n float2 staging for (un)permuted inputs / outputs
+  // NP1 metric (kernels_np.cu), allocated at the first tfdp_np1 call
+  void* np_scratch = nullptr;
+  int* np_hits = nullptr;    // [n_local] slot order
+  int* np_hits2 = nullptr;   // [n] caller order (reordered contexts)
+  BoxKeys* np_slots = nullptr;
+  BoxKeys* np_keys = nullptr;
+  double* np_sum = nullptr;
   struct Pend {
     int kind;
     cudaEvent_t a, b;
@@ -1048,6 +1055,47 @@ tfdp_status tfdp_set_params(tfdp_ctx* c, const tfdp_params* p) {
   return TFDP_OK;
 }
 
+tfdp_status tfdp_np1(tfdp_ctx* c, double* np1, int32_t* hits) {
+  if (!c) return fail(nullptr, TFDP_ERR_ARG, "ctx is NULL");
+  if (c->errored) return fail(c, TFDP_ERR_STATE, "context is errored: %s", c->err.c_str());
+  cudaSetDevice(c->device);
+  const int64_t n_local = c->hi - c->lo;
+  if (!c->np_scratch) {
+    CUDA_TRY(c, cudaMalloc(&c->np_scratch, tfdp::np_scratch_bytes(c->n, n_local)));
+    CUDA_TRY(c, cudaMalloc(&c->np_hits, std::max<int64_t>(n_local, 1) * sizeof(int)));
+    if (c->reorder) CUDA_TRY(c, cudaMalloc(&c->np_hits2, c->n * sizeof(int)));
+    CUDA_TRY(c, cudaMalloc(&c->np_slots, tfdp::kBoxSlots * sizeof(BoxKeys)));
+    CUDA_TRY(c, cudaMalloc(&c->np_keys, sizeof(BoxKeys)));
+    CUDA_TRY(c, cudaMalloc(&c->np_sum, sizeof(double)));
+  }
+  const float2* xy = c->xy[c->cur];
+  tfdp::launch_reset_slots(c->np_slots, c->stream);
+  const int np = tfdp::launch_bbox(xy, c->n, c->np_slots, c->stream);
+  tfdp::launch_box_reduce(c->np_slots, np, c->np_keys, c->stream);
+  c->launches += 3;
+  c->launches += tfdp::launch_np1(xy, c->n, c->lo, n_local, c->row_ptr, c->col,
+                                  c->reorder ? c->perm : nullptr, c->np_keys, c->np_scratch,
+                                  c->np_hits, c->np_sum, c->stream);
+  if (c->world > 1 && c->comm)
+    NCCL_TRY(c, c->nccl->AllReduce(c->np_sum, c->np_sum, 1, ncclDouble, ncclSum, c->comm,
+                                   c->stream));
+  CUDA_TRY(c, cudaGetLastError());
+  if (hits) {
+    const int* src = c->np_hits;
+    if (c->reorder) {  // internal slot -> caller order
+      tfdp::launch_unpermute_int(c->np_hits, c->perm, c->n, c->np_hits2, c->stream);
+      c->launches++;
+      src = c->np_hits2;
+    }
+    const bool d = is_device_ptr(hits);
+    CUDA_TRY(c, cudaMemcpyAsync(hits, src, n_local * sizeof(int),
+                                d ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->stream));
+  }
+  if (np1) CUDA_TRY(c, cudaMemcpyAsync(np1, c->np_sum, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return TFDP_OK;
+}
+
 tfdp_status tfdp_global_refine(tfdp_ctx* c, double gamma, double rho, int32_t iterations) {
   if (!c) return fail(nullptr, TFDP_ERR_ARG, "ctx is NULL");
   if (!std::isfinite(gamma) || gamma <= 1.0)
@@ -1177,6 +1225,12 @@ void tfdp_destroy(tfdp_ctx* c) {
   cudaFree(c->col_o);
   cudaFree(c->rscratch);
   cudaFree(c->iobuf);
+  cudaFree(c->np_scratch);
+  cudaFree(c->np_hits);
+  cudaFree(c->np_hits2);
+  cudaFree(c->np_slots);
+  cudaFree(c->np_keys);
+  cudaFree(c->np_sum);
   cudaFree(c->geom);
   if (c->h_status) cudaFreeHost(c->h_status);
   if (c->comm && c->nccl) c->nccl->CommDestroy(c->comm);

@@ -184,6 +184,11 @@ void exclusive_scan(const long long* in, long long* out, int64_t n, long long* s
 
 }  // namespace
 
+void exclusive_scan_ll(const long long* in, long long* out, int64_t n, long long* sums,
+                       cudaStream_t s) {
+  exclusive_scan(in, out, n, sums, s);
+}
+
 size_t reorder_scratch_bytes(int64_t n) {
   // keys int[n], hist/offs ll[kBins], deg ll[n+1], sums ll[blocks]
   const int64_t nbins = kBins;

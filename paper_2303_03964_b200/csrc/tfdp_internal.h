@@ -111,6 +111,18 @@ int launch_reorder(const float2* xy_old, float2* xy_new, const BoxKeys* box, con
 void launch_unpermute(const float2* in, const int* perm, int64_t n, float2* out, cudaStream_t s);
 void launch_permute(const float2* in, const int* perm, int64_t n, float2* out, cudaStream_t s);
 
+// NP1 of the layout (kernels_np.cu): hits[q] = |N_G(t) ∩ N_L(t, deg t)| for t = lo + q;
+// *np_sum = sum over the shard of (deg == 0 ? 1 : h / (2 deg - h)) / n (fixed-order sum).
+// ids = caller node id per internal slot (tie rule), NULL = identity.  Returns launches.
+int np_grid_side(int64_t n);
+size_t np_scratch_bytes(int64_t n, int64_t n_local);
+int launch_np1(const float2* xy, int64_t n, int64_t lo, int64_t n_local, const int64_t* row_ptr,
+               const int32_t* col, const int* ids, const BoxKeys* box_keys, void* scratch,
+               int* hits, double* np_sum, cudaStream_t s);
+void launch_unpermute_int(const int* in, const int* perm, int64_t n, int* out, cudaStream_t s);
+void exclusive_scan_ll(const long long* in, long long* out, int64_t n, long long* sums,
+                       cudaStream_t s);
+
 void launch_gather_update(const float2* xy, float2* xy_next, int64_t lo, int64_t n_local,
                           const GridGeom* geom, int k, const float* phi,
                           const int64_t* row_ptr, const int32_t* col, ForceArgs fa,

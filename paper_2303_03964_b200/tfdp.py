@@ -198,6 +198,14 @@ class Layout:
         check(lib().tfdp_global_refine(self._ctx, g, r, T), self._ctx)
         self.params = dataclasses.replace(self.params, gamma=g, rho=r, iterations=T, t0=0)
 
+    def np1(self, hits=None):
+        """NP1 of the current layout on the device (tfdp_np1, P:599-606).  Returns the float;
+        with hits (int32 array / tensor of hi - lo entries) also fills the per-node counts."""
+        v = C.c_double(0.0)
+        hp, keep = _ptr(hits)
+        check(lib().tfdp_np1(self._ctx, C.byref(v), hp), self._ctx)
+        return v.value
+
     @property
     def iteration(self) -> int:
         return int(lib().tfdp_iteration(self._ctx))

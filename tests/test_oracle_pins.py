@@ -231,3 +231,37 @@ def test_np1_isolated_and_kdtree_path():
     assert a == pytest.approx(b, abs=1e-12)
     rp1, col1 = O.csr_build(3, [0], [1])  # node 2 isolated -> contributes 1
     assert O.np1(np.array([[0, 0], [1, 0], [5, 5.0]]), rp1, col1) == pytest.approx(1.0)
+
+
+def test_np1_hits_hand_examples_and_consistency():
+    """Per-node hits reproduce S:427-429 (K3: 2,2,2; P3: 1,2,1; two far pairs: 0) and the
+    brute-force / KD-tree np1 through NP1 = mean |∩| / (2k - |∩|)."""
+    want = [[2, 2, 2], [1, 2, 1], [0, 0, 0, 0]]
+    for c, w in zip(GOLD["np1"]["cases"], want):
+        rp, col = csr_of(c["n"], c["edges"])
+        X = np.array(c["X"], dtype=np.float64)
+        for dist in ("fp64", "fp32"):
+            h = O.np1_hits(X, rp, col, dist=dist)
+            assert h.tolist() == w
+            assert O.np1_from_hits(h, rp) == pytest.approx(c["np1"])
+    X, rp, col = _rand_case(3000, 6000, 8, 20.0)
+    h64 = O.np1_hits(X, rp, col)
+    assert O.np1_from_hits(h64, rp) == pytest.approx(O.np1(X, rp, col, brute_max=0), abs=1e-12)
+    # no near-ties in generic fp32 data: both precisions take the same decisions
+    h32 = O.np1_hits(X.astype(np.float32), rp, col, dist="fp32")
+    assert (h32 != h64).sum() <= 3
+
+
+def test_np1_hits_tie_rule():
+    """Equal distances are broken by the lower node id: node 0 at the origin with
+    nodes 1, 2, 3 at distance 1 (exact in fp32) and k_0 = 1."""
+    X = np.array([[0, 0], [0, 1], [-1, 0], [1, 0], [5, 5]], dtype=np.float64)
+    for nb, hit in ((3, 0), (1, 1), (2, 0)):
+        rp, col = O.csr_build(5, [0], [nb])
+        assert O.np1_hits(X, rp, col, nodes=[0], dist="fp32")[0] == hit
+    # coincident nodes: distance 0 ties, again by id
+    X = np.array([[0, 0], [2, 0], [2, 0], [9, 9]], dtype=np.float64)
+    rp, col = O.csr_build(4, [0, 3], [2, 1])  # node 1's nearest: node 2 (d=0), then 0
+    assert O.np1_hits(X, rp, col, nodes=[1], dist="fp32")[0] == 0
+    rp, col = O.csr_build(4, [2], [1])  # node 2's nearest other: node 1 (d=0, lower id)
+    assert O.np1_hits(X, rp, col, nodes=[2], dist="fp32")[0] == 1
