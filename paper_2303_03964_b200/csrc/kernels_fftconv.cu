@@ -17,6 +17,7 @@
 // strided stores conflict-free.  Twiddles come from a two-level fp64-generated table in
 // shared memory and short product chains.  1/P^2 is folded into the kernel samples.
 #include <algorithm>
+#include <cstdlib>
 
 #include "device_math.cuh"
 #include "tfdp_internal.h"
@@ -212,7 +213,7 @@ enum { kZeroUpper = 1, kLowOut = 2 };
 // sub-transform size Ns (1 for the first stage, else a multiple of 16 since N % 256 == 0 and
 // the first stage is radix 16).  Loads + butterflies into registers, barrier, stores, barrier.
 template <int T, int R, int N, int Ns, bool ZERO_UPPER, bool LOW_OUT>
-__device__ __forceinline__ void stage(float2* buf, const float2* __restrict__ tw) {
+__device__ __forceinline__ void stage(float2* buf, const float2* __restrict__ tw, int tid) {
   constexpr int nb = N / R;
   constexpr int MB = (nb + T - 1) / T;  // butterflies per thread
   constexpr int step = nb / Ns;         // N / (Ns R)
@@ -222,7 +223,7 @@ __device__ __forceinline__ void stage(float2* buf, const float2* __restrict__ tw
   float2 v[MB][R];
 #pragma unroll
   for (int b = 0; b < MB; ++b) {
-    const int j = threadIdx.x + b * T;
+    const int j = tid + b * T;
     if (nb % T == 0 || j < nb) {
       const int pj = j + (j >> 4);
 #pragma unroll
@@ -244,7 +245,7 @@ __device__ __forceinline__ void stage(float2* buf, const float2* __restrict__ tw
   __syncthreads();
 #pragma unroll
   for (int b = 0; b < MB; ++b) {
-    const int j = threadIdx.x + b * T;
+    const int j = tid + b * T;
     if (nb % T == 0 || j < nb) {
       const int k = Ns == 1 ? 0 : (p2 ? (j & (Ns - 1)) : (j % Ns));
       const int d = (j - k) * R + k;
@@ -263,23 +264,25 @@ __host__ __device__ constexpr int next_radix(int rem) {
 }
 
 template <int T, int N, int FLAGS, int Ns, int REM>
-__device__ __forceinline__ void fft_rec(float2* buf, const float2* __restrict__ tw) {
+__device__ __forceinline__ void fft_rec(float2* buf, const float2* __restrict__ tw, int tid) {
   if constexpr (REM > 1) {
     constexpr int R = next_radix(REM);
     constexpr bool first = Ns == 1, last = REM == R;
     stage<T, R, N, Ns, first && (FLAGS & kZeroUpper) != 0,
-          last && (FLAGS & kLowOut) != 0 && R % 2 == 0>(buf, tw);
-    fft_rec<T, N, FLAGS, Ns * R, REM / R>(buf, tw);
+          last && (FLAGS & kLowOut) != 0 && R % 2 == 0>(buf, tw, tid);
+    fft_rec<T, N, FLAGS, Ns * R, REM / R>(buf, tw, tid);
   }
 }
 
 // Forward complex FFT of buf[0..N) in place (padded layout), N = 2^a 3^b 5^c, N % 256 == 0.
 // Radix 16 first (so Ns is a multiple of 16 afterwards), then 16/8/4/2, then 3, 5.  Called
-// by the whole block (T >= N/16 threads) after a barrier; ends with a barrier.
+// by the whole block after a barrier (threads tid = 0..T-1 of each group of T own one FFT;
+// the barriers are block-wide, so every group runs the same plan); ends with a barrier.
 template <int T, int N, int FLAGS>
-__device__ __forceinline__ void fft_smem(float2* buf, const float2* __restrict__ tw) {
+__device__ __forceinline__ void fft_smem(float2* buf, const float2* __restrict__ tw,
+                                         int tid = threadIdx.x) {
   static_assert(N % 256 == 0 && T * 16 >= N, "FFT plan");
-  fft_rec<T, N, FLAGS, 1, N>(buf, tw);
+  fft_rec<T, N, FLAGS, 1, N>(buf, tw, tid);
 }
 
 __global__ void twiddle_kernel(float2* tw, int N) {
@@ -381,48 +384,65 @@ TFDP_FFT_KERNEL(kspec_cols_kernel)(const GridGeom* __restrict__ geom,
 }
 
 // ---------------------------------------------------------------- forward rows
-TFDP_FFT_KERNEL(rows_fwd_kernel)(const GridGeom* __restrict__ geom, float* __restrict__ C,
-                                 int cpitch, const float2* __restrict__ tw,
-                                 float2* __restrict__ CA, int ca_pitch) {
+// RB row pairs per block (RB groups of T threads, one FFT each): the block's 2 RB rows are
+// consecutive in the column-major half spectra, so the transposed stores write 16 RB
+// contiguous bytes per q (RB = 1: half a sector).
+template <int P, int RB>
+constexpr int rows_min_blocks() {
+  return kMinBlocks<fft_threads_c(P)> / RB > 0 ? kMinBlocks<fft_threads_c(P)> / RB : 1;
+}
+
+template <int P, int RB>
+__global__ void __launch_bounds__(fft_threads_c(P) * RB, (rows_min_blocks<P, RB>()))
+rows_fwd_kernel(const GridGeom* __restrict__ geom, float* __restrict__ C, int cpitch,
+                const float2* __restrict__ tw, float2* __restrict__ CA, int ca_pitch) {
   constexpr int T = fft_threads_c(P);
+  constexpr int NT = T * RB;
+  constexpr int PL = padded_len(P);
   extern __shared__ float2 sm[];
-  float2* a = sm;
-  float2* tws = sm + padded_len(P);
+  float2* tws = sm + RB * PL;
   load_tw(tws, tw, P);  // constant since the plan: safe before the wait
   pdl_wait();
   pdl_trigger();
   const int M = geom->M;
-  const int ra = 2 * blockIdx.x, rb = ra + 1;
-  if (ra >= M) return;
+  const int p0 = blockIdx.x * RB;  // first row pair of the block
+  if (2 * p0 >= M) return;
+  const int g = threadIdx.x / T, lt = threadIdx.x - g * T;
+  const int ra = 2 * (p0 + g), rb = ra + 1;
+  const bool ha = ra < M, hb = rb < M;
   const int ch = blockIdx.y;
+  float2* a = sm + g * PL;
   float* rowa = C + ((int64_t)ch * cpitch + ra) * cpitch;
   float* rowb = rowa + cpitch;
-  const bool hb = rb < M;
   constexpr int half = P / 2;
 #pragma unroll
-  for (int x = threadIdx.x; x < half; x += T) {  // [P/2, P) is zero and never read
+  for (int x = lt; x < half; x += T) {  // [P/2, P) is zero and never read
     float va = 0.f, vb = 0.f;
     if (x < M) {
-      va = __ldcs(rowa + x);  // read once: evict-first
+      if (ha) va = __ldcs(rowa + x);  // read once: evict-first
       if (hb) vb = __ldcs(rowb + x);
     }
     a[pad(x)] = make_float2(va, vb);
   }
   // consumed: leave the planes zero for the next spread (stores issued after all loads)
-  for (int x = threadIdx.x; x < M; x += T) {
-    rowa[x] = 0.f;
+  for (int x = lt; x < M; x += T) {
+    if (ha) rowa[x] = 0.f;
     if (hb) rowb[x] = 0.f;
   }
   __syncthreads();
-  fft_smem<T, P, kZeroUpper>(a, tws);
-  float2* out = CA + (int64_t)ch * (half + 1) * ca_pitch;
-  for (int q = threadIdx.x; q <= half; q += T) {
-    const float2 z = a[pad(q)];
-    const float2 zc = conjf2(a[pad(q == 0 ? 0 : P - q)]);
+  fft_smem<T, P, kZeroUpper>(a, tws, lt);
+  const int rows_here = min(2 * RB, M - 2 * p0);
+  float2* out = CA + (int64_t)ch * (half + 1) * ca_pitch + 2 * p0;
+  for (int f = threadIdx.x; f < (half + 1) * RB; f += NT) {
+    const int q = f / RB, gg = f - q * RB;
+    if (2 * gg >= rows_here) continue;
+    const float2* ag = sm + gg * PL;
+    const float2 z = ag[pad(q)];
+    const float2 zc = conjf2(ag[pad(q == 0 ? 0 : P - q)]);
     const float2 xa = make_float2(0.5f * (z.x + zc.x), 0.5f * (z.y + zc.y));
     const float2 xb = mul_mi(make_float2(0.5f * (z.x - zc.x), 0.5f * (z.y - zc.y)));
-    float2* o = out + (int64_t)q * ca_pitch + ra;
-    if (hb) *reinterpret_cast<float4*>(o) = make_float4(xa.x, xa.y, xb.x, xb.y);
+    float2* o = out + (int64_t)q * ca_pitch + 2 * gg;
+    if (2 * gg + 1 < rows_here) *reinterpret_cast<float4*>(o) = make_float4(xa.x, xa.y, xb.x, xb.y);
     else *o = xa;
   }
 }
@@ -463,49 +483,56 @@ TFDP_FFT_KERNEL(cols_kernel)(const GridGeom* __restrict__ geom, float2* __restri
 }
 
 // ---------------------------------------------------------------- inverse rows
-TFDP_FFT_KERNEL(rows_inv_kernel)(const GridGeom* __restrict__ geom,
-                                 const float2* __restrict__ CA, int ca_pitch,
-                                 const float2* __restrict__ tw, float* __restrict__ Phi,
-                                 int cpitch) {
+// RB row pairs per block as in rows_fwd: the transposed loads read 16 RB contiguous bytes
+// per q, each half-spectrum entry once (it feeds q and its Hermitian mirror P - q).
+template <int P, int RB>
+__global__ void __launch_bounds__(fft_threads_c(P) * RB, (rows_min_blocks<P, RB>()))
+rows_inv_kernel(const GridGeom* __restrict__ geom, const float2* __restrict__ CA, int ca_pitch,
+                const float2* __restrict__ tw, float* __restrict__ Phi, int cpitch) {
   constexpr int T = fft_threads_c(P);
+  constexpr int NT = T * RB;
+  constexpr int PL = padded_len(P);
   extern __shared__ float2 sm[];
-  float2* a = sm;
-  float2* tws = sm + padded_len(P);
+  float2* tws = sm + RB * PL;
   load_tw(tws, tw, P);  // constant since the plan: safe before the wait
   pdl_wait();
   pdl_trigger();
   const int M = geom->M;
-  const int ra = 2 * blockIdx.x, rb = ra + 1;
-  if (ra >= M) return;
+  const int p0 = blockIdx.x * RB;
+  if (2 * p0 >= M) return;
   const int ch = blockIdx.y;
-  const bool hb = rb < M;
+  const int rows_here = min(2 * RB, M - 2 * p0);
   constexpr int half = P / 2;
-  const float2* in = CA + (int64_t)ch * (half + 1) * ca_pitch;
+  const float2* in = CA + (int64_t)ch * (half + 1) * ca_pitch + 2 * p0;
   // Z[q] = Xa[q] + i Xb[q] over the full circle (Hermitian extension), stored conjugated so
   // that the forward FFT computes the inverse.
-#pragma unroll 8
-  for (int q = threadIdx.x; q < P; q += T) {
-    const int qq = (q <= half) ? q : P - q;
-    float2 xa, xb = make_float2(0.f, 0.f);
-    const float2* p = in + (int64_t)qq * ca_pitch + ra;
-    if (hb) {
+#pragma unroll 4
+  for (int f = threadIdx.x; f < (half + 1) * RB; f += NT) {
+    const int q = f / RB, gg = f - q * RB;
+    float2 xa = make_float2(0.f, 0.f), xb = make_float2(0.f, 0.f);
+    const float2* p = in + (int64_t)q * ca_pitch + 2 * gg;
+    if (2 * gg + 1 < rows_here) {
       const float4 v = *reinterpret_cast<const float4*>(p);
       xa = make_float2(v.x, v.y);
       xb = make_float2(v.z, v.w);
-    } else {
+    } else if (2 * gg < rows_here) {
       xa = *p;
     }
-    if (q > half) {
-      xa = conjf2(xa);
-      xb = conjf2(xb);
-    }
-    a[pad(q)] = conjf2(make_float2(xa.x - xb.y, xa.y + xb.x));  // conj(xa + i xb)
+    float2* ag = sm + gg * PL;
+    ag[pad(q)] = conjf2(make_float2(xa.x - xb.y, xa.y + xb.x));  // conj(xa + i xb)
+    if (q > 0 && q < half)  // mirror P - q: conj(conj(xa) + i conj(xb))
+      ag[pad(P - q)] = make_float2(xa.x + xb.y, xa.y - xb.x);
   }
   __syncthreads();
-  fft_smem<T, P, kLowOut>(a, tws);
+  const int g = threadIdx.x / T, lt = threadIdx.x - g * T;
+  float2* a = sm + g * PL;
+  fft_smem<T, P, kLowOut>(a, tws, lt);
+  const int ra = 2 * (p0 + g), rb = ra + 1;
+  if (ra >= M) return;
+  const bool hb = rb < M;
   float* pa = Phi + ((int64_t)ch * cpitch + ra) * cpitch;
   float* pb = pa + cpitch;
-  for (int x = threadIdx.x; x < M; x += T) {
+  for (int x = lt; x < M; x += T) {
     const float2 z = a[pad(x)];  // conj(result) = xa + i xb
     pa[x] = z.x;
     if (hb) pb[x] = -z.y;
@@ -526,25 +553,51 @@ bool fft_size_supported(int P) {
   return false;
 }
 
-size_t fftconv_smem_bytes(int P) { return (size_t)(padded_len(P) + tw_len(P)) * sizeof(float2); }
+size_t fftconv_smem_bytes(int P, int groups) {
+  return (size_t)(groups * padded_len(P) + tw_len(P)) * sizeof(float2);
+}
+
+// Row pairs per block of the row passes: 2 up to 512-thread blocks (P <= 4096; C4 k = 1:
+// rows_fwd 27.0 -> 23.0 us, k = 2: 94.8 -> 77.3 us), else 1 (P = 6144 at RB = 2 holds one
+// 768-thread block per SM: 217 -> 232 us).  TFDP_ROWS_RB = 1, 2, 4 overrides (A/B runs),
+// limited to blocks of <= 1024 threads.
+int rows_rb(int P) {
+  static const int env = [] {
+    const char* e = std::getenv("TFDP_ROWS_RB");
+    return e ? std::atoi(e) : 0;
+  }();
+  int rb = env == 4 ? 4 : env == 1 ? 1 : env == 2 ? 2 : (fft_threads_c(P) * 2 <= 512 ? 2 : 1);
+  while (rb > 1 && fft_threads_c(P) * rb > 1024) rb /= 2;
+  return rb;
+}
 
 cudaError_t fftconv_prepare(int P) {
-  const int b = (int)fftconv_smem_bytes(P);
+  const int b = (int)fftconv_smem_bytes(P, 1);
+  const int rb = rows_rb(P);
+  const int br = (int)fftconv_smem_bytes(P, rb);
   cudaError_t e = cudaErrorInvalidValue;
+#define TFDP_PREP_ROWS(S, RB)                                                                  \
+  if constexpr (fft_threads_c(S) * RB <= 1024) {                                             \
+    if (e == cudaSuccess && rb == RB) {                                                        \
+      e = cudaFuncSetAttribute(rows_fwd_kernel<S, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, br); \
+      if (e == cudaSuccess)                                                                    \
+        e = cudaFuncSetAttribute(rows_inv_kernel<S, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, br); \
+    }                                                                                          \
+  }
 #define TFDP_PREP(S)                                                                          \
   case S:                                                                                     \
     e = cudaFuncSetAttribute(kspec_rows_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, b); \
     if (e == cudaSuccess)                                                                     \
       e = cudaFuncSetAttribute(kspec_cols_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, b); \
     if (e == cudaSuccess)                                                                     \
-      e = cudaFuncSetAttribute(rows_fwd_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, b); \
-    if (e == cudaSuccess)                                                                     \
       e = cudaFuncSetAttribute(cols_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, b); \
-    if (e == cudaSuccess)                                                                     \
-      e = cudaFuncSetAttribute(rows_inv_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, b); \
+    TFDP_PREP_ROWS(S, 1)                                                                      \
+    TFDP_PREP_ROWS(S, 2)                                                                      \
+    TFDP_PREP_ROWS(S, 4)                                                                      \
     break;
   switch (P) { TFDP_FFT_SIZES(TFDP_PREP) default: break; }
 #undef TFDP_PREP
+#undef TFDP_PREP_ROWS
   return e;
 }
 
@@ -554,7 +607,7 @@ void launch_twiddles(float2* tw, int P, cudaStream_t s) {
 
 void launch_kspec(const GridGeom* geom, int P, int Mcap, ForceArgs fa, const float2* tw,
                   float* KA, int ka_pitch, float* KH, cudaStream_t s) {
-  const size_t sm = fftconv_smem_bytes(P);
+  const size_t sm = fftconv_smem_bytes(P, 1);
 #define TFDP_KS(S)                                                                          \
   case S:                                                                                   \
     kspec_rows_kernel<S><<<(unsigned)((Mcap + 1) / 2), fft_threads_c(S), sm, s>>>(          \
@@ -566,13 +619,28 @@ void launch_kspec(const GridGeom* geom, int P, int Mcap, ForceArgs fa, const flo
 #undef TFDP_KS
 }
 
+// launches one instantiation per (P, RB) with RB a compile-time constant
+#define TFDP_ROWS_DISPATCH(S, KERN, ...)                                                       \
+  {                                                                                           \
+    const int rb = rows_rb(S);                                                                \
+    const size_t smb = fftconv_smem_bytes(S, rb);                                             \
+    const dim3 grid((unsigned)(((Mcap + 1) / 2 + rb - 1) / rb), 3);                           \
+    if (rb == 4) {                                                                            \
+      if constexpr (fft_threads_c(S) * 4 <= 1024)                                             \
+        launch_chained(KERN<S, 4>, grid, fft_threads_c(S) * 4, smb, s, __VA_ARGS__);          \
+    } else if (rb == 2) {                                                                     \
+      if constexpr (fft_threads_c(S) * 2 <= 1024)                                             \
+        launch_chained(KERN<S, 2>, grid, fft_threads_c(S) * 2, smb, s, __VA_ARGS__);          \
+    } else {                                                                                  \
+      launch_chained(KERN<S, 1>, grid, fft_threads_c(S), smb, s, __VA_ARGS__);                \
+    }                                                                                         \
+  }
+
 void launch_rows_fwd(const GridGeom* geom, float* C, int cpitch, int P, int Mcap,
                      const float2* tw, float2* CA, int ca_pitch, cudaStream_t s) {
-  const size_t sm = fftconv_smem_bytes(P);
 #define TFDP_RF(S)                                                                          \
   case S:                                                                                   \
-    launch_chained(rows_fwd_kernel<S>, dim3((unsigned)((Mcap + 1) / 2), 3), fft_threads_c(S), \
-                   sm, s, geom, C, cpitch, tw, CA, ca_pitch);                               \
+    TFDP_ROWS_DISPATCH(S, rows_fwd_kernel, geom, C, cpitch, tw, CA, ca_pitch)               \
     break;
   switch (P) { TFDP_FFT_SIZES(TFDP_RF) default: break; }
 #undef TFDP_RF
@@ -580,7 +648,7 @@ void launch_rows_fwd(const GridGeom* geom, float* C, int cpitch, int P, int Mcap
 
 void launch_cols(const GridGeom* geom, float2* CA, int ca_pitch, const float* KH, int P,
                  const float2* tw, cudaStream_t s) {
-  const size_t sm = fftconv_smem_bytes(P);
+  const size_t sm = fftconv_smem_bytes(P, 1);
 #define TFDP_CO(S)                                                                          \
   case S:                                                                                   \
     cols_kernel<S><<<(unsigned)(3 * (S / 2 + 1)), fft_threads_c(S), sm, s>>>(               \
@@ -592,11 +660,9 @@ void launch_cols(const GridGeom* geom, float2* CA, int ca_pitch, const float* KH
 
 void launch_rows_inv(const GridGeom* geom, const float2* CA, int ca_pitch, int P, int Mcap,
                      const float2* tw, float* Phi, int cpitch, cudaStream_t s) {
-  const size_t sm = fftconv_smem_bytes(P);
 #define TFDP_RI(S)                                                                          \
   case S:                                                                                   \
-    launch_chained(rows_inv_kernel<S>, dim3((unsigned)((Mcap + 1) / 2), 3), fft_threads_c(S), \
-                   sm, s, geom, CA, ca_pitch, tw, Phi, cpitch);                             \
+    TFDP_ROWS_DISPATCH(S, rows_inv_kernel, geom, CA, ca_pitch, tw, Phi, cpitch)             \
     break;
   switch (P) { TFDP_FFT_SIZES(TFDP_RI) default: break; }
 #undef TFDP_RI
