@@ -169,6 +169,31 @@ tfdp_status tfdp_set_params(tfdp_ctx* ctx, const tfdp_params* p);
  * errors of tfdp_step. */
 tfdp_status tfdp_global_refine(tfdp_ctx* ctx, double gamma, double rho, int32_t iterations);
 
+/* Local (fisheye) refinement mask (SPEC RefinementMask S:155-158).  The region
+ * F u N(F) = the focal nodes and their graph neighbours.  Forces with the mask:
+ *   repulsion pair weight  lf if both ends are in the region, ls if both are outside, else 1
+ *   attraction edge weight la if both ends are in the region, else 1
+ * ("we enhance the attractive forces between the focal nodes and their neighbors ... while
+ * exerting repulsive forces to highlight them ... large repulsive forces between other
+ * nodes").  The exact path applies the weights exactly; the ibFFT path computes the unmasked
+ * grid sum S_all plus an exact sum S1 over the region's sources and combines
+ * rho [w0 (S_all - S1) + w1 S1] (R23).  The mask stays active for every later
+ * tfdp_step / tfdp_forces until replaced; n_focal = 0 clears it; boosts (1, 1, 1) are the
+ * identity (the unmasked kernels run).
+ *   focal   host int32[n_focal] caller node ids (duplicates allowed)
+ *   la, lf, ls  boosts >= 1, finite
+ * TFDP_ERR_ARG on an id out of range, a boost < 1 or non-finite.  Syncs the stream.  Cost per
+ * iteration: one n_local x |region| exact pass. */
+tfdp_status tfdp_set_focus(tfdp_ctx* ctx, const int32_t* focal, int64_t n_focal, double la,
+                           double lf, double ls);
+
+/* Local refinement (SPEC local_refine S:368-372): tfdp_set_focus, then `iterations`
+ * iterations t = 0 .. T-1 from the current layout (T = iterations, schedules rebuilt, as in
+ * tfdp_global_refine).  TFDP_ERR_ARG on an empty focal set or iterations < 1; else
+ * the errors of tfdp_set_focus and tfdp_step.  The mask stays set afterwards. */
+tfdp_status tfdp_local_refine(tfdp_ctx* ctx, const int32_t* focal, int64_t n_focal, double la,
+                              double lf, double ls, int32_t iterations);
+
 /* Neighbourhood preservation NP1 of the current layout, computed on
  * the device (NEXT-3: per-iteration convergence traces):
  *   NP1 = (1/n) sum_i |N_G(i) ∩ N_L(i, k_i)| / |N_G(i) ∪ N_L(i, k_i)|,  k_i = deg(i),

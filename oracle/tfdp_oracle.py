@@ -26,6 +26,9 @@ __all__ = [
     "lagrange_weights", "spread", "kernel_tdist", "convolve_direct", "convolve_fft",
     "gather", "repulsion_ibfft", "forces", "step", "run", "np1", "rel_l2",
     "equilibrium_distance", "global_refine", "np1_hits", "np1_from_hits",
+    "Focus", "focus_region", "repulsion_masked_exact", "repulsion_masked_loops",
+    "attraction_masked", "repulsion_masked_ibfft", "forces_masked", "energy_masked",
+    "local_refine",
 ]
 
 
@@ -446,6 +449,157 @@ def global_refine(X, row_ptr, col, p: Params = Params(), gamma: float | None = N
     if not (g > 1.0) or not (r > 0.0):
         raise ValueError("global refinement needs gamma > 1 and rho > 0 (S:362)")
     return run(X, row_ptr, col, dataclasses.replace(p, gamma=g, rho=r), T=T, **kw)
+
+
+# ---------------------------------------------------------------------------------------
+# Local (fisheye) refinement (SPEC RefinementMask S:155-158, local_refine S:368-376)
+# ---------------------------------------------------------------------------------------
+@dataclasses.dataclass
+class Focus:
+    """RefinementMask: focal node set F and boosts lambda_a (attraction on edges
+    with both ends in F u N(F)), lambda_f (repulsion among F u N(F)), lambda_s (repulsion
+    among the other nodes); every boost >= 1.  Pairs with one end in the region keep
+    weight 1 (reading R23)."""
+    focal: tuple
+    la: float = 1.0
+    lf: float = 1.0
+    ls: float = 1.0
+
+
+def focus_region(n, row_ptr, col, focal):
+    """label_i = 1 for i in F u N(F) (the focal nodes and their graph neighbours), else 0."""
+    lab = np.zeros(n, dtype=np.int64)
+    for f in focal:
+        f = int(f)
+        lab[f] = 1
+        lab[col[row_ptr[f]:row_ptr[f + 1]]] = 1
+    return lab
+
+
+def _rep_weights(lab_i, lab_j, fo: Focus):
+    """w_ij = lambda_f if both in the region, lambda_s if both outside, else 1."""
+    both_in = (lab_i == 1) & (lab_j == 1)
+    both_out = (lab_i == 0) & (lab_j == 0)
+    return np.where(both_in, fo.lf, np.where(both_out, fo.ls, 1.0))
+
+
+def repulsion_masked_exact(X, lab, fo: Focus, gamma=2.0, rho=1.0):
+    """Masked repulsion, the definition written out: R_i = rho sum_j w_ij (x_i - x_j) s_ij^-gamma
+    (Eq. repfK P:463 with the per-pair boosts of the refinement mask)."""
+    X = np.asarray(X, dtype=np.float64)
+    lab = np.asarray(lab)
+    r = X[:, None, :] - X[None, :, :]
+    sij = 1.0 + (r * r).sum(-1)
+    w = _rep_weights(lab[:, None], lab[None, :], fo)
+    return rho * (r * (w * sij ** (-gamma))[..., None]).sum(1)
+
+
+def repulsion_masked_loops(X, lab, fo: Focus, gamma=2.0, rho=1.0):
+    """Literal double loop of the masked repulsion (brute force, small n)."""
+    X = np.asarray(X, dtype=np.float64)
+    n = X.shape[0]
+    out = np.zeros((n, 2))
+    for i in range(n):
+        for j in range(n):
+            if i == j:
+                continue
+            if lab[i] and lab[j]:
+                w = fo.lf
+            elif not lab[i] and not lab[j]:
+                w = fo.ls
+            else:
+                w = 1.0
+            dx, dy = X[i, 0] - X[j, 0], X[i, 1] - X[j, 1]
+            f = w * (1.0 + dx * dx + dy * dy) ** (-gamma)
+            out[i, 0] += rho * f * dx
+            out[i, 1] += rho * f * dy
+    return out
+
+
+def attraction_masked(X, row_ptr, col, lab, fo: Focus, alpha=0.1, beta=8.0):
+    """A_i = -alpha sum_{j in adj(i)} a_ij (1 + beta/s_ij)(x_i - x_j), a_ij = lambda_a if both
+    ends are in F u N(F) else 1 (P:26 'we enhance the attractive forces between the focal
+    nodes and their neighbors')."""
+    X = np.asarray(X, dtype=np.float64)
+    row_ptr = np.asarray(row_ptr, dtype=np.int64)
+    col = np.asarray(col, dtype=np.int64)
+    n = X.shape[0]
+    rows = np.repeat(np.arange(n), np.diff(row_ptr))
+    r = X[rows] - X[col]
+    s = 1.0 + (r * r).sum(1)
+    a = np.where((lab[rows] == 1) & (lab[col] == 1), fo.la, 1.0)
+    out = np.zeros((n, 2))
+    np.add.at(out, rows, -alpha * (a * (1.0 + beta / s))[:, None] * r)
+    return out
+
+
+def repulsion_masked_ibfft(X, lab, fo: Focus, k: int, gamma=2.0, rho=1.0, **kw):
+    """Masked repulsion on the interpolation/FFT path (reading R23): the grid cannot carry
+    per-pair weights, so with S_all the unmasked sum (ibFFT) and S1_i the exact sum over the
+    region's sources j in F u N(F),
+      R_i = rho [w0(i) (S_all,i - S1_i) + w1(i) S1_i],  w0/w1 = the weight of (i, j) for j
+    outside / inside the region (exact masked corrections inside the region)."""
+    X = np.asarray(X, dtype=np.float64)
+    lab = np.asarray(lab)
+    R_all = repulsion_ibfft(X, k, gamma, 1.0, **kw)
+    src = np.nonzero(lab == 1)[0]
+    r = X[:, None, :] - X[None, src, :]
+    S1 = (r * ((1.0 + (r * r).sum(-1)) ** (-gamma))[..., None]).sum(1)
+    w0 = np.where(lab == 1, 1.0, fo.ls)[:, None]
+    w1 = np.where(lab == 1, fo.lf, 1.0)[:, None]
+    return rho * (w0 * (R_all - S1) + w1 * S1)
+
+
+def forces_masked(X, row_ptr, col, lab, fo: Focus, p: Params = Params(), solver="exact",
+                  k: int = 3, **kw):
+    if solver == "exact":
+        R = repulsion_masked_exact(X, lab, fo, p.gamma, p.rho)
+    else:
+        R = repulsion_masked_ibfft(X, lab, fo, k, p.gamma, p.rho, **kw)
+    return R, attraction_masked(X, row_ptr, col, lab, fo, p.alpha, p.beta)
+
+
+def energy_masked(X, row_ptr, col, lab, fo: Focus, p: Params = Params()):
+    """E with D = -grad E for the masked forces (constant weights; gamma > 1):
+    rho sum_{i<j} w_ij s^(1-gamma)/(2(gamma-1)) + alpha sum_edges a_ij (d^2/2 + (beta/2) ln s)."""
+    X = np.asarray(X, dtype=np.float64)
+    n = X.shape[0]
+    iu, ju = np.triu_indices(n, 1)
+    r = X[iu] - X[ju]
+    s = 1.0 + (r * r).sum(1)
+    w = _rep_weights(lab[iu], lab[ju], fo)
+    Er = p.rho * (w * s ** (1.0 - p.gamma)).sum() / (2.0 * (p.gamma - 1.0))
+    rows = np.repeat(np.arange(n), np.diff(np.asarray(row_ptr)))
+    col = np.asarray(col)
+    keep = rows < col
+    r = X[rows[keep]] - X[col[keep]]
+    s = 1.0 + (r * r).sum(1)
+    a = np.where((lab[rows[keep]] == 1) & (lab[col[keep]] == 1), fo.la, 1.0)
+    Ea = p.alpha * (a * (0.5 * (s - 1.0) + 0.5 * p.beta * np.log(s))).sum()
+    return Er + Ea
+
+
+def local_refine(X, row_ptr, col, fo: Focus, p: Params = Params(), T: int = 300,
+                 eta0: float = 0.1, solver: str = "exact", k: int = 0, cooling: str = "linear",
+                 **kw):
+    """Local refinement (SPEC local_refine S:368-372): re-run from the given layout
+    for t = 0 .. T-1 with the refinement mask.  Empty focal set -> ValueError."""
+    if len(fo.focal) == 0:
+        raise ValueError("empty focal set (S:372)")
+    if min(fo.la, fo.lf, fo.ls) < 1.0:
+        raise ValueError("boosts must be >= 1 (S:156)")
+    X = np.asarray(X, dtype=np.float64).copy()
+    n = X.shape[0]
+    lab = focus_region(n, row_ptr, col, fo.focal)
+    ks = k_schedule(T)
+    for t in range(T):
+        kt = int(ks[t]) if k == 0 else k
+        R, A = forces_masked(X, row_ptr, col, lab, fo, p, solver=solver, k=kt, **kw)
+        X = X + eta(t, T, eta0, cooling) * (R + A)
+        bad = ~np.isfinite(X).all(1)
+        if bad.any():
+            raise FloatingPointError(f"diverged at iter {t} node {int(np.argmax(bad))}")
+    return X
 
 
 # ---------------------------------------------------------------------------------------

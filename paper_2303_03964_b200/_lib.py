@@ -53,6 +53,9 @@ _SIGS = {
     "tfdp_set_params": (C.c_int, [_P, C.POINTER(tfdp_params)]),
     "tfdp_global_refine": (C.c_int, [_P, C.c_double, C.c_double, C.c_int32]),
     "tfdp_np1": (C.c_int, [_P, C.POINTER(C.c_double), _P]),
+    "tfdp_set_focus": (C.c_int, [_P, _P, C.c_int64, C.c_double, C.c_double, C.c_double]),
+    "tfdp_local_refine": (C.c_int, [_P, _P, C.c_int64, C.c_double, C.c_double, C.c_double,
+                                    C.c_int32]),
     "tfdp_shard": (C.c_int, [_P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "tfdp_fft_geometry": (C.c_int, [_P, _P, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                     C.POINTER(C.c_int32)]),

@@ -128,6 +128,15 @@ struct tfdp_ctx {
   BoxKeys* np_slots = nullptr;
   BoxKeys* np_keys = nullptr;
   double* np_sum = nullptr;
+  // local refinement mask (kernels_focus.cu), tfdp_set_focus
+  bool focus_on = false;
+  float fo_la = 1.f, fo_lf = 1.f, fo_ls = 1.f;
+  unsigned char* label_caller = nullptr;
+  unsigned char* label_slot = nullptr;
+  int* region_caller = nullptr;
+  int* region_slot = nullptr;
+  int region_m = 0, region_cap = 0;
+  float2* s1 = nullptr;
   struct Pend {
     int kind;
     cudaEvent_t a, b;
@@ -490,6 +499,12 @@ tfdp_status evaluate(tfdp_ctx* c, int update, float eta, int k) {
   const int64_t n_local = c->hi - c->lo;
   float2* xy = c->xy[c->cur];
   float2* xyn = c->xy[c->cur ^ 1];
+  tfdp::FocusArgs fo{nullptr, nullptr, 1.f, 1.f, 1.f};
+  if (c->focus_on) {  // exact repulsion sum over the focal region's sources (R23)
+    tfdp::launch_focus_s1(xy, c->lo, n_local, c->region_slot, c->region_m, c->fa, c->s1, c->stream);
+    c->launches++;
+    fo = tfdp::FocusArgs{c->label_slot, c->s1, c->fo_la, c->fo_lf, c->fo_ls};
+  }
   if (c->p.solver == TFDP_EXACT) {
     {
       Scope sc(c, K_EXACT_PARTIAL);
@@ -499,7 +514,7 @@ tfdp_status evaluate(tfdp_ctx* c, int update, float eta, int k) {
     {
       Scope sc(c, K_EXACT_FINISH);
       tfdp::launch_exact_finish(xy, xyn, c->lo, n_local, c->n_chunks, c->part, c->row_ptr,
-                                c->col, c->fa, eta, c->t, update, c->rep, c->att, c->diverge,
+                                c->col, c->fa, fo, eta, c->t, update, c->rep, c->att, c->diverge,
                                 c->stream);
     }
   } else {
@@ -573,7 +588,7 @@ tfdp_status evaluate(tfdp_ctx* c, int update, float eta, int k) {
       BoxKeys* nk = (update && c->world == 1) ? c->box_part : nullptr;
       if (nk) c->n_part = tfdp::kBoxSlots;
       tfdp::launch_gather_update(xy, xyn, c->lo, n_local, c->geom, k, c->phi, c->row_ptr, c->col,
-                                 c->fa, eta, c->t, update, c->rep, c->att, c->diverge, nk,
+                                 c->fa, fo, eta, c->t, update, c->rep, c->att, c->diverge, nk,
                                  c->stream);
     }
     c->box_valid = update && c->world == 1;
@@ -636,6 +651,11 @@ tfdp_status reorder_nodes(tfdp_ctx* c) {
   std::swap(c->perm, c->perm2);
   std::swap(c->inv, c->inv2);
   c->cur ^= 1;
+  if (c->focus_on) {  // the mask follows the renumbering
+    tfdp::launch_focus_slots(c->label_caller, c->perm, c->inv, c->n, c->region_caller,
+                             c->region_m, c->label_slot, c->region_slot, c->stream);
+    c->launches += c->region_m > 0 ? 2 : 1;
+  }
   c->box_valid = true;
   c->n_part = tfdp::kBoxSlots;
   CUDA_TRY(c, cudaGetLastError());
@@ -1096,6 +1116,82 @@ tfdp_status tfdp_np1(tfdp_ctx* c, double* np1, int32_t* hits) {
   return TFDP_OK;
 }
 
+tfdp_status tfdp_set_focus(tfdp_ctx* c, const int32_t* focal, int64_t n_focal, double la,
+                           double lf, double ls) {
+  if (!c) return fail(nullptr, TFDP_ERR_ARG, "ctx is NULL");
+  if (c->errored) return fail(c, TFDP_ERR_STATE, "context is errored: %s", c->err.c_str());
+  if (n_focal < 0 || (n_focal > 0 && !focal)) return fail(c, TFDP_ERR_ARG, "bad focal list");
+  if (n_focal == 0) {
+    c->focus_on = false;
+    return TFDP_OK;
+  }
+  if (!std::isfinite(la) || !std::isfinite(lf) || !std::isfinite(ls) || la < 1.0 || lf < 1.0 ||
+      ls < 1.0)
+    return fail(c, TFDP_ERR_ARG, "boosts must be finite and >= 1 (S:156), got %g %g %g", la, lf, ls);
+  if (n_focal > c->n) return fail(c, TFDP_ERR_ARG, "more focal nodes than nodes");
+  for (int64_t i = 0; i < n_focal; ++i)
+    if (focal[i] < 0 || focal[i] >= c->n)
+      return fail(c, TFDP_ERR_ARG, "focal node %lld out of range", (long long)focal[i]);
+  cudaSetDevice(c->device);
+  const int64_t n_local = c->hi - c->lo;
+  if (!c->label_caller) {
+    CUDA_TRY(c, cudaMalloc(&c->label_caller, c->n));
+    CUDA_TRY(c, cudaMalloc(&c->label_slot, c->n));
+    CUDA_TRY(c, cudaMalloc(&c->s1, std::max<int64_t>(n_local, 1) * sizeof(float2)));
+  }
+  int* dfocal = nullptr;
+  CUDA_TRY(c, cudaMalloc(&dfocal, n_focal * sizeof(int)));
+  cudaMemcpyAsync(dfocal, focal, n_focal * sizeof(int), cudaMemcpyHostToDevice, c->stream);
+  cudaMemsetAsync(c->label_caller, 0, c->n, c->stream);
+  const int64_t* rp = c->reorder ? c->row_ptr_o : c->row_ptr;  // caller-order CSR
+  const int32_t* cl = c->reorder ? c->col_o : c->col;
+  tfdp::launch_mark_focus(dfocal, (int)n_focal, rp, cl, c->label_caller, c->stream);
+  std::vector<unsigned char> lab(c->n);
+  cudaMemcpyAsync(lab.data(), c->label_caller, c->n, cudaMemcpyDeviceToHost, c->stream);
+  const cudaError_t e = cudaStreamSynchronize(c->stream);
+  cudaFree(dfocal);
+  CUDA_TRY(c, e);
+  std::vector<int> region;  // caller ids of F u N(F), ascending (fixed source order of S1)
+  for (int64_t i = 0; i < c->n; ++i)
+    if (lab[i]) region.push_back((int)i);
+  if ((int)region.size() > c->region_cap) {
+    cudaFree(c->region_caller);
+    cudaFree(c->region_slot);
+    c->region_caller = c->region_slot = nullptr;
+    CUDA_TRY(c, cudaMalloc(&c->region_caller, region.size() * sizeof(int)));
+    CUDA_TRY(c, cudaMalloc(&c->region_slot, region.size() * sizeof(int)));
+    c->region_cap = (int)region.size();
+  }
+  c->region_m = (int)region.size();
+  CUDA_TRY(c, cudaMemcpyAsync(c->region_caller, region.data(), region.size() * sizeof(int),
+                              cudaMemcpyHostToDevice, c->stream));
+  tfdp::launch_focus_slots(c->label_caller, c->reorder ? c->perm : nullptr,
+                           c->reorder ? c->inv : nullptr, c->n, c->region_caller, c->region_m,
+                           c->label_slot, c->region_slot, c->stream);
+  c->launches += 3;
+  CUDA_TRY(c, cudaGetLastError());
+  c->fo_la = (float)la;
+  c->fo_lf = (float)lf;
+  c->fo_ls = (float)ls;
+  // the identity mask changes nothing: run the unmasked kernels, bit for bit
+  c->focus_on = !(la == 1.0 && lf == 1.0 && ls == 1.0);
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return TFDP_OK;
+}
+
+tfdp_status tfdp_local_refine(tfdp_ctx* c, const int32_t* focal, int64_t n_focal, double la,
+                              double lf, double ls, int32_t iterations) {
+  if (!c) return fail(nullptr, TFDP_ERR_ARG, "ctx is NULL");
+  if (n_focal < 1) return fail(c, TFDP_ERR_ARG, "empty focal set (S:372)");
+  if (iterations < 1) return fail(c, TFDP_ERR_ARG, "iterations must be >= 1");
+  TRY(tfdp_set_focus(c, focal, n_focal, la, lf, ls));
+  tfdp_params p = c->p;
+  p.iterations = iterations;
+  p.t0 = 0;
+  TRY(tfdp_set_params(c, &p));
+  return tfdp_step(c, iterations);
+}
+
 tfdp_status tfdp_global_refine(tfdp_ctx* c, double gamma, double rho, int32_t iterations) {
   if (!c) return fail(nullptr, TFDP_ERR_ARG, "ctx is NULL");
   if (!std::isfinite(gamma) || gamma <= 1.0)
@@ -1225,6 +1321,11 @@ void tfdp_destroy(tfdp_ctx* c) {
   cudaFree(c->col_o);
   cudaFree(c->rscratch);
   cudaFree(c->iobuf);
+  cudaFree(c->label_caller);
+  cudaFree(c->label_slot);
+  cudaFree(c->region_caller);
+  cudaFree(c->region_slot);
+  cudaFree(c->s1);
   cudaFree(c->np_scratch);
   cudaFree(c->np_hits);
   cudaFree(c->np_hits2);

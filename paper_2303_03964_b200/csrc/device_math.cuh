@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "tfdp_internal.h"
+
 namespace tfdp {
 
 // PDL (tfdp_internal.h launch_chained): let the next chain kernel be scheduled now / wait
@@ -87,6 +89,40 @@ __device__ __forceinline__ float2 attraction_sum(const float2* __restrict__ xy, 
   }
   for (; e < e1; ++e) term(__ldg(xy + __ldg(col + e)));
   return make_float2(sx, sy);
+}
+
+// Attraction row sum with the refinement mask's edge weight (la on edges whose both ends are
+// in the focal region): rows outside the region take the unmasked path (weight 1).
+__device__ __forceinline__ float2 attraction_sum_masked(const float2* __restrict__ xy, float2 xi,
+                                                        const int64_t* __restrict__ row_ptr,
+                                                        const int32_t* __restrict__ col,
+                                                        int64_t i, float beta,
+                                                        const unsigned char* __restrict__ label,
+                                                        float la) {
+  if (!label || !label[i]) return attraction_sum(xy, xi, row_ptr, col, i, beta);
+  float sx = 0.f, sy = 0.f;
+  for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
+    const int j = __ldg(col + e);
+    const float2 xj = __ldg(xy + j);
+    const float dx = xi.x - xj.x, dy = xi.y - xj.y;
+    const float s = fmaf(dx, dx, fmaf(dy, dy, 1.0f));
+    float c = fmaf(beta, rcp_approx(s), 1.0f);
+    if (label[j]) c *= la;
+    sx = fmaf(c, dx, sx);
+    sy = fmaf(c, dy, sy);
+  }
+  return make_float2(sx, sy);
+}
+
+// Masked repulsion from the unmasked R (already x rho) and the region sum S1 (R23):
+// rho [w0 (S - S1) + w1 S1] = w0 R + rho (w1 - w0) S1.
+__device__ __forceinline__ float2 focus_repulsion(float2 R, int64_t i, int64_t t, float rho,
+                                                  const FocusArgs& fo) {
+  const bool in = fo.label[i] != 0;
+  const float w0 = in ? 1.0f : fo.ls, w1 = in ? fo.lf : 1.0f;
+  const float c = rho * (w1 - w0);
+  const float2 s1 = fo.s1[t];
+  return make_float2(fmaf(c, s1.x, w0 * R.x), fmaf(c, s1.y, w0 * R.y));
 }
 
 // Lagrange basis on K equispaced nodes t_c = (c + 1/2)/K of [0, 1] (R8):

@@ -166,8 +166,9 @@ __global__ void __launch_bounds__(kNodeThreads)
 exact_finish_kernel(const float2* __restrict__ xy, float2* __restrict__ xy_next, int64_t lo,
                     int64_t n_local, int n_chunks, const double2* __restrict__ part,
                     const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
-                    ForceArgs fa, float eta, int iter, int update, float2* __restrict__ rep_out,
-                    float2* __restrict__ att_out, unsigned long long* diverge) {
+                    ForceArgs fa, FocusArgs fo, float eta, int iter, int update,
+                    float2* __restrict__ rep_out, float2* __restrict__ att_out,
+                    unsigned long long* diverge) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n_local) return;
   const int64_t i = lo + t;
@@ -177,9 +178,18 @@ exact_finish_kernel(const float2* __restrict__ xy, float2* __restrict__ xy_next,
     sx += d.x;
     sy += d.y;
   }
-  const float Rx = (float)(fa.rho * sx), Ry = (float)(fa.rho * sy);
+  float Rx = (float)(fa.rho * sx), Ry = (float)(fa.rho * sy);
   const float2 xi = xy[i];
-  const float2 A = attraction_row(xy, xi, row_ptr, col, i, fa.alpha, fa.beta);
+  float2 A;
+  if (fo.label) {  // local refinement mask (R23)
+    const float2 Rm = focus_repulsion(make_float2(Rx, Ry), i, t, fa.rho, fo);
+    Rx = Rm.x;
+    Ry = Rm.y;
+    const float2 as = attraction_sum_masked(xy, xi, row_ptr, col, i, fa.beta, fo.label, fo.la);
+    A = make_float2(-fa.alpha * as.x, -fa.alpha * as.y);
+  } else {
+    A = attraction_row(xy, xi, row_ptr, col, i, fa.alpha, fa.beta);
+  }
   if (update) {
     const float nx = fmaf(eta, Rx + A.x, xi.x);
     const float ny = fmaf(eta, Ry + A.y, xi.y);
@@ -194,13 +204,13 @@ exact_finish_kernel(const float2* __restrict__ xy, float2* __restrict__ xy_next,
 
 void launch_exact_finish(const float2* xy, float2* xy_next, int64_t lo, int64_t n_local,
                          int n_chunks, const double2* part, const int64_t* row_ptr,
-                         const int32_t* col, ForceArgs fa, float eta, int iter, int update,
-                         float2* rep_out, float2* att_out, unsigned long long* diverge,
-                         cudaStream_t s) {
+                         const int32_t* col, ForceArgs fa, FocusArgs fo, float eta, int iter,
+                         int update, float2* rep_out, float2* att_out,
+                         unsigned long long* diverge, cudaStream_t s) {
   if (n_local <= 0) return;
   const unsigned blocks = (unsigned)((n_local + kNodeThreads - 1) / kNodeThreads);
   exact_finish_kernel<<<blocks, kNodeThreads, 0, s>>>(xy, xy_next, lo, n_local, n_chunks, part,
-                                                      row_ptr, col, fa, eta, iter, update,
+                                                      row_ptr, col, fa, fo, eta, iter, update,
                                                       rep_out, att_out, diverge);
 }
 

@@ -266,9 +266,10 @@ __global__ void __launch_bounds__(kNodeThreads)
 gather_update_kernel(const float2* __restrict__ xy, float2* __restrict__ xy_next, int64_t lo,
                      int64_t n_local, const GridGeom* __restrict__ geom,
                      const float* __restrict__ phi, const int64_t* __restrict__ row_ptr,
-                     const int32_t* __restrict__ col, ForceArgs fa, float eta, int iter,
-                     int update, float2* __restrict__ rep_out, float2* __restrict__ att_out,
-                     unsigned long long* diverge, BoxKeys* next_part) {
+                     const int32_t* __restrict__ col, ForceArgs fa, FocusArgs fo, float eta,
+                     int iter, int update, float2* __restrict__ rep_out,
+                     float2* __restrict__ att_out, unsigned long long* diverge,
+                     BoxKeys* next_part) {
   pdl_wait();
   pdl_trigger();
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -298,9 +299,17 @@ gather_update_kernel(const float2* __restrict__ xy, float2* __restrict__ xy_next
     }
     const float xt = p.x - g.cx, yt = p.y - g.cy;
     // F^r = x~ psi_1 - psi_x~  (Eqs. Fr1/Fr2); fused to limit cancellation (R11)
-    const float Rx = fa.rho * fmaf(xt, psi0, -psi1);
-    const float Ry = fa.rho * fmaf(yt, psi0, -psi2);
-    const float2 as = attraction_sum(xy, p, row_ptr, col, i, fa.beta);
+    float Rx = fa.rho * fmaf(xt, psi0, -psi1);
+    float Ry = fa.rho * fmaf(yt, psi0, -psi2);
+    float2 as;
+    if (fo.label) {  // local refinement mask (R23)
+      const float2 Rm = focus_repulsion(make_float2(Rx, Ry), i, t, fa.rho, fo);
+      Rx = Rm.x;
+      Ry = Rm.y;
+      as = attraction_sum_masked(xy, p, row_ptr, col, i, fa.beta, fo.label, fo.la);
+    } else {
+      as = attraction_sum(xy, p, row_ptr, col, i, fa.beta);
+    }
     const float ax = -fa.alpha * as.x, ay = -fa.alpha * as.y;
     if (update) {
       const float nx = fmaf(eta, Rx + ax, p.x);
@@ -323,13 +332,14 @@ gather_update_kernel(const float2* __restrict__ xy, float2* __restrict__ xy_next
 void launch_gather_update(const float2* xy, float2* xy_next, int64_t lo, int64_t n_local,
                           const GridGeom* geom, int k, const float* phi,
                           const int64_t* row_ptr, const int32_t* col, ForceArgs fa,
-                          float eta, int iter, int update, float2* rep_out, float2* att_out,
-                          unsigned long long* diverge, BoxKeys* next_part, cudaStream_t s) {
+                          FocusArgs fo, float eta, int iter, int update, float2* rep_out,
+                          float2* att_out, unsigned long long* diverge, BoxKeys* next_part,
+                          cudaStream_t s) {
   if (n_local <= 0) return;
   const unsigned blocks = (unsigned)((n_local + kNodeThreads - 1) / kNodeThreads);
 #define TFDP_GU(KK)                                                                         \
   launch_chained(gather_update_kernel<KK>, blocks, kNodeThreads, 0, s, xy, xy_next, lo,      \
-                 n_local, geom, phi, row_ptr, col, fa, eta, iter, update, rep_out, att_out,   \
+                 n_local, geom, phi, row_ptr, col, fa, fo, eta, iter, update, rep_out, att_out, \
                  diverge, next_part)
   if (k == 1) TFDP_GU(1);
   else if (k == 2) TFDP_GU(2);

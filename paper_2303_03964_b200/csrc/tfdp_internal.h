@@ -39,6 +39,18 @@ struct ForceArgs {
   int gamma_int;  // 1..8 if gamma is that integer, else 0 (general path)
 };
 
+// Local (fisheye) refinement mask (SPEC RefinementMask): label[i] = 1 for the focal
+// region F u N(F) (internal slot order), s1 = exact repulsion sum over the region's sources
+// for the shard's targets (focus_s1 kernel, unscaled by rho).  Repulsion weight w(i,j) = lf
+// if both in the region, ls if both outside, else 1; attraction weight la if both in the
+// region.  R_i = rho [w0(i) (S_all - S1_i) + w1(i) S1_i] (R23).  label == nullptr:
+// no mask (the unmasked kernels' arithmetic, bit for bit).
+struct FocusArgs {
+  const unsigned char* label;
+  const float2* s1;
+  float la, lf, ls;
+};
+
 // ---- programmatic dependent launch (PDL) for the per-iteration kernel chain -----------
 // Chain kernels are launched with programmatic stream serialization: a kernel may be
 // scheduled while its predecessor's last wave is still running, does its independent
@@ -71,9 +83,9 @@ void launch_exact_partial(const float2* xy, int64_t n, int64_t lo, int64_t n_loc
 // finish: sum partials (fixed chunk order) + CSR attraction + (update | write forces)
 void launch_exact_finish(const float2* xy, float2* xy_next, int64_t lo, int64_t n_local,
                          int n_chunks, const double2* part, const int64_t* row_ptr,
-                         const int32_t* col, ForceArgs fa, float eta, int iter, int update,
-                         float2* rep_out, float2* att_out, unsigned long long* diverge,
-                         cudaStream_t s);
+                         const int32_t* col, ForceArgs fa, FocusArgs fo, float eta, int iter,
+                         int update, float2* rep_out, float2* att_out,
+                         unsigned long long* diverge, cudaStream_t s);
 
 // ibFFT path
 // Box: producers merge one block-reduced BoxKeys per block into kBoxSlots slots (atomic
@@ -126,8 +138,17 @@ void exclusive_scan_ll(const long long* in, long long* out, int64_t n, long long
 void launch_gather_update(const float2* xy, float2* xy_next, int64_t lo, int64_t n_local,
                           const GridGeom* geom, int k, const float* phi,
                           const int64_t* row_ptr, const int32_t* col, ForceArgs fa,
-                          float eta, int iter, int update, float2* rep_out, float2* att_out,
-                          unsigned long long* diverge, BoxKeys* next_part,
+                          FocusArgs fo, float eta, int iter, int update, float2* rep_out,
+                          float2* att_out, unsigned long long* diverge, BoxKeys* next_part,
                           cudaStream_t s);
+
+// local refinement (kernels_focus.cu)
+void launch_mark_focus(const int* focal, int n_focal, const int64_t* row_ptr_caller,
+                       const int32_t* col_caller, unsigned char* label_caller, cudaStream_t s);
+void launch_focus_slots(const unsigned char* label_caller, const int* perm, const int* inv,
+                        int64_t n, const int* region_caller, int m, unsigned char* label_slot,
+                        int* region_slot, cudaStream_t s);
+void launch_focus_s1(const float2* xy, int64_t lo, int64_t n_local, const int* region_slot,
+                     int m, ForceArgs fa, float2* s1, cudaStream_t s);
 
 }  // namespace tfdp

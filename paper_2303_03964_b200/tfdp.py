@@ -198,6 +198,21 @@ class Layout:
         check(lib().tfdp_global_refine(self._ctx, g, r, T), self._ctx)
         self.params = dataclasses.replace(self.params, gamma=g, rho=r, iterations=T, t0=0)
 
+    def set_focus(self, focal, la: float = 1.0, lf: float = 1.0, ls: float = 1.0):
+        """tfdp_set_focus: local-refinement mask on F u N(F); focal=[] clears it."""
+        f = np.ascontiguousarray(np.asarray(focal, dtype=np.int32).ravel())
+        check(lib().tfdp_set_focus(self._ctx, f.ctypes.data if f.size else None, int(f.size),
+                                   float(la), float(lf), float(ls)), self._ctx)
+
+    def local_refine(self, focal, la: float = 1.0, lf: float = 1.0, ls: float = 1.0,
+                     iterations: int | None = None):
+        """Local (fisheye) refinement (tfdp_local_refine)."""
+        f = np.ascontiguousarray(np.asarray(focal, dtype=np.int32).ravel())
+        T = self.params.iterations if iterations is None else int(iterations)
+        check(lib().tfdp_local_refine(self._ctx, f.ctypes.data if f.size else None, int(f.size),
+                                      float(la), float(lf), float(ls), T), self._ctx)
+        self.params = dataclasses.replace(self.params, iterations=T, t0=0)
+
     def np1(self, hits=None):
         """NP1 of the current layout on the device (tfdp_np1, P:599-606).  Returns the float;
         with hits (int32 array / tensor of hi - lo entries) also fills the per-node counts."""
