@@ -311,6 +311,21 @@ def run_np1(r, reps=5):
             "nodes_per_s": r["n"] / (ms / 1e3), "timing": "host wall clock around the synchronous call, median of 5"}
 
 
+def run_pmds(r, n_pivots=50):
+    """NEXT-2: device PivotMDS of the bench graph (tfdp_pivot_mds), untimed by the contract;
+    a fresh context so the bench layout is untouched."""
+    import paper_2303_03964_b200 as P
+
+    w = r["w"]
+    with P.Layout(w.n, r["rp"], r["col"], w.xy, P.Params(solver="ibfft", k=1)) as L:
+        L.pivot_mds(n_pivots, 0)  # warm-up
+        t0 = time.perf_counter()
+        L.pivot_mds(n_pivots, 0)  # synchronous
+        ms = 1e3 * (time.perf_counter() - t0)
+    return {"workload": "C4 graph", "pivots": n_pivots, "ms": round(ms, 2),
+            "timing": "host wall clock around the synchronous call"}
+
+
 def run_exact(args, rank, world, local):
     import torch
 
@@ -469,6 +484,7 @@ def main():
     torch.cuda.set_device(local)
     r = run_fft(args, rank, world, local)
     npm = run_np1(r)
+    pm = run_pmds(r) if rank == 0 else None
     exact = None if args.no_exact else run_exact(args, rank, world, local)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -491,7 +507,7 @@ def main():
             },
             "e2e": r["e2e"], "gpu_launches": r["launches"], "clocks": r["clocks"],
             "roofline": r["roofline"], "cpu_baseline": cpu, "kernels": r["kernels"],
-            "exact": exact, "np1": npm,
+            "exact": exact, "np1": npm, "pmds": pm,
         }
         print(json.dumps(line), flush=True)
     r["L"].close()

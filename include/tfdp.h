@@ -169,6 +169,20 @@ tfdp_status tfdp_set_params(tfdp_ctx* ctx, const tfdp_params* p);
  * errors of tfdp_step. */
 tfdp_status tfdp_global_refine(tfdp_ctx* ctx, double gamma, double rho, int32_t iterations);
 
+/* PivotMDS initialisation ("we use the same PMDS layout as initialization"; SPEC
+ * init_pivot_mds S:110-118; Brandes & Pich 2006), computed on the device; replaces the
+ * context's layout (the paper's evaluation protocol: PMDS, then t-FDP).
+ *   p = min(n_pivots, n) pivots by max-min farthest-point BFS selection, the first one
+ *   splitmix64(seed) mod n, ties by the lowest node id; hop distances D (n x p; unreachable
+ *   = that pivot's eccentricity + 1, R24); C = double-centred -D^2/2; the top-2
+ *   eigenvectors v_1, v_2 of C^T C (power iteration, fp64; sign: largest-|.| component
+ *   positive); positions C v_k, centred, scaled to mean edge length 1 (rank < 2: the
+ *   second axis is 0).
+ *   pivots  host int32[min(n_pivots, n)] (may be NULL): the chosen pivots (caller ids)
+ * TFDP_ERR_ARG unless 1 <= n_pivots <= 64.  Syncs once per pivot.  Scratch (~4 p + 60 B per
+ * node) is allocated for the call and freed. */
+tfdp_status tfdp_pivot_mds(tfdp_ctx* ctx, int32_t n_pivots, uint64_t seed, int32_t* pivots);
+
 /* Local (fisheye) refinement mask (SPEC RefinementMask S:155-158).  The region
  * F u N(F) = the focal nodes and their graph neighbours.  Forces with the mask:
  *   repulsion pair weight  lf if both ends are in the region, ls if both are outside, else 1

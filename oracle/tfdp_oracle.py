@@ -28,7 +28,7 @@ __all__ = [
     "equilibrium_distance", "global_refine", "np1_hits", "np1_from_hits",
     "Focus", "focus_region", "repulsion_masked_exact", "repulsion_masked_loops",
     "attraction_masked", "repulsion_masked_ibfft", "forces_masked", "energy_masked",
-    "local_refine",
+    "local_refine", "splitmix64", "bfs_hops", "pmds_pivots", "pivot_mds",
 ]
 
 
@@ -600,6 +600,90 @@ def local_refine(X, row_ptr, col, fo: Focus, p: Params = Params(), T: int = 300,
         if bad.any():
             raise FloatingPointError(f"diverged at iter {t} node {int(np.argmax(bad))}")
     return X
+
+
+# ---------------------------------------------------------------------------------------
+# PivotMDS initialisation (SPEC init_pivot_mds S:110-118; Brandes & Pich 2006)
+# ---------------------------------------------------------------------------------------
+def splitmix64(x: int) -> int:
+    """SplitMix64 output for counter x (the counter-based generator both sides implement)."""
+    m = (1 << 64) - 1
+    z = (x + 0x9E3779B97F4A7C15) & m
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & m
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & m
+    return z ^ (z >> 31)
+
+
+def bfs_hops(row_ptr, col, src: int):
+    """Hop distances from src (-1 = unreachable), plain queue BFS."""
+    from collections import deque
+
+    n = len(row_ptr) - 1
+    d = np.full(n, -1, dtype=np.int64)
+    d[src] = 0
+    q = deque([src])
+    while q:
+        u = q.popleft()
+        for v in col[row_ptr[u]:row_ptr[u + 1]]:
+            if d[v] < 0:
+                d[v] = d[u] + 1
+                q.append(int(v))
+    return d
+
+
+def pmds_pivots(row_ptr, col, n_pivots: int, seed: int):
+    """Max-min farthest-point pivots: the first is splitmix64(seed) mod n, each next
+    one maximises the hop distance to the chosen set (ties: lowest index).  Returns
+    (pivots, D) with D[:, j] the hop distances from pivot j; unreachable nodes get the
+    pivot's eccentricity + 1 (reading R24)."""
+    n = len(row_ptr) - 1
+    p = min(int(n_pivots), n)
+    D = np.zeros((n, p), dtype=np.int64)
+    mind = np.full(n, np.iinfo(np.int64).max)
+    piv = splitmix64(int(seed)) % n
+    pivots = []
+    for j in range(p):
+        pivots.append(int(piv))
+        d = bfs_hops(row_ptr, col, piv)
+        d[d < 0] = d.max() + 1
+        D[:, j] = d
+        mind = np.minimum(mind, d)
+        piv = int(np.argmax(mind))  # first index of the maximum
+    return np.array(pivots, dtype=np.int64), D
+
+
+def pivot_mds(row_ptr, col, n_pivots: int = 50, seed: int = 0):
+    """PivotMDS layout: squared hop distances to the pivots, double-centred
+    C = -1/2 (D2 - row means - column means + grand mean) (n x p), the top-2 eigenvectors
+    v_1, v_2 of C^T C (library eigh; the right singular vectors of C), positions C v_k,
+    centred and scaled to mean edge length 1.  Eigenvector signs: the largest-|.| component
+    positive (lowest index on ties).  Returns (X, pivots)."""
+    if n_pivots < 1:
+        raise ValueError("pivot_count >= 1 (S:117)")
+    row_ptr = np.asarray(row_ptr, dtype=np.int64)
+    col = np.asarray(col, dtype=np.int64)
+    n = len(row_ptr) - 1
+    pivots, D = pmds_pivots(row_ptr, col, n_pivots, seed)
+    D2 = D.astype(np.float64) ** 2
+    C = -0.5 * (D2 - D2.mean(1, keepdims=True) - D2.mean(0, keepdims=True) + D2.mean())
+    w, V = np.linalg.eigh(C.T @ C)
+    order = np.argsort(-w, kind="stable")
+    X = np.zeros((n, 2))
+    for a in range(min(2, V.shape[1])):
+        v = V[:, order[a]]
+        if w[order[a]] <= 1e-12 * max(w[order[0]], 1e-300):
+            continue  # rank < 2: that axis stays 0 (reading R24)
+        m = np.abs(v)
+        if v[int(np.argmax(m))] < 0:
+            v = -v
+        X[:, a] = C @ v
+    X -= X.mean(0)
+    if row_ptr[-1] > 0:
+        rows = np.repeat(np.arange(n), np.diff(row_ptr))
+        L = np.linalg.norm(X[rows] - X[col], axis=1).mean()
+        if L > 0:
+            X /= L
+    return X, pivots
 
 
 # ---------------------------------------------------------------------------------------

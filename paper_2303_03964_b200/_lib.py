@@ -53,6 +53,7 @@ _SIGS = {
     "tfdp_set_params": (C.c_int, [_P, C.POINTER(tfdp_params)]),
     "tfdp_global_refine": (C.c_int, [_P, C.c_double, C.c_double, C.c_int32]),
     "tfdp_np1": (C.c_int, [_P, C.POINTER(C.c_double), _P]),
+    "tfdp_pivot_mds": (C.c_int, [_P, C.c_int32, C.c_uint64, _P]),
     "tfdp_set_focus": (C.c_int, [_P, _P, C.c_int64, C.c_double, C.c_double, C.c_double]),
     "tfdp_local_refine": (C.c_int, [_P, _P, C.c_int64, C.c_double, C.c_double, C.c_double,
                                     C.c_int32]),

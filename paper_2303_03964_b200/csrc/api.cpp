@@ -1192,6 +1192,42 @@ tfdp_status tfdp_local_refine(tfdp_ctx* c, const int32_t* focal, int64_t n_focal
   return tfdp_step(c, iterations);
 }
 
+tfdp_status tfdp_pivot_mds(tfdp_ctx* c, int32_t n_pivots, uint64_t seed, int32_t* pivots) {
+  if (!c) return fail(nullptr, TFDP_ERR_ARG, "ctx is NULL");
+  if (c->errored) return fail(c, TFDP_ERR_STATE, "context is errored: %s", c->err.c_str());
+  if (n_pivots < 1 || n_pivots > tfdp::pmds_max_pivots())
+    return fail(c, TFDP_ERR_ARG, "pivot count must be in 1..%d (S:117)", tfdp::pmds_max_pivots());
+  cudaSetDevice(c->device);
+  const int p = (int)std::min<int64_t>(n_pivots, c->n);
+  // splitmix64(seed): the first pivot (the counter-based generator the oracle implements too)
+  uint64_t z = seed + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  void* scratch = nullptr;
+  CUDA_TRY(c, cudaMalloc(&scratch, tfdp::pmds_scratch_bytes(c->n, p)));
+  std::vector<int> piv(p);
+  const int64_t* rp = c->reorder ? c->row_ptr_o : c->row_ptr;  // caller order
+  const int32_t* cl = c->reorder ? c->col_o : c->col;
+  float2* out = c->reorder ? c->iobuf : c->xy[c->cur];
+  const char* stage = "";
+  const cudaError_t e = tfdp::launch_pmds(rp, cl, c->n, c->nnz, p, z, scratch, out, piv.data(),
+                                          &c->launches, &stage, c->stream);
+  if (e == cudaSuccess && c->reorder) {  // caller order -> internal order
+    tfdp::launch_permute(c->iobuf, c->perm, c->n, c->xy[c->cur], c->stream);
+    c->launches++;
+  }
+  const cudaError_t e2 = cudaStreamSynchronize(c->stream);
+  cudaFree(scratch);
+  if (e != cudaSuccess || e2 != cudaSuccess)
+    return fail(c, TFDP_ERR_CUDA, "pivot_mds (%s): %s", stage,
+                cudaGetErrorString(e != cudaSuccess ? e : e2));
+  c->box_valid = false;
+  if (pivots)
+    for (int j = 0; j < p; ++j) pivots[j] = piv[j];
+  return TFDP_OK;
+}
+
 tfdp_status tfdp_global_refine(tfdp_ctx* c, double gamma, double rho, int32_t iterations) {
   if (!c) return fail(nullptr, TFDP_ERR_ARG, "ctx is NULL");
   if (!std::isfinite(gamma) || gamma <= 1.0)

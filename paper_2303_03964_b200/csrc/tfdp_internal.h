@@ -142,6 +142,15 @@ void launch_gather_update(const float2* xy, float2* xy_next, int64_t lo, int64_t
                           float2* att_out, unsigned long long* diverge, BoxKeys* next_part,
                           cudaStream_t s);
 
+// PivotMDS initialisation (kernels_pmds.cu): caller-order CSR, p <= pmds_max_pivots();
+// xy (device, n) receives the layout, pivots_out (host, p) the pivots.
+int pmds_max_pivots();
+size_t pmds_scratch_bytes(int64_t n, int p);
+cudaError_t launch_pmds(const int64_t* rp, const int32_t* col, int64_t n, int64_t nnz, int p,
+                        unsigned long long seed_pivot, void* scratch, float2* xy,
+                        int* pivots_out, int64_t* launches, const char** stage,
+                        cudaStream_t s);
+
 // local refinement (kernels_focus.cu)
 void launch_mark_focus(const int* focal, int n_focal, const int64_t* row_ptr_caller,
                        const int32_t* col_caller, unsigned char* label_caller, cudaStream_t s);

@@ -198,6 +198,15 @@ class Layout:
         check(lib().tfdp_global_refine(self._ctx, g, r, T), self._ctx)
         self.params = dataclasses.replace(self.params, gamma=g, rho=r, iterations=T, t0=0)
 
+    def pivot_mds(self, n_pivots: int = 50, seed: int = 0):
+        """tfdp_pivot_mds: replace the layout by the PivotMDS initialisation.
+        Returns the pivots (caller ids)."""
+        p = min(int(n_pivots), self.n)
+        piv = np.empty(max(p, 1), np.int32)
+        check(lib().tfdp_pivot_mds(self._ctx, int(n_pivots), int(seed) & ((1 << 64) - 1),
+                                   piv.ctypes.data), self._ctx)
+        return piv[:p]
+
     def set_focus(self, focal, la: float = 1.0, lf: float = 1.0, ls: float = 1.0):
         """tfdp_set_focus: local-refinement mask on F u N(F); focal=[] clears it."""
         f = np.ascontiguousarray(np.asarray(focal, dtype=np.int32).ravel())
