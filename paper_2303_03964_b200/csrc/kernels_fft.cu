@@ -14,13 +14,19 @@
 
 namespace tfdp {
 
+namespace {
+thread_local bool g_pdl_active = true;
+}
+
 bool pdl_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("TFDP_PDL");
     return !(e && e[0] == '0');
   }();
-  return on;
+  return on && g_pdl_active;
 }
+
+void set_pdl_active(bool on) { g_pdl_active = on; }
 
 // ------------------------------------------------------------------ bbox
 // Two-level exact min/max: every block reduces its keys (warp __reduce + smem) and merges

@@ -3,21 +3,34 @@
 // Replaces a zero-padded P x P 2-D R2C -> x K^ -> C2R by five passes that never transform
 // the zero padding and never store outputs that are discarded:
 //   kspec_rows  K rows dy = 0..M-1 generated on the fly (K is even in x and y, so each row
-//               spectrum is real), two rows per complex FFT: KA[q][dy], q = 0..P/2
-//   kspec_cols  two K^ columns per packed real-even FFT: KH[q][u] (real), u = 0..P-1
-//   rows_fwd    two charge rows (a + i b) per complex FFT, untangled into the half
-//               spectra of rows a and b: CA[c][q][row]; the consumed rows are re-zeroed
-//   cols        one (channel, column) per block: FFT -> x K^ -> inverse FFT, rows 0..M-1 kept
-//   rows_inv    Hermitian rows, two rows per complex inverse FFT, columns 0..M-1 kept
+//               spectrum is real), four rows per block: KA[q][dy], q = 0..P/2
+//   kspec_cols  four K^ columns per block (real-even): KH[q][u] (real), u = 0..P-1
+//   rows_fwd    four charge rows per block, two per complex FFT (a + i b), untangled into
+//               the half spectra CA[c][q][row] (32 contiguous bytes per q); consumed rows
+//               are re-zeroed
+//   cols        two (channel, column) items per block: FFT -> x K^ -> inverse FFT, rows
+//               0..M-1 kept
+//   rows_inv    four Hermitian rows per block, two per complex inverse FFT, columns 0..M-1
 // The inputs of every forward FFT are zero beyond P/2 (M <= P/2), so the first stage skips
 // those loads; every inverse FFT keeps only outputs below P/2, so its last stage stores half.
-// FFTs are in-place Stockham stages (radix 16, then 16/8/4/2, then 3, 5) in shared memory,
-// fully specialised at compile time for each supported P (P % 256 == 0, 2^a 3^b 5^c): every
-// index, stride and loop bound is a constant.  One float2 of padding per 16 makes the
-// strided stores conflict-free.  Twiddles come from a two-level fp64-generated table in
-// shared memory and short product chains.  1/P^2 is folded into the kernel samples.
+//
+// Every block runs TWO independent complex FFTs (lanes A, B) in SoA form: shared element e
+// is the float4 {re_A, re_B, im_A, im_B} and a thread holds each value as two fp32x2 packs
+// (re pair, im pair).  Then one LDS.128 / STS.128 moves a value of both FFTs; a complex add
+// is 2 FADD2 for both lanes; a product with a twiddle (shared by the lanes: same position)
+// is 4 instructions for both lanes with scalar-broadcast FMUL2/FFMA2 operands; a product
+// by -i is a register renaming whose sign folds into the next FADD2; the twiddle chains are
+// computed once for both FFTs.
+//
+// FFTs are in-place Stockham autosort stages (radix 16, then 16/8/4/2, then 3, 5) in shared
+// memory, fully specialised at compile time for each supported P (P % 256 == 0,
+// 2^a 3^b 5^c): every index, stride and loop bound is a constant.  One element of padding
+// per 16 makes the strided stores conflict-free.  Twiddles come from a two-level
+// fp64-generated table in shared memory and short product chains.  1/P^2 is folded into the
+// kernel samples.
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include "device_math.cuh"
 #include "tfdp_internal.h"
@@ -26,13 +39,499 @@ namespace tfdp {
 
 namespace {
 
-
-// Complex arithmetic on packed fp32x2 (sm_100a FADD2 / FMUL2 / FFMA2): a complex add is one
-// instruction, a complex product two.
+// ---------------------------------------------------------------- scalar complex (twiddles)
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
   return __ffma2_rn(make_float2(a.y, a.y), make_float2(-b.y, b.x),
                     __fmul2_rn(make_float2(a.x, a.x), b));
 }
+
+// ---------------------------------------------------------------- SoA pair arithmetic
+struct C2 {
+  float2 re, im;  // (lane A, lane B)
+};
+
+__device__ __forceinline__ float2 bc(float s) { return make_float2(s, s); }
+__device__ __forceinline__ float2 neg2(float2 a) { return make_float2(-a.x, -a.y); }
+__device__ __forceinline__ C2 add(C2 a, C2 b) {
+  return {__fadd2_rn(a.re, b.re), __fadd2_rn(a.im, b.im)};
+}
+__device__ __forceinline__ C2 sub(C2 a, C2 b) {
+  return {__fadd2_rn(a.re, neg2(b.re)), __fadd2_rn(a.im, neg2(b.im))};
+}
+__device__ __forceinline__ C2 mul_mi(C2 a) { return {a.im, neg2(a.re)}; }  // * (-i)
+// a * (c + i s) for both lanes
+__device__ __forceinline__ C2 mulw(C2 a, float c, float s) {
+  return {__ffma2_rn(a.im, bc(-s), __fmul2_rn(a.re, bc(c))),
+          __ffma2_rn(a.im, bc(c), __fmul2_rn(a.re, bc(s)))};
+}
+__device__ __forceinline__ C2 zero2() { return {make_float2(0.f, 0.f), make_float2(0.f, 0.f)}; }
+__device__ __forceinline__ C2 ld(const float4* p) {
+  const float4 q = *p;
+  return {make_float2(q.x, q.y), make_float2(q.z, q.w)};
+}
+__device__ __forceinline__ void st(float4* p, C2 v) { *p = make_float4(v.re.x, v.re.y, v.im.x, v.im.y); }
+
+template <int R>
+__device__ __forceinline__ void dft(C2 (&v)[R]);
+
+template <>
+__device__ __forceinline__ void dft<2>(C2 (&v)[2]) {
+  const C2 a = v[0], b = v[1];
+  v[0] = add(a, b);
+  v[1] = sub(a, b);
+}
+
+template <>
+__device__ __forceinline__ void dft<3>(C2 (&v)[3]) {
+  // w = exp(-2 pi i / 3) = (-1/2, -sqrt3/2)
+  const float sn = -0.86602540378443865f;
+  const C2 s12 = add(v[1], v[2]), d12 = sub(v[1], v[2]);
+  const C2 m = {__ffma2_rn(s12.re, bc(-0.5f), v[0].re), __ffma2_rn(s12.im, bc(-0.5f), v[0].im)};
+  const C2 t = {__fmul2_rn(d12.im, bc(-sn)), __fmul2_rn(d12.re, bc(sn))};  // i * sn * d12
+  v[0] = add(v[0], s12);
+  v[1] = add(m, t);
+  v[2] = sub(m, t);
+}
+
+template <>
+__device__ __forceinline__ void dft<5>(C2 (&v)[5]) {
+  const float c1 = 0.30901699437494742f, c2 = -0.80901699437494742f;
+  const float s1 = -0.95105651629515357f, s2 = -0.58778525229247313f;
+  const C2 a1 = add(v[1], v[4]), b1 = sub(v[1], v[4]);
+  const C2 a2 = add(v[2], v[3]), b2 = sub(v[2], v[3]);
+  const C2 x0 = v[0];
+  const C2 m1 = {__ffma2_rn(a2.re, bc(c2), __ffma2_rn(a1.re, bc(c1), x0.re)),
+                 __ffma2_rn(a2.im, bc(c2), __ffma2_rn(a1.im, bc(c1), x0.im))};
+  const C2 m2 = {__ffma2_rn(a2.re, bc(c1), __ffma2_rn(a1.re, bc(c2), x0.re)),
+                 __ffma2_rn(a2.im, bc(c1), __ffma2_rn(a1.im, bc(c2), x0.im))};
+  // n1 = i (s1 b1 + s2 b2), n2 = i (s2 b1 - s1 b2)
+  const float2 u1r = __ffma2_rn(b2.re, bc(s2), __fmul2_rn(b1.re, bc(s1)));
+  const float2 u1i = __ffma2_rn(b2.im, bc(s2), __fmul2_rn(b1.im, bc(s1)));
+  const float2 u2r = __ffma2_rn(b2.re, bc(-s1), __fmul2_rn(b1.re, bc(s2)));
+  const float2 u2i = __ffma2_rn(b2.im, bc(-s1), __fmul2_rn(b1.im, bc(s2)));
+  const C2 n1 = {neg2(u1i), u1r}, n2 = {neg2(u2i), u2r};
+  v[0] = add(x0, add(a1, a2));
+  v[1] = add(m1, n1);
+  v[4] = sub(m1, n1);
+  v[2] = add(m2, n2);
+  v[3] = sub(m2, n2);
+}
+
+template <>
+__device__ __forceinline__ void dft<4>(C2 (&v)[4]) {
+  const C2 s02 = add(v[0], v[2]), d02 = sub(v[0], v[2]);
+  const C2 s13 = add(v[1], v[3]), d13 = mul_mi(sub(v[1], v[3]));
+  v[0] = add(s02, s13);
+  v[2] = sub(s02, s13);
+  v[1] = add(d02, d13);
+  v[3] = sub(d02, d13);
+}
+
+// o * W8 = o (h - i h) = (h (re + im), h (im - re));  o * W8^3 = o (-h - i h) =
+// (h (im - re), -h (re + im))
+__device__ __forceinline__ C2 mul_w8(C2 o, float h) {
+  return {__fmul2_rn(__fadd2_rn(o.re, o.im), bc(h)), __fmul2_rn(__fadd2_rn(o.im, neg2(o.re)), bc(h))};
+}
+__device__ __forceinline__ C2 mul_w8_3(C2 o, float h) {
+  return {__fmul2_rn(__fadd2_rn(o.im, neg2(o.re)), bc(h)), __fmul2_rn(__fadd2_rn(o.re, o.im), bc(-h))};
+}
+
+template <>
+__device__ __forceinline__ void dft<8>(C2 (&v)[8]) {
+  C2 e[4] = {v[0], v[2], v[4], v[6]};
+  C2 o[4] = {v[1], v[3], v[5], v[7]};
+  dft<4>(e);
+  dft<4>(o);
+  const float h = 0.70710678118654752f;
+  const C2 o1 = mul_w8(o[1], h);
+  const C2 o2 = mul_mi(o[2]);
+  const C2 o3 = mul_w8_3(o[3], h);
+  v[0] = add(e[0], o[0]);
+  v[4] = sub(e[0], o[0]);
+  v[1] = add(e[1], o1);
+  v[5] = sub(e[1], o1);
+  v[2] = add(e[2], o2);
+  v[6] = sub(e[2], o2);
+  v[3] = add(e[3], o3);
+  v[7] = sub(e[3], o3);
+}
+
+// DFT-16 as 4 x 4 (Cooley-Tukey, r = 4 r1 + r2, s = s1 + 4 s2): DFT-4 over r1, twiddle
+// W16^(r2 s1), DFT-4 over r2; outputs written back in natural order.
+// ZU: inputs v[8..15] are zero (first stage of a zero-padded forward FFT): the first-level
+// DFT-4s of (a, b, 0, 0) reduce to (a + b, a - i b, a - b, a + i b).
+template <bool ZU = false>
+__device__ __forceinline__ void dft16(C2 (&v)[16]) {
+  C2 y[4][4];  // y[r2][s1]
+#pragma unroll
+  for (int r2 = 0; r2 < 4; ++r2) {
+    if constexpr (ZU) {
+      const C2 a = v[r2], b = v[r2 + 4], ib = mul_mi(b);  // -i b
+      y[r2][0] = add(a, b);
+      y[r2][1] = add(a, ib);
+      y[r2][2] = sub(a, b);
+      y[r2][3] = sub(a, ib);
+    } else {
+      C2 t[4] = {v[r2], v[r2 + 4], v[r2 + 8], v[r2 + 12]};
+      dft<4>(t);
+#pragma unroll
+      for (int s1 = 0; s1 < 4; ++s1) y[r2][s1] = t[s1];
+    }
+  }
+  const float h = 0.70710678118654752f;
+  const float c1 = 0.92387953251128674f, s1_ = 0.38268343236508978f;  // cos, sin(pi/8)
+  // W16^e = exp(-2 pi i e / 16) for the products e = r2 * s1
+  y[1][1] = mulw(y[1][1], c1, -s1_);  // W1
+  y[1][2] = mul_w8(y[1][2], h);       // W2
+  y[1][3] = mulw(y[1][3], s1_, -c1);  // W3
+  y[2][1] = mul_w8(y[2][1], h);       // W2
+  y[2][2] = mul_mi(y[2][2]);          // W4 = -i
+  y[2][3] = mul_w8_3(y[2][3], h);     // W6
+  y[3][1] = mulw(y[3][1], s1_, -c1);  // W3
+  y[3][2] = mul_w8_3(y[3][2], h);     // W6
+  y[3][3] = mulw(y[3][3], -c1, s1_);  // W9
+#pragma unroll
+  for (int s1 = 0; s1 < 4; ++s1) {
+    C2 t[4] = {y[0][s1], y[1][s1], y[2][s1], y[3][s1]};
+    dft<4>(t);
+#pragma unroll
+    for (int s2 = 0; s2 < 4; ++s2) v[s1 + 4 * s2] = t[s2];
+  }
+}
+
+template <>
+__device__ __forceinline__ void dft<16>(C2 (&v)[16]) {
+  dft16<false>(v);
+}
+
+// Shared-memory layout: one element of padding per 16 (pad(i) = i + i/16): the strided
+// Stockham stores of the first stages become conflict-free and, since every stride is a
+// multiple of 16 (P % 256 == 0), address(r) = base + r * padded_stride.
+__device__ __forceinline__ int pad(int i) { return i + (i >> 4); }
+__host__ __device__ constexpr int padded_len(int N) { return N + (N >> 4) + 1; }
+
+// Two-level twiddle table: tw[0..64) = exp(-2 pi i t / N), tw[64 + u] = exp(-2 pi i 64u / N),
+// exp(-2 pi i t / N) = tw[64 + t/64] * tw[t % 64].
+__host__ __device__ constexpr int tw_len(int N) { return 64 + N / 64 + 1; }
+__device__ __forceinline__ float2 tw_at(const float2* __restrict__ tw, int t) {
+  return cmul(tw[64 + (t >> 6)], tw[t & 63]);
+}
+
+// w^r for r = 1..R-1 from one table lookup and a product chain of depth <= 3.
+template <int R>
+__device__ __forceinline__ void twiddles(const float2* __restrict__ tw, int base, float2 (&w)[R]) {
+  w[1] = tw_at(tw, base);
+  if constexpr (R >= 3) w[2] = cmul(w[1], w[1]);
+  if constexpr (R >= 4) w[3] = cmul(w[2], w[1]);
+  if constexpr (R >= 5) w[4] = cmul(w[2], w[2]);
+  if constexpr (R >= 8) {
+    w[5] = cmul(w[4], w[1]);
+    w[6] = cmul(w[4], w[2]);
+    w[7] = cmul(w[4], w[3]);
+  }
+  if constexpr (R == 16) {  // second lookup keeps the product chains at depth <= 3
+    w[8] = tw_at(tw, 8 * base);
+#pragma unroll
+    for (int r = 1; r < 8; ++r) w[8 + r] = cmul(w[8], w[r]);
+  }
+}
+
+// Threads per FFT-pair block: the smallest of {128, 256, 384, 512} >= P/16 (one radix-16
+// butterfly of both FFTs per thread).
+__host__ __device__ constexpr int fft_threads_c(int P) {
+  return P <= 2048 ? 128 : P <= 4096 ? 256 : P <= 6144 ? 384 : 512;
+}
+
+// Blocks per SM the register cap aims for.
+template <int T>
+constexpr int kMinBlocks = T == 128 ? 5 : T == 256 ? 3 : T == 384 ? 2 : 1;
+
+// FFT flags: inputs zero at index >= N/2 (first stage skips them); only outputs < N/2 needed
+// (last stage stores half).
+enum { kZeroUpper = 1, kLowOut = 2 };
+
+// In-place Stockham autosort stage (Govindaraju et al. 2008 formulation): radix R, size N,
+// sub-transform size Ns (1 for the first stage, else a multiple of 16 since N % 256 == 0 and
+// the first stage is radix 16).  Loads + butterflies into registers, barrier, stores, barrier.
+// The last stage (Ns R = N) reads and writes the same elements per butterfly, so it needs no
+// barrier between its loads and stores and streams one butterfly at a time.
+// I/O fusion: the first stage takes its inputs from src(e) (element e in natural order) and
+// the last stage hands its outputs to dst(e, v) unless they are SmemIO — so a kernel reads its
+// global inputs straight into the first butterflies and writes its global outputs straight
+// from the last ones, without a shared-memory round trip for either.
+struct SmemIO {};
+
+template <int T, int R, int N, int Ns, bool ZERO_UPPER, bool LOW_OUT, class Src, class Dst>
+__device__ __forceinline__ void stage(float4* buf, const float2* __restrict__ tw, int tid,
+                                      const Src& src, const Dst& dst) {
+  constexpr int nb = N / R;
+  constexpr int MB = (nb + T - 1) / T;  // butterflies per thread
+  constexpr int step = nb / Ns;         // N / (Ns R)
+  constexpr int sin_ = nb + (nb >> 4);  // padded stride of the loads (nb % 16 == 0)
+  constexpr int sout = Ns == 1 ? 1 : Ns + (Ns >> 4);
+  constexpr bool p2 = (Ns & (Ns - 1)) == 0;
+  constexpr bool first = Ns == 1;
+  constexpr bool last = Ns * R == N;
+  constexpr bool src_smem = !first || std::is_same<Src, SmemIO>::value;
+  constexpr bool dst_smem = !last || std::is_same<Dst, SmemIO>::value;
+  auto butterfly = [&](int j, C2 (&v)[R]) {
+    const int pj = j + (j >> 4);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (ZERO_UPPER && 2 * r >= R) v[r] = zero2();
+      else if constexpr (src_smem) v[r] = ld(buf + pj + r * sin_);
+      else v[r] = src(j + r * nb);
+    }
+    if constexpr (Ns > 1) {
+      const int k = p2 ? (j & (Ns - 1)) : (j % Ns);
+      float2 w[R];
+      twiddles<R>(tw, k * step, w);
+#pragma unroll
+      for (int r = 1; r < R; ++r) v[r] = mulw(v[r], w[r].x, w[r].y);
+    }
+    if constexpr (ZERO_UPPER && R == 16) dft16<true>(v);
+    else dft<R>(v);
+  };
+  if constexpr (last && Ns > 1) {
+    // d = j: in place per butterfly
+#pragma unroll 1
+    for (int b = 0; b < MB; ++b) {
+      const int j = tid + b * T;
+      if (nb % T == 0 || j < nb) {
+        C2 v[R];
+        butterfly(j, v);
+        const int pd = j + (j >> 4);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          if (!LOW_OUT || 2 * r < R) {
+            if constexpr (dst_smem) st(buf + pd + r * sout, v[r]);
+            else dst(j + r * Ns, v[r]);
+          }
+        }
+      }
+    }
+    if constexpr (dst_smem) __syncthreads();
+  } else {
+    C2 v[MB][R];
+#pragma unroll
+    for (int b = 0; b < MB; ++b) {
+      const int j = tid + b * T;
+      if (nb % T == 0 || j < nb) butterfly(j, v[b]);
+    }
+    if constexpr (src_smem) __syncthreads();
+#pragma unroll
+    for (int b = 0; b < MB; ++b) {
+      const int j = tid + b * T;
+      if (nb % T == 0 || j < nb) {
+        const int k = Ns == 1 ? 0 : (p2 ? (j & (Ns - 1)) : (j % Ns));
+        const int d = (j - k) * R + k;
+        const int pd = d + (d >> 4);
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          if (!LOW_OUT || 2 * r < R) st(buf + pd + r * sout, v[b][r]);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+__host__ __device__ constexpr int next_radix(int rem) {
+  return rem % 16 == 0 ? 16 : rem % 8 == 0 ? 8 : rem % 4 == 0 ? 4 : rem % 2 == 0 ? 2
+       : rem % 3 == 0 ? 3 : 5;
+}
+
+template <int T, int N, int FLAGS, int Ns, int REM, class Src, class Dst>
+__device__ __forceinline__ void fft_rec(float4* buf, const float2* __restrict__ tw, int tid,
+                                        const Src& src, const Dst& dst) {
+  if constexpr (REM > 1) {
+    constexpr int R = next_radix(REM);
+    constexpr bool first = Ns == 1, last = REM == R;
+    stage<T, R, N, Ns, first && (FLAGS & kZeroUpper) != 0,
+          last && (FLAGS & kLowOut) != 0 && R % 2 == 0>(buf, tw, tid, src, dst);
+    fft_rec<T, N, FLAGS, Ns * R, REM / R>(buf, tw, tid, src, dst);
+  }
+}
+
+// Forward complex FFTs (both lanes) of N elements, N = 2^a 3^b 5^c, N % 256 == 0, in the
+// padded shared buffer (in place) — inputs from src / outputs to dst when those are not
+// SmemIO.  Radix 16 first (so Ns is a multiple of 16 afterwards), then 16/8/4/2, then 3, 5.
+// Called by the whole block (T >= N/16 threads); a shared-memory source must be complete
+// (barrier) before the call; ends with a barrier unless the outputs go to dst.
+template <int T, int N, int FLAGS, class Src = SmemIO, class Dst = SmemIO>
+__device__ __forceinline__ void fft_smem(float4* buf, const float2* __restrict__ tw,
+                                         const Src& src = Src{}, const Dst& dst = Dst{}) {
+  static_assert(N % 256 == 0 && T * 16 >= N, "FFT plan");
+  fft_rec<T, N, FLAGS, 1, N>(buf, tw, threadIdx.x, src, dst);
+}
+
+__global__ void twiddle_kernel(float2* tw, int N) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= tw_len(N)) return;
+  const int t = i < 64 ? i : 64 * (i - 64);
+  double s, c;
+  sincospi(2.0 * (double)t / (double)N, &s, &c);
+  tw[i] = make_float2((float)c, (float)-s);
+}
+
+__device__ __forceinline__ void load_tw(float2* dst, const float2* __restrict__ src, int N) {
+  for (int i = threadIdx.x; i < tw_len(N); i += blockDim.x) dst[i] = src[i];
+}
+
+// t-kernel sample (1 + d^2)^-gamma with the integer-gamma fast paths (uniform branch).
+__device__ __forceinline__ float ksample(float s, float neg_gamma, int gi) {
+  switch (gi) {
+    case 1: return pow_neg<1>(s, neg_gamma);
+    case 2: return pow_neg<2>(s, neg_gamma);
+    case 3: return pow_neg<3>(s, neg_gamma);
+    case 4: return pow_neg<4>(s, neg_gamma);
+    case 8: return pow_neg<8>(s, neg_gamma);
+    default: return pow_neg<0>(s, neg_gamma);
+  }
+}
+
+#define TFDP_FFT_KERNEL(name) \
+  template <int P>            \
+  __global__ void __launch_bounds__(fft_threads_c(P), kMinBlocks<fft_threads_c(P)>) name
+
+// Common prologue: smem = [padded_len(P)] float4 + the twiddle table.
+#define TFDP_FFT_PROLOGUE                                              \
+  constexpr int T = fft_threads_c(P);                                  \
+  extern __shared__ float4 sm4[];                                      \
+  float4* a = sm4;                                                     \
+  float2* tws = reinterpret_cast<float2*>(sm4 + padded_len(P));        \
+  load_tw(tws, tw, P); /* constant since the plan: before the wait */ \
+  pdl_wait();                                                          \
+  pdl_trigger();
+
+// ---------------------------------------------------------------- K spectrum: rows
+// four rows dy0..dy0+3 per block: lane A = row dy0 + i row dy0+1, lane B = rows dy0+2, +3;
+// the real-even row spectra (q <= P/2) leave from the last stage
+TFDP_FFT_KERNEL(kspec_rows_kernel)(const GridGeom* __restrict__ geom, float neg_gamma, int gi,
+                                   const float2* __restrict__ tw, float* __restrict__ KA,
+                                   int ka_pitch) {
+  TFDP_FFT_PROLOGUE
+  const GridGeom g = *geom;
+  const int M = g.M;
+  const int dy0 = 4 * blockIdx.x;
+  if (dy0 >= M) return;
+  const float h2 = g.h * g.h;
+  const float scale = 1.0f / ((float)P * (float)P);
+  for (int x = threadIdx.x; x < P; x += T) {
+    const int dx = (x <= M - 1) ? x : ((x >= P - (M - 1)) ? x - P : INT32_MAX);
+    float v[4] = {0.f, 0.f, 0.f, 0.f};
+    if (dx != INT32_MAX) {
+      const float dx2 = (float)(dx * dx);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int dy = dy0 + c;
+        if (dy < M) v[c] = ksample(fmaf(h2, dx2 + (float)(dy * dy), 1.0f), neg_gamma, gi) * scale;
+      }
+    }
+    a[pad(x)] = make_float4(v[0], v[2], v[1], v[3]);
+  }
+  __syncthreads();
+  auto dst = [&](int q, C2 z) {  // real-even rows: Re = even row, Im = odd row
+    if (q > P / 2) return;
+    float* o = KA + (int64_t)q * ka_pitch + dy0;
+    const float r4[4] = {z.re.x, z.im.x, z.re.y, z.im.y};
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      if (dy0 + c < M) o[c] = r4[c];
+  };
+  fft_smem<T, P, 0>(a, tws, SmemIO{}, dst);
+}
+
+// ---------------------------------------------------------------- K spectrum: columns
+// four columns q0..q0+3 per block (lane A = q0 + i q0+1, lane B = q0+2 + i q0+3), each the
+// real-even mirror of dy = 0..M-1, read by the first stage; KH written by the last
+TFDP_FFT_KERNEL(kspec_cols_kernel)(const GridGeom* __restrict__ geom,
+                                   const float* __restrict__ KA, int ka_pitch,
+                                   const float2* __restrict__ tw, float* __restrict__ KH) {
+  TFDP_FFT_PROLOGUE
+  const int M = geom->M;
+  constexpr int half = P / 2;
+  const int q0 = 4 * blockIdx.x;
+  __syncthreads();  // twiddle table
+  auto src = [&](int u) {
+    const int dy = (u <= M - 1) ? u : ((u >= P - (M - 1)) ? P - u : -1);
+    float v[4] = {0.f, 0.f, 0.f, 0.f};
+    if (dy >= 0) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (q0 + c <= half) v[c] = KA[(int64_t)(q0 + c) * ka_pitch + dy];
+    }
+    return C2{make_float2(v[0], v[2]), make_float2(v[1], v[3])};
+  };
+  auto dst = [&](int u, C2 z) {
+    const float r4[4] = {z.re.x, z.im.x, z.re.y, z.im.y};
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      if (q0 + c <= half) KH[(int64_t)(q0 + c) * P + u] = r4[c];
+  };
+  fft_smem<T, P, 0>(a, tws, src, dst);
+}
+
+// ---------------------------------------------------------------- columns
+// Two (channel, column) items per block, three blocks per two columns q = 2u, 2u+1:
+//   sub 0: (ch 0, 2u) and (ch 0, 2u+1);  sub 1: (ch 1, 2u), (ch 2, 2u);  sub 2: (ch 1, 2u+1),
+//   (ch 2, 2u+1) — the blocks of a column pair are adjacent (K^ columns shared in L2).
+// The forward FFT reads the columns in its first stage and multiplies by K^ (conjugated for
+// the inverse) in its last; the inverse FFT writes rows 0..M-1 from its last stage.
+TFDP_FFT_KERNEL(cols_kernel)(const GridGeom* __restrict__ geom, float2* __restrict__ CA,
+                             int ca_pitch, const float* __restrict__ KH,
+                             const float2* __restrict__ tw) {
+  TFDP_FFT_PROLOGUE
+  const int M = geom->M;
+  constexpr int half = P / 2;
+  const int u2 = blockIdx.x / 3, sub = blockIdx.x % 3;
+  int chA, qA, chB, qB;
+  if (sub == 0) {
+    chA = 0, qA = 2 * u2, chB = 0, qB = 2 * u2 + 1;
+  } else {
+    const int q = 2 * u2 + sub - 1;
+    chA = 1, qA = q, chB = 2, qB = q;
+  }
+  if (qA > half) return;
+  const bool hB = qB <= half;
+  float2* colA = CA + ((int64_t)chA * (half + 1) + qA) * ca_pitch;
+  float2* colB = CA + ((int64_t)chB * (half + 1) + (hB ? qB : qA)) * ca_pitch;
+  const float* khA = KH + (int64_t)qA * P;
+  const float* khB = KH + (int64_t)(hB ? qB : qA) * P;
+  __syncthreads();  // twiddle table
+  auto src = [&](int u) {  // u < P/2 (ZU)
+    float2 va = make_float2(0.f, 0.f), vb = va;
+    if (u < M) {
+      va = colA[u];
+      if (hB) vb = colB[u];
+    }
+    return C2{make_float2(va.x, vb.x), make_float2(va.y, vb.y)};
+  };
+  auto mult = [&](int u, C2 z) {  // x K^ (real), conjugated for the inverse
+    const float2 k = make_float2(__ldg(khA + u), __ldg(khB + u));
+    st(a + pad(u), C2{__fmul2_rn(z.re, k), __fmul2_rn(z.im, neg2(k))});
+  };
+  fft_smem<T, P, kZeroUpper>(a, tws, src, mult);
+  __syncthreads();
+  auto out = [&](int u, C2 z) {  // u < P/2 (LowOut)
+    if (u < M) {
+      colA[u] = make_float2(z.re.x, -z.im.x);
+      if (hB) colB[u] = make_float2(z.re.y, -z.im.y);
+    }
+  };
+  fft_smem<T, P, kLowOut>(a, tws, SmemIO{}, out);
+}
+
+// ================================================================ AoS core (row passes)
+// The row passes keep one complex FFT per group of T threads in AoS (float2) layout with RB
+// groups per block: the transposed half-spectrum accesses of a row pass are latency-bound,
+// and the AoS form needs ~60 registers (radix-16 butterfly of one FFT) against ~84 for the
+// SoA pair, i.e. 32 instead of 24 warps per SM (C4 k = 1: rows_fwd 23.0 vs 28.8 us, rows_inv
+// 20.9 vs 23.0 us; k = 3: 158 vs 214 us).
+namespace aos {
+
+template <int T>
+constexpr int kMinBlocksA = T == 128 ? 8 : T == 256 ? 4 : T == 384 ? 3 : 2;
+
 __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return __fadd2_rn(a, b); }
 __device__ __forceinline__ float2 csub(float2 a, float2 b) {
   return __ffma2_rn(b, make_float2(-1.0f, -1.0f), a);
@@ -161,54 +660,6 @@ __device__ __forceinline__ void dft<16>(float2 (&v)[16]) {
   dft16<false>(v);
 }
 
-// Shared-memory layout: one float2 of padding per 16 (pad(i) = i + i/16): the strided
-// Stockham stores of the first stages become conflict-free and, since every stride is a
-// multiple of 16 (P % 256 == 0), address(r) = base + r * padded_stride.
-__device__ __forceinline__ int pad(int i) { return i + (i >> 4); }
-__host__ __device__ constexpr int padded_len(int N) { return N + (N >> 4) + 1; }
-
-// Two-level twiddle table: tw[0..64) = exp(-2 pi i t / N), tw[64 + u] = exp(-2 pi i 64u / N),
-// exp(-2 pi i t / N) = tw[64 + t/64] * tw[t % 64].
-__host__ __device__ constexpr int tw_len(int N) { return 64 + N / 64 + 1; }
-__device__ __forceinline__ float2 tw_at(const float2* __restrict__ tw, int t) {
-  return cmul(tw[64 + (t >> 6)], tw[t & 63]);
-}
-
-// w^r for r = 1..R-1 from one table lookup and a product chain of depth <= 3.
-template <int R>
-__device__ __forceinline__ void twiddles(const float2* __restrict__ tw, int base, float2 (&w)[R]) {
-  w[1] = tw_at(tw, base);
-  if constexpr (R >= 3) w[2] = cmul(w[1], w[1]);
-  if constexpr (R >= 4) w[3] = cmul(w[2], w[1]);
-  if constexpr (R >= 5) w[4] = cmul(w[2], w[2]);
-  if constexpr (R >= 8) {
-    w[5] = cmul(w[4], w[1]);
-    w[6] = cmul(w[4], w[2]);
-    w[7] = cmul(w[4], w[3]);
-  }
-  if constexpr (R == 16) {  // second lookup keeps the product chains at depth <= 3
-    w[8] = tw_at(tw, 8 * base);
-#pragma unroll
-    for (int r = 1; r < 8; ++r) w[8 + r] = cmul(w[8], w[r]);
-  }
-}
-
-// Threads per FFT block: the smallest of {128, 256, 384, 512} >= P/16 (one radix-16
-// butterfly per thread).
-__host__ __device__ constexpr int fft_threads_c(int P) {
-  return P <= 2048 ? 128 : P <= 4096 ? 256 : P <= 6144 ? 384 : 512;
-}
-
-// Register cap via min blocks per SM: 64 registers per thread (56 for 384-thread blocks, so
-// three P = 4608..6144 blocks fit per SM instead of two: k = 3 cols -19%).  Tighter caps
-// spill (40 registers: 36-264 B).
-template <int T>
-constexpr int kMinBlocks = T == 128 ? 8 : T == 256 ? 4 : T == 384 ? 3 : 2;
-
-// FFT flags: inputs zero at index >= N/2 (first stage skips them); only outputs < N/2 needed
-// (last stage stores half).
-enum { kZeroUpper = 1, kLowOut = 2 };
-
 // In-place Stockham autosort stage (Govindaraju et al. 2008 formulation): radix R, size N,
 // sub-transform size Ns (1 for the first stage, else a multiple of 16 since N % 256 == 0 and
 // the first stage is radix 16).  Loads + butterflies into registers, barrier, stores, barrier.
@@ -258,10 +709,6 @@ __device__ __forceinline__ void stage(float2* buf, const float2* __restrict__ tw
   __syncthreads();
 }
 
-__host__ __device__ constexpr int next_radix(int rem) {
-  return rem % 16 == 0 ? 16 : rem % 8 == 0 ? 8 : rem % 4 == 0 ? 4 : rem % 2 == 0 ? 2
-       : rem % 3 == 0 ? 3 : 5;
-}
 
 template <int T, int N, int FLAGS, int Ns, int REM>
 __device__ __forceinline__ void fft_rec(float2* buf, const float2* __restrict__ tw, int tid) {
@@ -285,111 +732,13 @@ __device__ __forceinline__ void fft_smem(float2* buf, const float2* __restrict__
   fft_rec<T, N, FLAGS, 1, N>(buf, tw, tid);
 }
 
-__global__ void twiddle_kernel(float2* tw, int N) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= tw_len(N)) return;
-  const int t = i < 64 ? i : 64 * (i - 64);
-  double s, c;
-  sincospi(2.0 * (double)t / (double)N, &s, &c);
-  tw[i] = make_float2((float)c, (float)-s);
-}
-
-__device__ __forceinline__ void load_tw(float2* dst, const float2* __restrict__ src, int N) {
-  for (int i = threadIdx.x; i < tw_len(N); i += blockDim.x) dst[i] = src[i];
-}
-
-// t-kernel sample (1 + d^2)^-gamma with the integer-gamma fast paths (uniform branch).
-__device__ __forceinline__ float ksample(float s, float neg_gamma, int gi) {
-  switch (gi) {
-    case 1: return pow_neg<1>(s, neg_gamma);
-    case 2: return pow_neg<2>(s, neg_gamma);
-    case 3: return pow_neg<3>(s, neg_gamma);
-    case 4: return pow_neg<4>(s, neg_gamma);
-    case 8: return pow_neg<8>(s, neg_gamma);
-    default: return pow_neg<0>(s, neg_gamma);
-  }
-}
-
-#define TFDP_FFT_KERNEL(name) \
-  template <int P>            \
-  __global__ void __launch_bounds__(fft_threads_c(P), kMinBlocks<fft_threads_c(P)>) name
-
-// ---------------------------------------------------------------- K spectrum: rows
-TFDP_FFT_KERNEL(kspec_rows_kernel)(const GridGeom* __restrict__ geom, float neg_gamma, int gi,
-                                   const float2* __restrict__ tw, float* __restrict__ KA,
-                                   int ka_pitch) {
-  constexpr int T = fft_threads_c(P);
-  extern __shared__ float2 sm[];
-  float2* a = sm;
-  float2* tws = sm + padded_len(P);
-  load_tw(tws, tw, P);  // constant since the plan: safe before the wait
-  pdl_wait();
-  pdl_trigger();
-  const GridGeom g = *geom;
-  const int M = g.M;
-  const int dya = 2 * blockIdx.x, dyb = dya + 1;
-  if (dya >= M) return;
-  const float h2 = g.h * g.h;
-  const float scale = 1.0f / ((float)P * (float)P);
-  for (int x = threadIdx.x; x < P; x += T) {
-    const int dx = (x <= M - 1) ? x : ((x >= P - (M - 1)) ? x - P : INT32_MAX);
-    float va = 0.f, vb = 0.f;
-    if (dx != INT32_MAX) {
-      const float dx2 = (float)(dx * dx);
-      va = ksample(fmaf(h2, dx2 + (float)(dya * dya), 1.0f), neg_gamma, gi) * scale;
-      if (dyb < M) vb = ksample(fmaf(h2, dx2 + (float)(dyb * dyb), 1.0f), neg_gamma, gi) * scale;
-    }
-    a[pad(x)] = make_float2(va, vb);
-  }
-  __syncthreads();
-  fft_smem<T, P, 0>(a, tws);
-  for (int q = threadIdx.x; q <= P / 2; q += T) {  // real-even rows: row a in Re, b in Im
-    const float2 z = a[pad(q)];
-    KA[(int64_t)q * ka_pitch + dya] = z.x;
-    if (dyb < M) KA[(int64_t)q * ka_pitch + dyb] = z.y;
-  }
-}
-
-// ---------------------------------------------------------------- K spectrum: columns
-TFDP_FFT_KERNEL(kspec_cols_kernel)(const GridGeom* __restrict__ geom,
-                                   const float* __restrict__ KA, int ka_pitch,
-                                   const float2* __restrict__ tw, float* __restrict__ KH) {
-  constexpr int T = fft_threads_c(P);
-  extern __shared__ float2 sm[];
-  float2* a = sm;
-  float2* tws = sm + padded_len(P);
-  load_tw(tws, tw, P);  // constant since the plan: safe before the wait
-  pdl_wait();
-  pdl_trigger();
-  const int M = geom->M;
-  constexpr int half = P / 2;
-  const int q0 = 2 * blockIdx.x, q1 = q0 + 1;
-  const bool h1 = q1 <= half;
-  for (int u = threadIdx.x; u < P; u += T) {  // mirror of dy = 0..M-1 (real even)
-    const int dy = (u <= M - 1) ? u : ((u >= P - (M - 1)) ? P - u : -1);
-    float va = 0.f, vb = 0.f;
-    if (dy >= 0) {
-      va = KA[(int64_t)q0 * ka_pitch + dy];
-      if (h1) vb = KA[(int64_t)q1 * ka_pitch + dy];
-    }
-    a[pad(u)] = make_float2(va, vb);
-  }
-  __syncthreads();
-  fft_smem<T, P, 0>(a, tws);
-  for (int u = threadIdx.x; u < P; u += T) {
-    const float2 z = a[pad(u)];
-    KH[(int64_t)q0 * P + u] = z.x;
-    if (h1) KH[(int64_t)q1 * P + u] = z.y;
-  }
-}
-
 // ---------------------------------------------------------------- forward rows
 // RB row pairs per block (RB groups of T threads, one FFT each): the block's 2 RB rows are
 // consecutive in the column-major half spectra, so the transposed stores write 16 RB
 // contiguous bytes per q (RB = 1: half a sector).
 template <int P, int RB>
 constexpr int rows_min_blocks() {
-  return kMinBlocks<fft_threads_c(P)> / RB > 0 ? kMinBlocks<fft_threads_c(P)> / RB : 1;
+  return kMinBlocksA<fft_threads_c(P)> / RB > 0 ? kMinBlocksA<fft_threads_c(P)> / RB : 1;
 }
 
 template <int P, int RB>
@@ -444,41 +793,6 @@ rows_fwd_kernel(const GridGeom* __restrict__ geom, float* __restrict__ C, int cp
     float2* o = out + (int64_t)q * ca_pitch + 2 * gg;
     if (2 * gg + 1 < rows_here) *reinterpret_cast<float4*>(o) = make_float4(xa.x, xa.y, xb.x, xb.y);
     else *o = xa;
-  }
-}
-
-// ---------------------------------------------------------------- columns
-TFDP_FFT_KERNEL(cols_kernel)(const GridGeom* __restrict__ geom, float2* __restrict__ CA,
-                             int ca_pitch, const float* __restrict__ KH,
-                             const float2* __restrict__ tw) {
-  constexpr int T = fft_threads_c(P);
-  extern __shared__ float2 sm[];
-  float2* a = sm;
-  float2* tws = sm + padded_len(P);
-  load_tw(tws, tw, P);  // constant since the plan: safe before the wait
-  pdl_wait();
-  pdl_trigger();
-  const int M = geom->M;
-  constexpr int half = P / 2;
-  // the three channels of one column are consecutive blocks: they share the K^ column in L2
-  const int q = blockIdx.x / 3, ch = blockIdx.x % 3;
-  float2* col = CA + ((int64_t)ch * (half + 1) + q) * ca_pitch;
-#pragma unroll
-  for (int u = threadIdx.x; u < half; u += T) a[pad(u)] = (u < M) ? col[u] : make_float2(0.f, 0.f);
-  __syncthreads();
-  fft_smem<T, P, kZeroUpper>(a, tws);
-  const float* kh = KH + (int64_t)q * P;
-#pragma unroll 4
-  for (int u = threadIdx.x; u < P; u += T) {  // x K^ (real), conjugated for the inverse
-    const float2 z = a[pad(u)];
-    const float kk = __ldg(kh + u);
-    a[pad(u)] = make_float2(z.x * kk, -z.y * kk);
-  }
-  __syncthreads();
-  fft_smem<T, P, kLowOut>(a, tws);
-  for (int u = threadIdx.x; u < M; u += T) {
-    const float2 z = a[pad(u)];
-    col[u] = make_float2(z.x, -z.y);
   }
 }
 
@@ -539,6 +853,8 @@ rows_inv_kernel(const GridGeom* __restrict__ geom, const float2* __restrict__ CA
   }
 }
 
+}  // namespace aos
+
 }  // namespace
 
 // Supported FFT sizes: P = 256 q, q = 2^a 3^b 5^c with b <= 2, c <= 1, P <= 8192.
@@ -553,11 +869,11 @@ bool fft_size_supported(int P) {
   return false;
 }
 
-size_t fftconv_smem_bytes(int P, int groups) {
-  return (size_t)(groups * padded_len(P) + tw_len(P)) * sizeof(float2);
+size_t fftconv_smem_bytes(int P) {
+  return (size_t)padded_len(P) * sizeof(float4) + (size_t)tw_len(P) * sizeof(float2);
 }
 
-// Row pairs per block of the row passes: 2 up to 512-thread blocks (P <= 4096; C4 k = 1:
+// Row pairs per block of the AoS row passes: 2 up to 512-thread blocks (P <= 4096; C4 k = 1:
 // rows_fwd 27.0 -> 23.0 us, k = 2: 94.8 -> 77.3 us), else 1 (P = 6144 at RB = 2 holds one
 // 768-thread block per SM: 217 -> 232 us).  TFDP_ROWS_RB = 1, 2, 4 overrides (A/B runs),
 // limited to blocks of <= 1024 threads.
@@ -571,17 +887,21 @@ int rows_rb(int P) {
   return rb;
 }
 
+size_t rows_smem_bytes(int P, int groups) {
+  return (size_t)(groups * padded_len(P) + tw_len(P)) * sizeof(float2);
+}
+
 cudaError_t fftconv_prepare(int P) {
-  const int b = (int)fftconv_smem_bytes(P, 1);
+  const int b = (int)fftconv_smem_bytes(P);
   const int rb = rows_rb(P);
-  const int br = (int)fftconv_smem_bytes(P, rb);
+  const int br = (int)rows_smem_bytes(P, rb);
   cudaError_t e = cudaErrorInvalidValue;
 #define TFDP_PREP_ROWS(S, RB)                                                                  \
   if constexpr (fft_threads_c(S) * RB <= 1024) {                                             \
     if (e == cudaSuccess && rb == RB) {                                                        \
-      e = cudaFuncSetAttribute(rows_fwd_kernel<S, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, br); \
+      e = cudaFuncSetAttribute(aos::rows_fwd_kernel<S, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, br); \
       if (e == cudaSuccess)                                                                    \
-        e = cudaFuncSetAttribute(rows_inv_kernel<S, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, br); \
+        e = cudaFuncSetAttribute(aos::rows_inv_kernel<S, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, br); \
     }                                                                                          \
   }
 #define TFDP_PREP(S)                                                                          \
@@ -607,23 +927,23 @@ void launch_twiddles(float2* tw, int P, cudaStream_t s) {
 
 void launch_kspec(const GridGeom* geom, int P, int Mcap, ForceArgs fa, const float2* tw,
                   float* KA, int ka_pitch, float* KH, cudaStream_t s) {
-  const size_t sm = fftconv_smem_bytes(P, 1);
+  const size_t sm = fftconv_smem_bytes(P);
 #define TFDP_KS(S)                                                                          \
   case S:                                                                                   \
-    kspec_rows_kernel<S><<<(unsigned)((Mcap + 1) / 2), fft_threads_c(S), sm, s>>>(          \
+    kspec_rows_kernel<S><<<(unsigned)((Mcap + 3) / 4), fft_threads_c(S), sm, s>>>(          \
         geom, -fa.gamma, fa.gamma_int, tw, KA, ka_pitch);                                   \
-    launch_chained(kspec_cols_kernel<S>, (unsigned)((S / 2 + 2) / 2), fft_threads_c(S), sm, s, \
+    launch_chained(kspec_cols_kernel<S>, (unsigned)((S / 2 + 4) / 4), fft_threads_c(S), sm, s, \
                    geom, KA, ka_pitch, tw, KH);                                             \
     break;
   switch (P) { TFDP_FFT_SIZES(TFDP_KS) default: break; }
 #undef TFDP_KS
 }
 
-// launches one instantiation per (P, RB) with RB a compile-time constant
+// launches one AoS row-pass instantiation per (P, RB) with RB a compile-time constant
 #define TFDP_ROWS_DISPATCH(S, KERN, ...)                                                       \
   {                                                                                           \
     const int rb = rows_rb(S);                                                                \
-    const size_t smb = fftconv_smem_bytes(S, rb);                                             \
+    const size_t smb = rows_smem_bytes(S, rb);                                                \
     const dim3 grid((unsigned)(((Mcap + 1) / 2 + rb - 1) / rb), 3);                           \
     if (rb == 4) {                                                                            \
       if constexpr (fft_threads_c(S) * 4 <= 1024)                                             \
@@ -640,7 +960,7 @@ void launch_rows_fwd(const GridGeom* geom, float* C, int cpitch, int P, int Mcap
                      const float2* tw, float2* CA, int ca_pitch, cudaStream_t s) {
 #define TFDP_RF(S)                                                                          \
   case S:                                                                                   \
-    TFDP_ROWS_DISPATCH(S, rows_fwd_kernel, geom, C, cpitch, tw, CA, ca_pitch)               \
+    TFDP_ROWS_DISPATCH(S, aos::rows_fwd_kernel, geom, C, cpitch, tw, CA, ca_pitch)          \
     break;
   switch (P) { TFDP_FFT_SIZES(TFDP_RF) default: break; }
 #undef TFDP_RF
@@ -648,10 +968,10 @@ void launch_rows_fwd(const GridGeom* geom, float* C, int cpitch, int P, int Mcap
 
 void launch_cols(const GridGeom* geom, float2* CA, int ca_pitch, const float* KH, int P,
                  const float2* tw, cudaStream_t s) {
-  const size_t sm = fftconv_smem_bytes(P, 1);
+  const size_t sm = fftconv_smem_bytes(P);
 #define TFDP_CO(S)                                                                          \
   case S:                                                                                   \
-    cols_kernel<S><<<(unsigned)(3 * (S / 2 + 1)), fft_threads_c(S), sm, s>>>(               \
+    cols_kernel<S><<<(unsigned)(3 * ((S / 2 + 2) / 2)), fft_threads_c(S), sm, s>>>(         \
         geom, CA, ca_pitch, KH, tw);                                                        \
     break;
   switch (P) { TFDP_FFT_SIZES(TFDP_CO) default: break; }
@@ -662,7 +982,7 @@ void launch_rows_inv(const GridGeom* geom, const float2* CA, int ca_pitch, int P
                      const float2* tw, float* Phi, int cpitch, cudaStream_t s) {
 #define TFDP_RI(S)                                                                          \
   case S:                                                                                   \
-    TFDP_ROWS_DISPATCH(S, rows_inv_kernel, geom, CA, ca_pitch, tw, Phi, cpitch)             \
+    TFDP_ROWS_DISPATCH(S, aos::rows_inv_kernel, geom, CA, ca_pitch, tw, Phi, cpitch)        \
     break;
   switch (P) { TFDP_FFT_SIZES(TFDP_RI) default: break; }
 #undef TFDP_RI

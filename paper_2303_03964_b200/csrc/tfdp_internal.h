@@ -59,6 +59,11 @@ struct FocusArgs {
 // Every chain kernel calls pdl_wait() before touching any buffer another kernel writes, so
 // the ordering is the plain stream order.  TFDP_PDL=0 disables the attribute (A/B runs).
 bool pdl_enabled();
+// Per-iteration switch (host thread): the ibFFT chain uses PDL only up to P = 2048 — at
+// P = 4096 / 6144 the overlapped launches were slower (C4 k = 2: 405 vs 385 us, k = 3: 1091
+// vs 973 us per iteration), at P = 2048 faster (122.6 vs 124.5 us).
+constexpr int kPdlMaxFft = 2048;
+void set_pdl_active(bool on);
 template <typename... KArgs, typename... Args>
 inline void launch_chained(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
                            cudaStream_t s, Args... args) {
