@@ -105,6 +105,21 @@ def load_peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)", {}
 
 
+TRAFFIC_JSON = os.path.join(ROOT, "profiles", "r1_traffic.json")
+
+
+def ncu_traffic(kind: str, ks) -> float | None:
+    """Measured DRAM bytes per launch of `kind`, averaged over the launch mix ks (one k per
+    launch), from the committed ncu --set full capture (tools/ncu_traffic.py) of the C4
+    workload; None when the capture does not cover the kernel or the workload differs."""
+    if not os.path.exists(TRAFFIC_JSON):
+        return None
+    per_k = json.load(open(TRAFFIC_JSON)).get("kernels", {}).get(kind)
+    if not per_k or any(str(k) not in per_k for k in ks):
+        return None
+    return float(np.mean([per_k[str(k)] for k in ks]))
+
+
 def alg_bytes(kind: str, n: int, nnz: int, M: int, P: int, n_spread: int) -> float:
     """Algorithmic HBM bytes of one launch (DESIGN.md §Kernels table)."""
     hq = P // 2 + 1  # half-spectrum length
@@ -274,17 +289,19 @@ def run_fft(args, rank, world, local):
             else:
                 work.append(alg_bytes(dom, n_local if dom == "gather_update" else w.n, nnz, M, Pk, w.n))
     dom_ms, dom_n = prof[dom]
+    traffic = ncu_traffic(dom, KS20) if args.config == "C4" else None
     total = float(np.sum(work)) if dom_n == len(work) else float(np.mean(work)) * dom_n
     if dom in FFT_KINDS:
         achieved = total / (dom_ms / 1e3) / 1e12
         roof = {"kernel": dom, "bound": "alu", "achieved": round(achieved, 2), "peak": round(fp32_peak / 1e12, 2),
-                "unit": "TFLOP/s", "frac": round(achieved * 1e12 / fp32_peak, 4), "traffic": None,
+                "unit": "TFLOP/s", "frac": round(achieved * 1e12 / fp32_peak, 4), "traffic": traffic,
+                "traffic_unit": "DRAM bytes per launch (ncu, profiles/r1_traffic.json)",
                 "peak_source": f"FP32 FMA peak {n_sm} SMs x 128 lanes x 2 x {f_mhz:.0f} MHz (measured clock)",
                 "work_per_launch": round(total / dom_n), "work_unit": "flop (5 N log2 N per complex FFT)"}
     else:
         achieved = total / (dom_ms / 1e3) / 1e9
         roof = {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
-                "frac": round(achieved / hbm_peak, 4), "traffic": None, "peak_source": peak_src,
+                "frac": round(achieved / hbm_peak, 4), "traffic": traffic, "peak_source": peak_src,
                 "work_per_launch": round(total / dom_n), "work_unit": "algorithmic bytes"}
     tot_all = sum(v[0] for v in prof_all.values())
     kernels = {k: {"us_per_launch": round(1e3 * v[0] / max(v[1], 1), 2), "launches": v[1],

@@ -7,7 +7,8 @@ import os
 import re
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtfdp.so")
+# TFDP_LIB_PATH: developer A/B runs against a variant build (build.py defines/out)
+LIB_PATH = os.environ.get("TFDP_LIB_PATH") or os.path.join(HERE, "libtfdp.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "tfdp.h")
 
 TFDP_OK = 0

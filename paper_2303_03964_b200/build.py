@@ -49,25 +49,46 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
-    if not force and not needs_build():
+def build(verbose: bool = False, force: bool = False, defines=(), out: str = None) -> str:
+    """Compiles every source to an object in parallel (one nvcc per file), then links.
+    defines / out: developer A/B variants (e.g. -DTFDP_ATTR_BATCH=4 into another .so)."""
+    out = out or LIB
+    if not force and out == LIB and not needs_build():
         return LIB
-    cmd = [
-        _nvcc(), "-O3", "-std=c++17", *ARCH, "-lineinfo", "--shared",
+    from concurrent.futures import ThreadPoolExecutor
+
+    common = [
+        _nvcc(), "-O3", "-std=c++17", *ARCH, "-lineinfo",
         "-Xcompiler", "-fPIC,-fopenmp,-O3",
         "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", _nccl_include(),
         *(["-Xptxas", "-v"] if verbose else []),
-        *sources(),
-        "-lgomp", "-ldl",
-        "-o", LIB + ".tmp",
+        *defines,
     ]
+    objdir = os.path.join(ROOT, "build", "obj" if out == LIB else "obj_" + os.path.basename(out))
+    os.makedirs(objdir, exist_ok=True)
+
+    def compile_one(src):
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        cmd = common + ["-c", src, "-o", obj]
+        return obj, cmd, subprocess.run(cmd, capture_output=True, text=True)
+
+    srcs = sources()
+    with ThreadPoolExecutor(max_workers=max(1, min(len(srcs), os.cpu_count() or 1))) as ex:
+        results = list(ex.map(compile_one, srcs))
+    for obj, cmd, r in results:
+        if verbose or r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+        if r.returncode != 0:
+            raise RuntimeError("nvcc failed:\n" + " ".join(cmd))
+    cmd = [_nvcc(), *ARCH, "--shared", "-Xcompiler", "-fPIC,-fopenmp",
+           *[o for o, _, _ in results], "-lgomp", "-ldl", "-o", out + ".tmp"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if verbose or r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
     if r.returncode != 0:
-        raise RuntimeError("nvcc failed:\n" + " ".join(cmd))
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+        raise RuntimeError("nvcc link failed:\n" + " ".join(cmd))
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":

@@ -87,9 +87,9 @@ struct tfdp_ctx {
   int P_of_k[4] = {0, 0, 0, 0};
   int cap_of_k[4] = {0, 0, 0, 0};
   int cpitch = 0;        // pitch of the compact [3][M][M] charge / potential planes
-  int ca_pitch = 0;      // row pitch of the half-spectra CA[3][P/2+1][.] (even)
+  int ca_pitch = 0;      // rows of the half-spectra CA (multiple of 32; kernels_fftconv.cu)
   int64_t alloc_planes = 0, alloc_ca = 0, alloc_ka = 0;
-  float* grid = nullptr;  // charges C (spread target)
+  float* grid = nullptr;  // charges C (spread target): float4 {C_1, C_x~, C_y~, 0} per node
   float* phi = nullptr;   // potentials Phi (gather source)
   float2* ca = nullptr;   // row half-spectra, transformed in place by the column pass
   float* ka = nullptr;    // kernel row spectra KA[q][dy]
@@ -424,8 +424,9 @@ tfdp_status configure_fft(tfdp_ctx* c, float L) {
   }
   c->nint_cap = need;
   const int cpitch = mcap;
-  const int capitch = (mcap + 1) & ~1;
-  int64_t planes = 3LL * cpitch * cpitch, ca = 0, ka = 0, kh = 0;
+  const int capitch = (mcap + 31) & ~31;  // multiple of the CA row tile (kernels_fftconv.cu)
+  // charges: one float4 {C_1, C_x~, C_y~, 0} per grid node; potentials: 3 planes
+  int64_t planes = 4LL * cpitch * cpitch, ca = 0, ka = 0, kh = 0;
   for (int k = 1; k <= 3; ++k) {
     if (!k_used(c, k)) continue;
     ca = std::max<int64_t>(ca, 3LL * (c->P_of_k[k] / 2 + 1) * capitch);
@@ -444,7 +445,7 @@ tfdp_status configure_fft(tfdp_ctx* c, float L) {
     CUDA_TRY(c, cudaMalloc(&c->grid, planes * sizeof(float)));
     // invariant: the charge planes are zero between iterations (rows_fwd re-zeroes)
     CUDA_TRY(c, cudaMemsetAsync(c->grid, 0, planes * sizeof(float), c->stream));
-    CUDA_TRY(c, cudaMalloc(&c->phi, planes * sizeof(float)));
+    CUDA_TRY(c, cudaMalloc(&c->phi, (planes / 4) * 3 * sizeof(float)));
     CUDA_TRY(c, cudaMalloc(&c->ca, ca * sizeof(float2)));
     CUDA_TRY(c, cudaMalloc(&c->ka, ka * sizeof(float)));
     CUDA_TRY(c, cudaMalloc(&c->kh, kh * sizeof(float)));
@@ -548,32 +549,28 @@ tfdp_status evaluate(tfdp_ctx* c, int update, float eta, int k) {
       tfdp::launch_kspec(c->geom, P, mcap, c->fa, tw, c->ka, c->cpitch, c->kh, ks);
     }
     if (overlap) CUDA_TRY(c, cudaEventRecord(c->ev_join, c->side));
-    // The charge planes are all-zero here: they start zeroed and rows_fwd clears every row
-    // it consumes (no separate zeroing pass).
+    // The charges are all-zero here: they start zeroed and rows_inv clears the rows rows_fwd
+    // consumed (no separate zeroing pass).
     const bool allreduce = c->world > 1 && c->p.dist_mode == TFDP_DIST_GRID_ALLREDUCE;
+    float4* grid4 = reinterpret_cast<float4*>(c->grid);
     {
       Scope sc(c, K_SPREAD);
       if (allreduce)
-        tfdp::launch_spread(xy, c->lo, n_local, c->geom, k, c->grid, c->stream);
+        tfdp::launch_spread(xy, c->lo, n_local, c->geom, k, grid4, c->stream);
       else
-        tfdp::launch_spread(xy, 0, c->n, c->geom, k, c->grid, c->stream);
+        tfdp::launch_spread(xy, 0, c->n, c->geom, k, grid4, c->stream);
     }
     if (allreduce) {
       if (!c->comm)
         return fail(c, TFDP_ERR_UNSUPPORTED, "grid all-reduce needs an NCCL communicator");
       Scope sc(c, K_COMM);
-      // rows [0, M_cap) of each plane (the charges live in [0, M) x [0, M))
-      NCCL_TRY(c, c->nccl->GroupStart());
-      for (int ch = 0; ch < 3; ++ch) {
-        float* pl = c->grid + (size_t)ch * c->cpitch * c->cpitch;
-        NCCL_TRY(c, c->nccl->AllReduce(pl, pl, (size_t)mcap * c->cpitch, ncclFloat, ncclSum,
-                                       c->comm, c->stream));
-      }
-      NCCL_TRY(c, c->nccl->GroupEnd());
+      // rows [0, M_cap) of the interleaved charges (they live in [0, M) x [0, M))
+      NCCL_TRY(c, c->nccl->AllReduce(c->grid, c->grid, (size_t)mcap * c->cpitch * 4, ncclFloat,
+                                     ncclSum, c->comm, c->stream));
     }
     {
       Scope sc(c, K_ROWS_FWD);
-      tfdp::launch_rows_fwd(c->geom, c->grid, c->cpitch, P, mcap, tw, c->ca, c->ca_pitch, c->stream);
+      tfdp::launch_rows_fwd(c->geom, grid4, c->cpitch, P, mcap, tw, c->ca, c->ca_pitch, c->stream);
     }
     if (overlap) CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_join, 0));
     {
@@ -582,7 +579,8 @@ tfdp_status evaluate(tfdp_ctx* c, int update, float eta, int k) {
     }
     {
       Scope sc(c, K_ROWS_INV);
-      tfdp::launch_rows_inv(c->geom, c->ca, c->ca_pitch, P, mcap, tw, c->phi, c->cpitch, c->stream);
+      tfdp::launch_rows_inv(c->geom, c->ca, c->ca_pitch, P, mcap, tw, c->phi, c->cpitch, grid4,
+                            c->stream);
     }
     {
       Scope sc(c, K_GATHER_UPDATE);

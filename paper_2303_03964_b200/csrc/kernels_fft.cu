@@ -2,7 +2,7 @@
 //   bbox          exact fp32 min/max of the positions (ordered-uint keys, block partials)
 //   setup         box -> (lo, L, N_int, w, h, centre) on the device, no host sync (R5/R6/R19)
 //   spread        step 1: Lagrange charges {1, x~, y~} onto the k x k nodes of each
-//                 node's own interval; fp32 atomics into L2
+//                 node's own interval; fp32 v4 reductions into L2
 //   gather_update step 3 + assemble + attraction + update,
 //                 fused bbox of the new positions for the next iteration
 // The grid convolution (step 2) is kernels_fftconv.cu.
@@ -227,38 +227,85 @@ __device__ __forceinline__ Cell cell_of(float2 p, const GridGeom& g) {
 }
 
 // ------------------------------------------------------------------ spread (step 1)
+// The charges live channel-interleaved, float4 {C_1, C_x~, C_y~, 0} per grid node, so one
+// node-to-grid-node contribution is ONE vector reduction (red.global.add.v4.f32) instead of
+// three scalar ones into three planes: the L2 reduction units process a v4 RED at the
+// instruction rate of a scalar one (tools/mbench_red.cu), and the spread is bound by that
+// rate (3 k^2 -> k^2 REDs per node).
+// Warp pre-aggregation for k >= 2: lanes whose nodes fall in the same interval have the
+// same k x k target nodes, so the group's lowest lane sums the members' charges (their
+// positions and Lagrange factors arrive by shuffles, in lane order) and issues the group's
+// k^2 REDs alone.  Morton-ordered nodes put ~60 % of a warp's nodes in an interval shared
+// with another lane at unit density.  Measured at C4 (us, plain / aggregated): k = 1
+// 12.7 / 14.8 (one RED per node: the shuffles cost more than they save), k = 2 37.4 / 34.3,
+// k = 3 83.9 / 71.9.
 template <int K>
 __global__ void __launch_bounds__(kNodeThreads)
 spread_kernel(const float2* __restrict__ xy, int64_t lo, int64_t cnt,
-              const GridGeom* __restrict__ geom, float* __restrict__ grid) {
+              const GridGeom* __restrict__ geom, float4* __restrict__ grid) {
+  constexpr bool kAgg = K >= 2;
   pdl_wait();
   pdl_trigger();
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= cnt) return;
+  const bool active = t < cnt;
+  if (kAgg ? __all_sync(0xffffffffu, !active) : !active) return;
   const GridGeom g = *geom;
-  const float2 p = xy[lo + t];
+  const float2 p = active ? xy[lo + t] : make_float2(g.cx, g.cy);
   const Cell c = cell_of(p, g);
   float lx[K], ly[K];
   lagrange<K>(c.ux, lx);
   lagrange<K>(c.uy, ly);
   const float xt = p.x - g.cx, yt = p.y - g.cy;  // box-centred channels (R11)
-  const int64_t plane = (int64_t)g.pitch * g.pitch;
+  float4 acc[K][K];
+#pragma unroll
+  for (int b = 0; b < K; ++b)
+#pragma unroll
+    for (int a = 0; a < K; ++a) {
+      const float wgt = lx[a] * ly[b];
+      acc[b][a] = make_float4(wgt, wgt * xt, wgt * yt, 0.0f);
+    }
+  if constexpr (kAgg) {
+    const unsigned full = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const unsigned key = active ? (unsigned)c.by * (unsigned)g.n_int + (unsigned)c.bx : ~(unsigned)lane;
+    const unsigned grp = __match_any_sync(full, key);
+    const bool leader = (grp & ((1u << lane) - 1u)) == 0u;
+    const int gmax = (int)__reduce_max_sync(full, (unsigned)__popc(grp));
+    unsigned rest = grp & (grp - 1u);  // members after the leader
+    for (int r = 1; r < gmax; ++r) {
+      const int src = rest ? __ffs(rest) - 1 : lane;
+      const float mxt = __shfl_sync(full, xt, src), myt = __shfl_sync(full, yt, src);
+      float mlx[K], mly[K];
+#pragma unroll
+      for (int a = 0; a < K; ++a) {
+        mlx[a] = __shfl_sync(full, lx[a], src);
+        mly[a] = __shfl_sync(full, ly[a], src);
+      }
+      if (leader && rest) {
+#pragma unroll
+        for (int b = 0; b < K; ++b)
+#pragma unroll
+          for (int a = 0; a < K; ++a) {
+            const float wgt = mlx[a] * mly[b];
+            acc[b][a].x += wgt;
+            acc[b][a].y = fmaf(wgt, mxt, acc[b][a].y);
+            acc[b][a].z = fmaf(wgt, myt, acc[b][a].z);
+          }
+      }
+      rest &= rest - 1u;
+    }
+    if (!active || !leader) return;
+  }
 #pragma unroll
   for (int b = 0; b < K; ++b) {
     const int64_t row = (int64_t)(c.by * K + b) * g.pitch;
 #pragma unroll
-    for (int a = 0; a < K; ++a) {
-      const int64_t idx = row + c.bx * K + a;
-      const float wgt = lx[a] * ly[b];
-      atomicAdd(grid + idx, wgt);
-      atomicAdd(grid + plane + idx, wgt * xt);
-      atomicAdd(grid + 2 * plane + idx, wgt * yt);
-    }
+    for (int a = 0; a < K; ++a) atomicAdd(grid + row + c.bx * K + a, acc[b][a]);
   }
 }
 
 void launch_spread(const float2* xy, int64_t lo, int64_t cnt, const GridGeom* geom, int k,
-                   float* grid, cudaStream_t s) {
+                   float4* grid, cudaStream_t s) {
   if (cnt <= 0) return;
   const unsigned blocks = (unsigned)((cnt + kNodeThreads - 1) / kNodeThreads);
   if (k == 1) launch_chained(spread_kernel<1>, blocks, kNodeThreads, 0, s, xy, lo, cnt, geom, grid);

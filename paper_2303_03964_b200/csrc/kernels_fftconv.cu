@@ -5,12 +5,13 @@
 //   kspec_rows  K rows dy = 0..M-1 generated on the fly (K is even in x and y, so each row
 //               spectrum is real), four rows per block: KA[q][dy], q = 0..P/2
 //   kspec_cols  four K^ columns per block (real-even): KH[q][u] (real), u = 0..P-1
-//   rows_fwd    four charge rows per block, two per complex FFT (a + i b), untangled into
-//               the half spectra CA[c][q][row] (32 contiguous bytes per q); consumed rows
-//               are re-zeroed
+//   rows_fwd    four charge rows per block, two per complex FFT (a + i b), of one channel of
+//               the interleaved charges, untangled into the half spectra CA[c][q][row] (32
+//               contiguous bytes per q)
 //   cols        two (channel, column) items per block: FFT -> x K^ -> inverse FFT, rows
 //               0..M-1 kept
-//   rows_inv    four Hermitian rows per block, two per complex inverse FFT, columns 0..M-1
+//   rows_inv    four Hermitian rows per block, two per complex inverse FFT, columns 0..M-1;
+//               re-zeroes the same rows of the (consumed) charges, a third per channel block
 // The inputs of every forward FFT are zero beyond P/2 (M <= P/2), so the first stage skips
 // those loads; every inverse FFT keeps only outputs below P/2, so its last stage stores half.
 //
@@ -209,6 +210,27 @@ __device__ __forceinline__ void dft<16>(C2 (&v)[16]) {
 // multiple of 16 (P % 256 == 0), address(r) = base + r * padded_stride.
 __device__ __forceinline__ int pad(int i) { return i + (i >> 4); }
 __host__ __device__ constexpr int padded_len(int N) { return N + (N >> 4) + 1; }
+
+// Half-spectrum layout CA (element (channel ch, frequency q, grid row r), H = P/2 + 1
+// frequencies, ca_pitch rows, a multiple of kCaTile): row tiles of kCaTile rows,
+// CA[ch][r / kCaTile][q][r % kCaTile].  A row pass over 4 rows writes / reads 32 B per q at a
+// stride of 8 kCaTile bytes (a sequential sweep instead of the column-major stride of
+// 8 ca_pitch bytes), the column pass reads a column as kCaTile * 8-byte runs.  Measured at
+// C4 (rows_fwd + cols + rows_inv, us; column-major / tile 4 / 8 / 16 / 32): k = 1
+// 76.9 / 75.2 / 75.4 / 78.0 / 78.0, k = 2 276 / 289 / 277 / 277 / 278, k = 3
+// 692 / 674 / 649 / 675 / 670.
+#ifndef TFDP_CA_TILE
+#define TFDP_CA_TILE 8
+#endif
+constexpr int kCaTile = TFDP_CA_TILE;
+static_assert(kCaTile >= 4 && (kCaTile & (kCaTile - 1)) == 0, "CA tile: power of 2 >= 4");
+__device__ __forceinline__ int64_t ca_col_base(int ch, int q, int H, int ca_pitch) {
+  return ((int64_t)ch * (ca_pitch / kCaTile) * H + q) * kCaTile;
+}
+// offset of row r from its column base
+__device__ __forceinline__ int64_t ca_row_off(int r, int H) {
+  return (int64_t)(r / kCaTile) * kCaTile * H + (r % kCaTile);
+}
 
 // Two-level twiddle table: tw[0..64) = exp(-2 pi i t / N), tw[64 + u] = exp(-2 pi i 64u / N),
 // exp(-2 pi i t / N) = tw[64 + t/64] * tw[t % 64].
@@ -493,16 +515,18 @@ TFDP_FFT_KERNEL(cols_kernel)(const GridGeom* __restrict__ geom, float2* __restri
   }
   if (qA > half) return;
   const bool hB = qB <= half;
-  float2* colA = CA + ((int64_t)chA * (half + 1) + qA) * ca_pitch;
-  float2* colB = CA + ((int64_t)chB * (half + 1) + (hB ? qB : qA)) * ca_pitch;
+  constexpr int H = half + 1;
+  float2* colA = CA + ca_col_base(chA, qA, H, ca_pitch);
+  float2* colB = CA + ca_col_base(chB, hB ? qB : qA, H, ca_pitch);
   const float* khA = KH + (int64_t)qA * P;
   const float* khB = KH + (int64_t)(hB ? qB : qA) * P;
   __syncthreads();  // twiddle table
   auto src = [&](int u) {  // u < P/2 (ZU)
     float2 va = make_float2(0.f, 0.f), vb = va;
     if (u < M) {
-      va = colA[u];
-      if (hB) vb = colB[u];
+      const int64_t o = ca_row_off(u, H);
+      va = colA[o];
+      if (hB) vb = colB[o];
     }
     return C2{make_float2(va.x, vb.x), make_float2(va.y, vb.y)};
   };
@@ -514,8 +538,9 @@ TFDP_FFT_KERNEL(cols_kernel)(const GridGeom* __restrict__ geom, float2* __restri
   __syncthreads();
   auto out = [&](int u, C2 z) {  // u < P/2 (LowOut)
     if (u < M) {
-      colA[u] = make_float2(z.re.x, -z.im.x);
-      if (hB) colB[u] = make_float2(z.re.y, -z.im.y);
+      const int64_t o = ca_row_off(u, H);
+      colA[o] = make_float2(z.re.x, -z.im.x);
+      if (hB) colB[o] = make_float2(z.re.y, -z.im.y);
     }
   };
   fft_smem<T, P, kLowOut>(a, tws, SmemIO{}, out);
@@ -743,7 +768,7 @@ constexpr int rows_min_blocks() {
 
 template <int P, int RB>
 __global__ void __launch_bounds__(fft_threads_c(P) * RB, (rows_min_blocks<P, RB>()))
-rows_fwd_kernel(const GridGeom* __restrict__ geom, float* __restrict__ C, int cpitch,
+rows_fwd_kernel(const GridGeom* __restrict__ geom, const float4* __restrict__ C, int cpitch,
                 const float2* __restrict__ tw, float2* __restrict__ CA, int ca_pitch) {
   constexpr int T = fft_threads_c(P);
   constexpr int NT = T * RB;
@@ -754,34 +779,33 @@ rows_fwd_kernel(const GridGeom* __restrict__ geom, float* __restrict__ C, int cp
   pdl_wait();
   pdl_trigger();
   const int M = geom->M;
-  const int p0 = blockIdx.x * RB;  // first row pair of the block
+  // the three channel blocks of a row group are adjacent in launch order: they read the
+  // same interleaved charge sectors close together in time (L2 hits)
+  const int ch = blockIdx.x % 3;
+  const int p0 = (blockIdx.x / 3) * RB;  // first row pair of the block
   if (2 * p0 >= M) return;
   const int g = threadIdx.x / T, lt = threadIdx.x - g * T;
   const int ra = 2 * (p0 + g), rb = ra + 1;
   const bool ha = ra < M, hb = rb < M;
-  const int ch = blockIdx.y;
   float2* a = sm + g * PL;
-  float* rowa = C + ((int64_t)ch * cpitch + ra) * cpitch;
-  float* rowb = rowa + cpitch;
+  // channel ch of the interleaved charges (stride 4 floats; the three channel blocks of a
+  // row pair read the same sectors, from L2)
+  const float* rowa = reinterpret_cast<const float*>(C + (int64_t)ra * cpitch) + ch;
+  const float* rowb = rowa + 4 * (int64_t)cpitch;
   constexpr int half = P / 2;
 #pragma unroll
   for (int x = lt; x < half; x += T) {  // [P/2, P) is zero and never read
     float va = 0.f, vb = 0.f;
     if (x < M) {
-      if (ha) va = __ldcs(rowa + x);  // read once: evict-first
-      if (hb) vb = __ldcs(rowb + x);
+      if (ha) va = rowa[4 * x];
+      if (hb) vb = rowb[4 * x];
     }
     a[pad(x)] = make_float2(va, vb);
-  }
-  // consumed: leave the planes zero for the next spread (stores issued after all loads)
-  for (int x = lt; x < M; x += T) {
-    if (ha) rowa[x] = 0.f;
-    if (hb) rowb[x] = 0.f;
   }
   __syncthreads();
   fft_smem<T, P, kZeroUpper>(a, tws, lt);
   const int rows_here = min(2 * RB, M - 2 * p0);
-  float2* out = CA + (int64_t)ch * (half + 1) * ca_pitch + 2 * p0;
+  constexpr int H = half + 1;
   for (int f = threadIdx.x; f < (half + 1) * RB; f += NT) {
     const int q = f / RB, gg = f - q * RB;
     if (2 * gg >= rows_here) continue;
@@ -790,7 +814,7 @@ rows_fwd_kernel(const GridGeom* __restrict__ geom, float* __restrict__ C, int cp
     const float2 zc = conjf2(ag[pad(q == 0 ? 0 : P - q)]);
     const float2 xa = make_float2(0.5f * (z.x + zc.x), 0.5f * (z.y + zc.y));
     const float2 xb = mul_mi(make_float2(0.5f * (z.x - zc.x), 0.5f * (z.y - zc.y)));
-    float2* o = out + (int64_t)q * ca_pitch + 2 * gg;
+    float2* o = CA + ca_col_base(ch, q, H, ca_pitch) + ca_row_off(2 * p0 + 2 * gg, H);
     if (2 * gg + 1 < rows_here) *reinterpret_cast<float4*>(o) = make_float4(xa.x, xa.y, xb.x, xb.y);
     else *o = xa;
   }
@@ -802,7 +826,8 @@ rows_fwd_kernel(const GridGeom* __restrict__ geom, float* __restrict__ C, int cp
 template <int P, int RB>
 __global__ void __launch_bounds__(fft_threads_c(P) * RB, (rows_min_blocks<P, RB>()))
 rows_inv_kernel(const GridGeom* __restrict__ geom, const float2* __restrict__ CA, int ca_pitch,
-                const float2* __restrict__ tw, float* __restrict__ Phi, int cpitch) {
+                const float2* __restrict__ tw, float* __restrict__ Phi, int cpitch,
+                float4* __restrict__ C) {
   constexpr int T = fft_threads_c(P);
   constexpr int NT = T * RB;
   constexpr int PL = padded_len(P);
@@ -812,19 +837,19 @@ rows_inv_kernel(const GridGeom* __restrict__ geom, const float2* __restrict__ CA
   pdl_wait();
   pdl_trigger();
   const int M = geom->M;
-  const int p0 = blockIdx.x * RB;
+  const int ch = blockIdx.x % 3;  // channel blocks of a row group adjacent (as rows_fwd)
+  const int p0 = (blockIdx.x / 3) * RB;
   if (2 * p0 >= M) return;
-  const int ch = blockIdx.y;
   const int rows_here = min(2 * RB, M - 2 * p0);
   constexpr int half = P / 2;
-  const float2* in = CA + (int64_t)ch * (half + 1) * ca_pitch + 2 * p0;
+  constexpr int H = half + 1;
   // Z[q] = Xa[q] + i Xb[q] over the full circle (Hermitian extension), stored conjugated so
   // that the forward FFT computes the inverse.
 #pragma unroll 4
   for (int f = threadIdx.x; f < (half + 1) * RB; f += NT) {
     const int q = f / RB, gg = f - q * RB;
     float2 xa = make_float2(0.f, 0.f), xb = make_float2(0.f, 0.f);
-    const float2* p = in + (int64_t)q * ca_pitch + 2 * gg;
+    const float2* p = CA + ca_col_base(ch, q, H, ca_pitch) + ca_row_off(2 * p0 + 2 * gg, H);
     if (2 * gg + 1 < rows_here) {
       const float4 v = *reinterpret_cast<const float4*>(p);
       xa = make_float2(v.x, v.y);
@@ -836,6 +861,15 @@ rows_inv_kernel(const GridGeom* __restrict__ geom, const float2* __restrict__ CA
     ag[pad(q)] = conjf2(make_float2(xa.x - xb.y, xa.y + xb.x));  // conj(xa + i xb)
     if (q > 0 && q < half)  // mirror P - q: conj(conj(xa) + i conj(xb))
       ag[pad(P - q)] = make_float2(xa.x + xb.y, xa.y - xb.x);
+  }
+  // rows_fwd (a previous kernel) consumed these charge rows: leave them zero for the next
+  // spread, the three channel blocks of the row group taking a third of the columns each
+  // (measured cheaper than zeroing in rows_fwd after its last channel block or in cols)
+  {
+    const int x0 = ch * M / 3, x1 = (ch + 1) * M / 3;
+    float4* c0 = C + (int64_t)(2 * p0) * cpitch;
+    for (int r = 0; r < rows_here; ++r)
+      for (int x = x0 + threadIdx.x; x < x1; x += NT) c0[(int64_t)r * cpitch + x] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
   __syncthreads();
   const int g = threadIdx.x / T, lt = threadIdx.x - g * T;
@@ -944,7 +978,7 @@ void launch_kspec(const GridGeom* geom, int P, int Mcap, ForceArgs fa, const flo
   {                                                                                           \
     const int rb = rows_rb(S);                                                                \
     const size_t smb = rows_smem_bytes(S, rb);                                                \
-    const dim3 grid((unsigned)(((Mcap + 1) / 2 + rb - 1) / rb), 3);                           \
+    const dim3 grid((unsigned)(3 * (((Mcap + 1) / 2 + rb - 1) / rb)));                        \
     if (rb == 4) {                                                                            \
       if constexpr (fft_threads_c(S) * 4 <= 1024)                                             \
         launch_chained(KERN<S, 4>, grid, fft_threads_c(S) * 4, smb, s, __VA_ARGS__);          \
@@ -956,7 +990,7 @@ void launch_kspec(const GridGeom* geom, int P, int Mcap, ForceArgs fa, const flo
     }                                                                                         \
   }
 
-void launch_rows_fwd(const GridGeom* geom, float* C, int cpitch, int P, int Mcap,
+void launch_rows_fwd(const GridGeom* geom, const float4* C, int cpitch, int P, int Mcap,
                      const float2* tw, float2* CA, int ca_pitch, cudaStream_t s) {
 #define TFDP_RF(S)                                                                          \
   case S:                                                                                   \
@@ -979,10 +1013,10 @@ void launch_cols(const GridGeom* geom, float2* CA, int ca_pitch, const float* KH
 }
 
 void launch_rows_inv(const GridGeom* geom, const float2* CA, int ca_pitch, int P, int Mcap,
-                     const float2* tw, float* Phi, int cpitch, cudaStream_t s) {
+                     const float2* tw, float* Phi, int cpitch, float4* C, cudaStream_t s) {
 #define TFDP_RI(S)                                                                          \
   case S:                                                                                   \
-    TFDP_ROWS_DISPATCH(S, aos::rows_inv_kernel, geom, CA, ca_pitch, tw, Phi, cpitch)        \
+    TFDP_ROWS_DISPATCH(S, aos::rows_inv_kernel, geom, CA, ca_pitch, tw, Phi, cpitch, C)        \
     break;
   switch (P) { TFDP_FFT_SIZES(TFDP_RI) default: break; }
 #undef TFDP_RI

@@ -104,8 +104,9 @@ void launch_box_reduce(BoxKeys* slots, int n_part, BoxKeys* keys, cudaStream_t s
 void launch_setup(BoxKeys* slots, int n_part, BoxKeys* keys, GridGeom* geom, int k,
                   int n_int_min, int n_int_fixed, int n_int_cap, int P, int pitch,
                   int* capped_flag, cudaStream_t s);
+// charges: float4 {C_1, C_x~, C_y~, 0} per grid node, row pitch = GridGeom::pitch float4s
 void launch_spread(const float2* xy, int64_t lo, int64_t cnt, const GridGeom* geom, int k,
-                   float* grid, cudaStream_t s);
+                   float4* grid, cudaStream_t s);
 
 // hand-written FFT convolution (kernels_fftconv.cu)
 bool fft_size_supported(int P);  // P = 256 q, q = 2^a 3^b 5^c (b <= 2, c <= 1), P <= 8192
@@ -113,12 +114,13 @@ cudaError_t fftconv_prepare(int P);
 void launch_twiddles(float2* tw, int P, cudaStream_t s);
 void launch_kspec(const GridGeom* geom, int P, int Mcap, ForceArgs fa, const float2* tw,
                   float* KA, int ka_pitch, float* KH, cudaStream_t s);
-void launch_rows_fwd(const GridGeom* geom, float* C, int cpitch, int P, int Mcap,
+void launch_rows_fwd(const GridGeom* geom, const float4* C, int cpitch, int P, int Mcap,
                      const float2* tw, float2* CA, int ca_pitch, cudaStream_t s);
 void launch_cols(const GridGeom* geom, float2* CA, int ca_pitch, const float* KH, int P,
                  const float2* tw, cudaStream_t s);
+// rows_inv also re-zeroes the charge rows [0, M) x [0, M) of C (consumed by rows_fwd)
 void launch_rows_inv(const GridGeom* geom, const float2* CA, int ca_pitch, int P, int Mcap,
-                     const float2* tw, float* Phi, int cpitch, cudaStream_t s);
+                     const float2* tw, float* Phi, int cpitch, float4* C, cudaStream_t s);
 // internal node renumbering (kernels_reorder.cu)
 size_t reorder_scratch_bytes(int64_t n);
 void launch_iota(int* perm, int* inv, int64_t n, cudaStream_t s);
