@@ -546,7 +546,9 @@ tfdp_status evaluate(tfdp_ctx* c, int update, float eta, int k) {
     }
     {
       Scope sc(c, K_KSPEC, ks, 2);  // kspec_rows + kspec_cols
+#ifndef TFDP_DEV_SKIP_KSPEC  // developer timing experiment only (stale K^: wrong forces)
       tfdp::launch_kspec(c->geom, P, mcap, c->fa, tw, c->ka, c->cpitch, c->kh, ks);
+#endif
     }
     if (overlap) CUDA_TRY(c, cudaEventRecord(c->ev_join, c->side));
     // The charges are all-zero here: they start zeroed and rows_inv clears the rows rows_fwd

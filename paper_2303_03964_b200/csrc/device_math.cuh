@@ -78,24 +78,16 @@ __device__ __forceinline__ float2 attraction_sum(const float2* __restrict__ xy, 
     sx = fmaf(c, dx, sx);
     sy = fmaf(c, dy, sy);
   };
-#ifndef TFDP_COL_STREAM
-#define TFDP_COL_STREAM 0
-#endif
-#if TFDP_COL_STREAM
-  // column indices are a once-per-iteration stream: evict-first, keep L1 for the positions
-  auto ldc = [](const int32_t* p) { return __ldcs(p); };
-#else
-  auto ldc = [](const int32_t* p) { return __ldg(p); };
-#endif
   for (; e + 4 <= e1; e += 4) {
-    const int j0 = ldc(col + e), j1 = ldc(col + e + 1), j2 = ldc(col + e + 2), j3 = ldc(col + e + 3);
+    const int j0 = __ldg(col + e), j1 = __ldg(col + e + 1), j2 = __ldg(col + e + 2),
+              j3 = __ldg(col + e + 3);
     const float2 x0 = __ldg(xy + j0), x1 = __ldg(xy + j1), x2 = __ldg(xy + j2), x3 = __ldg(xy + j3);
     term(x0);
     term(x1);
     term(x2);
     term(x3);
   }
-  for (; e < e1; ++e) term(__ldg(xy + ldc(col + e)));
+  for (; e < e1; ++e) term(__ldg(xy + __ldg(col + e)));
   return make_float2(sx, sy);
 }
 
