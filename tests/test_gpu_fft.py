@@ -196,3 +196,25 @@ def test_internal_node_order_is_invisible():
     ulp = np.spacing(np.maximum(np.abs(w.xy), np.abs(out["auto"][2])).astype(np.float32))
     bound = np.linalg.norm(8 * 0.5 * ulp.astype(np.float64)) / np.linalg.norm(do)
     assert O.rel_l2(da, do) <= bound + 1e-3, bound
+
+
+def test_charges_cleared_between_evaluations():
+    """The interleaved charge grid is re-zeroed by every evaluation (rows_inv), whatever k:
+    repeated force calls, and calls after the dynamic schedule switched k (18/1/1 at T = 20,
+    P:545), match a fresh context on the same layout — leftover charges would add up."""
+    w, rp, col = _case("C2rgg")
+    with P.Layout(w.n, rp, col, w.xy, P.Params(solver="ibfft", k=0, iterations=20)) as L:
+        R1, _ = L.forces()
+        R1b, _ = L.forces()
+        assert O.rel_l2(R1b, R1) <= 1e-5  # fp32 atomics order only (R15)
+        L.step(18)  # k = 1 iterations; the next one is k = 2
+        X = L.layout()
+        R2, _ = L.forces()
+        R2b, _ = L.forces()
+        L.step(1)
+        X3 = L.layout()
+        R3, _ = L.forces()
+    for Xs, Rs, k in ((X, R2, 2), (X, R2b, 2), (X3, R3, 3)):
+        Rf, _, _ = _fft_forces(w.n, rp, col, Xs, k)
+        assert O.rel_l2(Rs, Rf) <= 1e-5, k
+    assert O.rel_l2(R1, O.repulsion_ibfft(w.xy.astype(np.float64), 1)) <= TOL_IB
