@@ -215,7 +215,10 @@ def test_charges_cleared_between_evaluations():
         L.step(1)
         X3 = L.layout()
         R3, _ = L.forces()
+    # the fresh context plans its FFT size from the moved layout (R9: any P >= 2M - 1 gives
+    # the same kept outputs up to fp32 rounding, measured 1e-5); leftover charges would
+    # shift the forces by O(1)
     for Xs, Rs, k in ((X, R2, 2), (X, R2b, 2), (X3, R3, 3)):
         Rf, _, _ = _fft_forces(w.n, rp, col, Xs, k)
-        assert O.rel_l2(Rs, Rf) <= 1e-5, k
+        assert O.rel_l2(Rs, Rf) <= 1e-4, k
     assert O.rel_l2(R1, O.repulsion_ibfft(w.xy.astype(np.float64), 1)) <= TOL_IB

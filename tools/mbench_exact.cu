@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 constexpr int TPB = 256, TILE = 1024;
+using u64 = unsigned long long;
 
 __device__ __forceinline__ float rcp_approx(float x) {
   float r;
@@ -160,6 +161,82 @@ __global__ void __launch_bounds__(TPB) v2(const float2* __restrict__ xy, int n, 
   }
 }
 
+// V3: as V2 (unpaired), but one source pair in every NE uses an FMA-pipe reciprocal:
+// -y0 from an integer magic (one 64-bit subtract on the packed bits, no borrow since
+// bits(s) < magic for s >= 1), then a cubic and a quadratic Newton step on the negated
+// iterate (5 FFMA2, rel. error ~4e-6), moving work from the MUFU pipe to the FMA pipe.
+__device__ __forceinline__ u64 rcp_neg_newton2(u64 s) {
+  const u64 one = pk(1.f, 1.f);
+  u64 z = 0xFEF311C3FEF311C3ull - s;  // -y0 per lane (sign bit set by the magic)
+  u64 e = fma2(s, z, one);            // 1 - s y0
+  u64 t = fma2(e, e, e);              // e + e^2
+  z = fma2(z, t, z);                  // -(y0 (1 + e + e^2))
+  e = fma2(s, z, one);
+  z = fma2(z, e, z);                  // -y2
+  return z;
+}
+template <int TPT, int NE>
+__global__ void __launch_bounds__(TPB) v3(const float2* __restrict__ xy, int n, float2* out) {
+  __shared__ float xs[TILE], ys[TILE];
+  u64 tx[TPT], ty[TPT], ax[TPT], ay[TPT];
+  for (int r = 0; r < TPT; ++r) {
+    float2 p = xy[(blockIdx.x * TPB * TPT + threadIdx.x + r * TPB) % n];
+    tx[r] = pk(p.x, p.x); ty[r] = pk(p.y, p.y); ax[r] = ay[r] = pk(0.f, 0.f);
+  }
+  const u64 one = pk(1.f, 1.f);
+  for (int base = 0; base < n; base += TILE) {
+    __syncthreads();
+    for (int j = threadIdx.x; j < TILE; j += TPB) {
+      const float2 p = xy[base + j];
+      xs[j] = p.x; ys[j] = p.y;
+    }
+    __syncthreads();
+    for (int j0 = 0; j0 < TILE; j0 += 2 * NE) {
+#pragma unroll
+      for (int jj = 0; jj < NE; ++jj) {
+        const int j = j0 + 2 * jj;
+        const u64 qx = *reinterpret_cast<const u64*>(xs + j);
+        const u64 qy = *reinterpret_cast<const u64*>(ys + j);
+#pragma unroll
+        for (int r = 0; r < TPT; ++r) {
+          const u64 dx = sub2(tx[r], qx), dy = sub2(ty[r], qy);
+          const u64 s = fma2(dy, dy, fma2(dx, dx, one));
+          u64 w;
+          if (jj == NE - 1) {
+            w = rcp_neg_newton2(s);
+          } else {
+            float s1, s2;
+            upk(s, s1, s2);
+            w = pk(rcp_approx(s1), rcp_approx(s2));
+          }
+          const u64 q2 = mul2(w, w);
+          ax[r] = fma2(q2, dx, ax[r]);
+          ay[r] = fma2(q2, dy, ay[r]);
+        }
+      }
+    }
+  }
+  for (int r = 0; r < TPT; ++r) {
+    float a1, a2, b1, b2;
+    upk(ax[r], a1, a2);
+    upk(ay[r], b1, b2);
+    out[blockIdx.x * TPB * TPT + threadIdx.x + r * TPB] = make_float2(a1 + a2, b1 + b2);
+  }
+}
+
+__global__ void check_newton(float* out) {
+  float worst = 0.f, at = 0.f;
+  for (float s = 1.0f; s < 1e7f; s *= 1.0001f) {
+    float a, b;
+    upk(rcp_neg_newton2(pk(s, s * 1.37f)), a, b);
+    const float ea = fabsf(-a * s - 1.0f), eb = fabsf(-b * (s * 1.37f) - 1.0f);
+    if (ea > worst) { worst = ea; at = s; }
+    if (eb > worst) { worst = eb; at = s * 1.37f; }
+  }
+  out[0] = worst;
+  out[1] = at;
+}
+
 template <typename K>
 double run(K kern, int grid, const float2* xy, int n, float2* out, const char* name, int tpt) {
   cudaEvent_t a, b;
@@ -196,5 +273,19 @@ int main() {
   run(v2<4, true>, grid4, xy, n, out, "v2 paired tpt4", 4);
   run(v2<8, false>, grid4 / 2, xy, n, out, "v2 f32x2(jj) tpt8", 8);
   run(v2<8, true>, grid4 / 2, xy, n, out, "v2 paired tpt8", 8);
+  run(v3<4, 16>, grid4, xy, n, out, "v3 newton 1/16 tpt4", 4);
+  run(v3<4, 12>, grid4, xy, n, out, "v3 newton 1/12 tpt4", 4);
+  run(v3<4, 8>, grid4, xy, n, out, "v3 newton 1/8 tpt4", 4);
+  run(v3<4, 6>, grid4, xy, n, out, "v3 newton 1/6 tpt4", 4);
+  run(v3<4, 4>, grid4, xy, n, out, "v3 newton 1/4 tpt4", 4);
+  run(v3<4, 1>, grid4, xy, n, out, "v3 newton all tpt4", 4);
+  {  // accuracy of the Newton reciprocal over s in [1, 1e7]
+    float* d;
+    cudaMalloc(&d, 2 * sizeof(float));
+    check_newton<<<1, 1>>>(d);
+    float h2[2];
+    cudaMemcpy(h2, d, sizeof(h2), cudaMemcpyDeviceToHost);
+    printf("newton rcp max rel err over s in [1, 1e7]: %.3e (at s = %.6g)\n", h2[0], h2[1]);
+  }
   return 0;
 }
