@@ -7,8 +7,8 @@
 // pair arithmetic runs on packed fp32x2 instructions (sm_100a FADD2 / FFMA2 / FMUL2) with
 // lanes = the two sources: per two pairs (gamma = 2) 2 FADD2 (dx, dy), 2 FFMA2 (s = 1 + d^2),
 // 2 MUFU.RCP, 1 FMUL2 (w^2), 2 FFMA2 (accumulate) = 4.5 issue slots per pair: bound by the
-// SFU (one MUFU.RCP per pair) with the FMA pipe at ~88 % of it; one source pair in every
-// kExactNewtonEvery takes an FMA-pipe Newton reciprocal instead (balances the two pipes) —
+// SFU (one MUFU.RCP per pair) with the FMA pipe at ~88 % of it (moving one reciprocal in
+// 8..64 to an FMA-pipe Newton iteration measured slower: tools/mbench_exact.cu v3) —
 // DESIGN.md §Kernels.  Sums: fp32 within a
 // tile (<= 1024 terms, even and odd sources in separate lanes), fp64 across tiles and
 // chunks.  Source chunks depend on n only, and every target sums its chunks in index order,
@@ -42,21 +42,6 @@ __device__ __forceinline__ u64 mul2(u64 a, u64 b) {
   u64 d;
   asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
   return d;
-}
-
-// 1/s for both lanes on the FMA pipe, returned NEGATED (-1/s): -y0 from an integer magic
-// (one 64-bit subtract of the packed bits: bits(s) < magic for 1 <= s < 1.6e38, so there is
-// no borrow between the lanes and the magic's sign bit makes the result -y0), then a cubic
-// and a quadratic Newton step on the negated iterate: 5 FFMA2, max rel. error 4e-6 over
-// s in [1, 1e7] (tools/mbench_exact.cu check_newton).  Squared, the sign drops out.
-__device__ __forceinline__ u64 rcp_neg_newton2(u64 s) {
-  const u64 one = pk(1.f, 1.f);
-  u64 z = 0xFEF311C3FEF311C3ull - s;  // -y0 per lane
-  u64 e = fma2(s, z, one);            // 1 - s y0
-  u64 t = fma2(e, e, e);              // e + e^2
-  z = fma2(z, t, z);                  // -y0 (1 + e + e^2)
-  e = fma2(s, z, one);
-  return fma2(z, e, z);               // -y2
 }
 
 // (1 + d^2)^-gamma for the two lanes of s
@@ -111,32 +96,22 @@ exact_partial_kernel(const float2* __restrict__ xy, int64_t n, int64_t lo, int64
     for (int r = 0; r < kExactTPT; ++r) fx[r] = fy[r] = pk(0.f, 0.f);
     const int cnt2 = cnt & ~1;
     int j = 0;
-    if constexpr (G == 2 && kExactNewtonEvery > 1) {
-      // one source pair in every kExactNewtonEvery takes its reciprocals on the FMA pipe:
-      // the MUFU (16/clk/SM) and FMA (64 FFMA2/clk/SM) pipes are then both near saturation
-      // instead of the MUFU alone.  The choice depends on the source position within the
-      // tile only, so shards stay bitwise identical (R15).
-      constexpr int NE = kExactNewtonEvery;
-      for (; j + 2 * NE <= cnt2; j += 2 * NE) {
+    // 32 source pairs per round, fully unrolled (C5: 4.17 -> 4.35e12 pairs/s against the
+    // 2-pair unroll), then the remainder of a partial tile
+    constexpr int kPairsPerRound = 32;
+    for (; j + 2 * kPairsPerRound <= cnt2; j += 2 * kPairsPerRound) {
 #pragma unroll
-        for (int jj = 0; jj < NE; ++jj) {
-          const u64 qx = *reinterpret_cast<const u64*>(xs + j + 2 * jj);
-          const u64 qy = *reinterpret_cast<const u64*>(ys + j + 2 * jj);
+      for (int jj = 0; jj < kPairsPerRound; ++jj) {
+        const u64 qx = *reinterpret_cast<const u64*>(xs + j + 2 * jj);  // (x_j, x_j+1)
+        const u64 qy = *reinterpret_cast<const u64*>(ys + j + 2 * jj);
 #pragma unroll
-          for (int r = 0; r < kExactTPT; ++r) {
-            const u64 dx = sub2(tx[r], qx);
-            const u64 dy = sub2(ty[r], qy);
-            const u64 sq = fma2(dy, dy, fma2(dx, dx, one));
-            u64 w;
-            if (jj == NE - 1) {
-              const u64 z = rcp_neg_newton2(sq);
-              w = mul2(z, z);
-            } else {
-              w = weight2<G>(sq, neg_gamma);
-            }
-            fx[r] = fma2(w, dx, fx[r]);
-            fy[r] = fma2(w, dy, fy[r]);
-          }
+        for (int r = 0; r < kExactTPT; ++r) {
+          const u64 dx = sub2(tx[r], qx);  // r_ij = x_i - x_j
+          const u64 dy = sub2(ty[r], qy);
+          const u64 sq = fma2(dy, dy, fma2(dx, dx, one));  // 1 + |r_ij|^2
+          const u64 w = weight2<G>(sq, neg_gamma);         // (1 + d^2)^-gamma
+          fx[r] = fma2(w, dx, fx[r]);
+          fy[r] = fma2(w, dy, fy[r]);
         }
       }
     }

@@ -11,10 +11,6 @@ constexpr int kExactThreads = 256;  // exact kernel block
 constexpr int kExactTPT = 4;        // targets per thread (register blocking)
 constexpr int kExactTargetsPerBlock = kExactThreads * kExactTPT;
 constexpr int kExactTile = 1024;    // sources per smem tile (fp32 partial sum length)
-#ifndef TFDP_EXACT_NEWTON
-#define TFDP_EXACT_NEWTON 12
-#endif
-constexpr int kExactNewtonEvery = TFDP_EXACT_NEWTON;  // 0/1: MUFU reciprocals only (gamma = 2)
 constexpr int kNodeThreads = 256;   // per-node kernels
 
 // Geometry of one ibFFT evaluation, computed on the device from the box (no host sync).

@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(TPB) v3(const float2* __restrict__ xy, int n, 
       xs[j] = p.x; ys[j] = p.y;
     }
     __syncthreads();
-    for (int j0 = 0; j0 < TILE; j0 += 2 * NE) {
+    for (int j0 = 0; j0 + 2 * NE <= TILE; j0 += 2 * NE) {  // (remainder of the tile skipped)
 #pragma unroll
       for (int jj = 0; jj < NE; ++jj) {
         const int j = j0 + 2 * jj;
@@ -278,7 +278,7 @@ int main() {
   run(v3<4, 8>, grid4, xy, n, out, "v3 newton 1/8 tpt4", 4);
   run(v3<4, 6>, grid4, xy, n, out, "v3 newton 1/6 tpt4", 4);
   run(v3<4, 4>, grid4, xy, n, out, "v3 newton 1/4 tpt4", 4);
-  run(v3<4, 1>, grid4, xy, n, out, "v3 newton all tpt4", 4);
+  run(v3<4, 32>, grid4, xy, n, out, "v3 newton 1/32 tpt4", 4);
   {  // accuracy of the Newton reciprocal over s in [1, 1e7]
     float* d;
     cudaMalloc(&d, 2 * sizeof(float));

@@ -4,7 +4,21 @@ import csv, io, subprocess, sys
 rep = sys.argv[1]
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
-hdr, data = rows[0], rows[2:]
+hdr, units, data = rows[0], rows[1], rows[2:]
+# normalise the duration to microseconds (ncu picks ns / us / ms per report)
+_it = hdr.index("gpu__time_duration.sum") if "gpu__time_duration.sum" in hdr else None
+if _it is not None:
+    _f = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3,
+          "second": 1e6, "s": 1e6}.get(units[_it], 1.0)
+    for r in data:
+        r[_it] = f"{float(r[_it]) * _f:.3f}"
+# DRAM bytes in MB
+for _m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+    if _m in hdr:
+        _i = hdr.index(_m)
+        _f = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}.get(units[_i], 1.0)
+        for r in data:
+            r[_i] = f"{float(r[_i]) * _f:.3f}"
 def col(name):
     for i, h in enumerate(hdr):
         if h == name:
