@@ -86,7 +86,7 @@ struct tfdp_ctx {
   int nint_cap = 0;
   int P_of_k[4] = {0, 0, 0, 0};
   int cap_of_k[4] = {0, 0, 0, 0};
-  int cpitch = 0;        // pitch of the compact [3][M][M] charge / potential planes
+  int cpitch = 0;        // row pitch of the charges (float4) and the potential planes
   int ca_pitch = 0;      // rows of the half-spectra CA (multiple of 32; kernels_fftconv.cu)
   int64_t alloc_planes = 0, alloc_ca = 0, alloc_ka = 0;
   float* grid = nullptr;  // charges C (spread target): float4 {C_1, C_x~, C_y~, 0} per node
@@ -1018,10 +1018,15 @@ tfdp_status tfdp_set_layout(tfdp_ctx* c, const float* xy) {
   if (!c || !xy) return fail(c, TFDP_ERR_ARG, "NULL argument");
   cudaSetDevice(c->device);
   const bool d = is_device_ptr(xy);
-  if (!d)
-    for (int64_t i = 0; i < 2 * c->n; ++i)
-      if (!std::isfinite(xy[i]))
-        return fail(c, TFDP_ERR_ARG, "layout non-finite at node %lld", (long long)(i / 2));
+  if (!d) {  // argument check on the host buffer, all cores: first non-finite node
+    const int64_t m = 2 * c->n;
+    int64_t first = m;
+#pragma omp parallel for schedule(static) reduction(min : first)
+    for (int64_t i = 0; i < m; ++i)
+      if (!std::isfinite(xy[i]) && i < first) first = i;
+    if (first < m)
+      return fail(c, TFDP_ERR_ARG, "layout non-finite at node %lld", (long long)(first / 2));
+  }
   float2* dst = c->reorder ? c->iobuf : c->xy[c->cur];
   CUDA_TRY(c, cudaMemcpyAsync(dst, xy, c->n * sizeof(float2),
                               d ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->stream));
