@@ -521,7 +521,11 @@ tfdp_status evaluate(tfdp_ctx* c, int update, float eta, int k) {
   } else {
     const int P = c->P_of_k[k];
     const int mcap = c->cap_of_k[k] * k;
-    tfdp::set_pdl_active(P <= tfdp::kPdlMaxFft);
+    static const int pdl_max = [] {  // TFDP_PDL_MAX_FFT overrides the threshold (A/B runs)
+      const char* e = getenv("TFDP_PDL_MAX_FFT");
+      return e ? atoi(e) : tfdp::kPdlMaxFft;
+    }();
+    tfdp::set_pdl_active(P <= pdl_max);
     const float2* tw = c->tw[k];
     if (!c->box_valid || c->world > 1) {
       Scope sc(c, K_BBOX, nullptr, 2);  // reset_slots + bbox
