@@ -763,6 +763,14 @@ __device__ __forceinline__ void fft_smem(float2* buf, const float2* __restrict__
 // contiguous bytes per q (RB = 1: half a sector).
 template <int P, int RB>
 constexpr int rows_min_blocks() {
+  // P = 2048 (k = 1 at C4): a 48-register cap (5 blocks of 2 x 128 threads per SM instead of
+  // 4; 4 B spills) leaves room for the K-spectrum side stream; k = 1 wall 118.6 -> 115.8 us.
+  // 6 blocks (40 registers, 8 B spills) measured 118.9 (tools/rows_ab.sh, profiles/r1_rows_ab.txt).
+#ifdef TFDP_ROWS_MINB2048
+  if (P == 2048) return TFDP_ROWS_MINB2048;
+#else
+  if (P == 2048 && RB == 2) return 5;
+#endif
   return kMinBlocksA<fft_threads_c(P)> / RB > 0 ? kMinBlocksA<fft_threads_c(P)> / RB : 1;
 }
 
