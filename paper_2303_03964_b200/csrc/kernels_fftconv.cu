@@ -771,6 +771,17 @@ constexpr int rows_min_blocks() {
 #else
   if (P == 2048 && RB == 2) return 5;
 #endif
+  // P = 4096 (k = 2): 3 blocks of 2 x 256 threads per SM (40 registers, 12-20 B spills)
+  // instead of 2; k = 2 wall 371.4 -> 354.1 us.  P = 6144 at 4 blocks measured 872 -> 906
+  // (36 B spills), kept at 3 (tools/rows_ab23.sh, profiles/r1_rows_ab23.txt).
+#ifdef TFDP_ROWS_MINB4096
+  if (P == 4096) return TFDP_ROWS_MINB4096;
+#else
+  if (P == 4096 && RB == 2) return 3;
+#endif
+#ifdef TFDP_ROWS_MINB6144
+  if (P == 6144) return TFDP_ROWS_MINB6144;
+#endif
   return kMinBlocksA<fft_threads_c(P)> / RB > 0 ? kMinBlocksA<fft_threads_c(P)> / RB : 1;
 }
 
