@@ -240,18 +240,24 @@ def k_schedule(T: int) -> np.ndarray:
 @dataclasses.dataclass
 class Box:
     lo: np.ndarray  # float32[2]  lower-left corner of the bounding square (R6)
-    L: np.float32  # side of the square (R6)
+    L: np.float32  # span max(span_x, span_y) of the points (R6)
     n_int: int  # intervals per axis (R5)
-    w: np.float32  # interval width L / n_int
-    center: np.ndarray  # float64[2] = lo + L/2 (R11)
+    w: np.float32  # interval width: 1 (R5') or L / n_int (R5)
+    center: np.ndarray  # float64[2] = lo + side/2, side = n_int w (R11)
 
 
-def box_rule(X, n_int_min: int = 50, n_int_fixed: int = 0) -> Box:
+def box_rule(X, n_int_min: int = 50, n_int_fixed: int = 0, rule: str = "unit") -> Box:
     """Bounding square + interval rule.  P:531 divides "[x_min,x_max] x [x_min,x_max]" into
     N_int x N_int intervals; P:540 N_int = max(50, [y_max - y_min]).  Readings: R6 square
-    anchored at (min x, min y) with side L = max(span_x, span_y); R5 bracket = ceil.
+    anchored at (min x, min y), L = max(span_x, span_y); R5 bracket = ceil.
+    rule = "unit" (reading R5', the default): when the span sets the count (ceil L >=
+    n_int_min) the N_int intervals have unit width, w = 1, and the square has side
+    N_int >= L; otherwise (N_int = n_int_min, or n_int_fixed) the N_int intervals divide
+    the span, w = L / N_int.  rule = "span" (reading R5): always w = L / N_int.
     R19: lo, L, w are computed in fp32 (the kernel's precision) because they decide the
     integer interval index; degenerate L = 0 -> unit square centred on the point."""
+    if rule not in ("unit", "span"):
+        raise ValueError("rule is 'unit' (R5') or 'span' (R5)")
     X32 = np.asarray(X, dtype=np.float32)
     mn = X32.min(0)
     mx = X32.max(0)
@@ -261,9 +267,15 @@ def box_rule(X, n_int_min: int = 50, n_int_fixed: int = 0) -> Box:
     if L == np.float32(0.0):
         lo = (mn - np.float32(0.5)).astype(np.float32)
         L = np.float32(1.0)
-    n_int = int(n_int_fixed) if n_int_fixed > 0 else max(int(n_int_min), int(math.ceil(float(L))))
-    w = np.float32(L / np.float32(n_int))  # IEEE fp32 division
-    center = lo.astype(np.float64) + 0.5 * np.float64(L)
+    cl = int(math.ceil(float(L)))
+    n_int = int(n_int_fixed) if n_int_fixed > 0 else max(int(n_int_min), cl)
+    if rule == "unit" and n_int_fixed <= 0 and cl >= n_int_min:
+        w = np.float32(1.0)  # R5': unit-width intervals, side N_int
+        side = float(n_int)
+    else:
+        w = np.float32(L / np.float32(n_int))  # IEEE fp32 division
+        side = float(L)
+    center = lo.astype(np.float64) + 0.5 * side
     return Box(lo=lo, L=L, n_int=n_int, w=w, center=center)
 
 
@@ -373,7 +385,7 @@ def gather(Phi, X, box: Box, k: int):
 
 def repulsion_ibfft(X, k: int, gamma: float = 2.0, rho: float = 1.0, n_int_min: int = 50,
                     n_int_fixed: int = 0, P: int | None = None, backend: str = "fft",
-                    kernel=None, return_info: bool = False):
+                    kernel=None, return_info: bool = False, rule: str = "unit"):
     """ibFFT repulsion.  F^r(i) = x_i psi_1(i) - psi_x(i)
     (P:465 Eq. repfK, P:474-475 Eqs. Fr1/Fr2) with the three kernel sums of Eq.
     kernelproduct approximated by spread -> grid convolution -> gather.
@@ -382,7 +394,7 @@ def repulsion_ibfft(X, k: int, gamma: float = 2.0, rho: float = 1.0, n_int_min: 
     if k not in (1, 2, 3):
         raise ValueError("k in {1,2,3}")
     X = np.asarray(X, dtype=np.float64)
-    box = box_rule(X, n_int_min, n_int_fixed)
+    box = box_rule(X, n_int_min, n_int_fixed, rule)
     M = box.n_int * k
     h = float(box.w) / k
     K = kernel_tdist(gamma) if kernel is None else kernel
@@ -400,12 +412,13 @@ def repulsion_ibfft(X, k: int, gamma: float = 2.0, rho: float = 1.0, n_int_min: 
 # Runner
 # ---------------------------------------------------------------------------------------
 def forces(X, row_ptr, col, p: Params = Params(), solver: str = "exact", k: int = 3,
-           n_int_min: int = 50, n_int_fixed: int = 0, P: int | None = None):
+           n_int_min: int = 50, n_int_fixed: int = 0, P: int | None = None,
+           rule: str = "unit"):
     """(R, A) for either repulsion path."""
     if solver == "exact":
         R = repulsion_exact(X, p.gamma, p.rho)
     elif solver == "ibfft":
-        R = repulsion_ibfft(X, k, p.gamma, p.rho, n_int_min, n_int_fixed, P)
+        R = repulsion_ibfft(X, k, p.gamma, p.rho, n_int_min, n_int_fixed, P, rule=rule)
     else:
         raise ValueError(solver)
     return R, attraction(X, row_ptr, col, p.alpha, p.beta)
@@ -420,10 +433,11 @@ def step(X, row_ptr, col, p: Params, eta_t: float, **kw):
 def run(X0, row_ptr, col, p: Params = Params(), T: int = 300, eta0: float = 0.1,
         t0: int = 0, solver: str = "exact", k: int = 0, n_int_min: int = 50,
         n_int_fixed: int = 0, P: int | None = None, t_end: int | None = None,
-        cooling: str = "linear"):
+        cooling: str = "linear", rule: str = "unit", round_fp32: bool = False):
     """Iterations t = t0 .. t_end-1 (default T-1) of the layout loop.
     k = 0 -> dynamic 90/5/5 schedule; raises on a non-finite position with the
-    iteration and node (S:353)."""
+    iteration and node.  round_fp32: store the positions in fp32 after every update
+    (the device's storage precision, R14) — a diagnostic of the storage rounding alone."""
     if T < 1 or eta0 <= 0:
         raise ValueError("T >= 1 and eta0 > 0")
     X = np.asarray(X0, dtype=np.float64).copy()
@@ -431,7 +445,9 @@ def run(X0, row_ptr, col, p: Params = Params(), T: int = 300, eta0: float = 0.1,
     for t in range(t0, T if t_end is None else t_end):
         kt = int(ks[t]) if k == 0 else k
         X = step(X, row_ptr, col, p, eta(t, T, eta0, cooling), solver=solver, k=kt,
-                 n_int_min=n_int_min, n_int_fixed=n_int_fixed, P=P)
+                 n_int_min=n_int_min, n_int_fixed=n_int_fixed, P=P, rule=rule)
+        if round_fp32:
+            X = X.astype(np.float32).astype(np.float64)
         bad = ~np.isfinite(X).all(1)
         if bad.any():
             raise FloatingPointError(f"diverged at iter {t} node {int(np.argmax(bad))}")

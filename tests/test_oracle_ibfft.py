@@ -140,3 +140,93 @@ def test_layout_level_band_C2():
     ne, nf = O.np1(Xe, rp, col), O.np1(Xf, rp, col)
     assert abs(nf - ne) / ne <= 0.04, (ne, nf)
     assert ne > O.np1(X0, rp, col)  # the run improves neighbourhood preservation
+
+
+# ---------------------------------------------------------------- reading R5' (unit width)
+@pytest.mark.parametrize("side", [0.3, 7.0, 49.6, 50.0, 50.2, 123.4, 1000.7])
+def test_unit_rule_box(side):
+    """R5': N_int = max(50, ceil L) either way; when the span sets the count the
+    intervals have unit width and the square (side N_int >= L) holds every point; below
+    50 intervals the span is divided (w = L / 50, the R5 box)."""
+    X = _uniform(2000, side, 11)
+    X[0], X[1] = (0.0, 0.0), (side, 0.25 * side)
+    u, s = O.box_rule(X, rule="unit"), O.box_rule(X, rule="span")
+    assert u.n_int == s.n_int and u.L == s.L and np.array_equal(u.lo, s.lo)
+    if math.ceil(float(u.L)) >= 50:
+        assert u.w == np.float32(1.0)
+        assert float(u.L) <= u.n_int < float(u.L) + 1.0
+        np.testing.assert_allclose(u.center, u.lo.astype(np.float64) + u.n_int / 2, rtol=0, atol=0)
+    else:
+        assert u.w == s.w and np.array_equal(u.center, s.center)
+    t = ((X.astype(np.float32) - u.lo) / u.w).astype(np.float32)
+    assert t.min() >= 0.0 and t.max() <= u.n_int
+    b, uu = O.interval_coords(X, u)
+    assert b.min() >= 0 and b.max() <= u.n_int - 1 and uu.min() >= 0.0 and uu.max() <= 1.0
+
+
+@pytest.mark.parametrize("k", [1, 2, 3])
+def test_unit_equals_span_on_integer_span(k):
+    """An integer span L >= 50 gives w = L / N_int = 1 under both readings: the same box,
+    centre and forces, bit for bit."""
+    g = np.random.default_rng(12)
+    X = g.integers(0, 64 * 64 + 1, (600, 2)) / 64.0
+    X[0], X[1] = (0.0, 0.0), (64.0, 3.0)
+    a = O.repulsion_ibfft(X, k, rule="unit")
+    b = O.repulsion_ibfft(X, k, rule="span")
+    np.testing.assert_array_equal(a, b)
+
+
+def test_unit_rule_polynomial_exactness_and_translation():
+    """Under R5' with a non-integer span (side N_int > L): K = |D|^2 is reproduced exactly
+    at k = 3 (a wrong width, anchor or centre would break it), and a dyadic shift leaves the
+    forces bit-identical."""
+    X = np.random.default_rng(13).integers(0, 60 * 64 + 33, (300, 2)) / 64.0
+    X[0], X[1] = (0.0, 0.0), (60.5, 60.5)
+    box = O.box_rule(X)
+    assert box.n_int == 61 and box.w == 1.0
+    K2 = lambda dx, dy: dx * dx + dy * dy
+    xt = X - box.center
+    d2 = ((X[:, None, :] - X[None, :, :]) ** 2).sum(-1)
+    psi_exact = np.stack([d2.sum(1), d2 @ xt[:, 0], d2 @ xt[:, 1]])
+    _, info = O.repulsion_ibfft(X, 3, kernel=K2, return_info=True)
+    assert np.abs(info["psi"] - psi_exact).max() / np.abs(psi_exact).max() < 1e-12
+    for k in (1, 3):
+        a = O.repulsion_ibfft(X, k)
+        b = O.repulsion_ibfft(X + np.array([1024.0, -512.0]), k)
+        np.testing.assert_allclose(b, a, rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("k", [1, 2, 3])
+def test_unit_rule_partition_of_unity(k):
+    X = _uniform(500, 130.0, 14)
+    R, info = O.repulsion_ibfft(X, k, kernel=lambda dx, dy: np.ones_like(dx + dy), return_info=True)
+    assert info["box"].w == 1.0
+    xt = X - info["box"].center
+    np.testing.assert_allclose(info["psi"][0], 500.0, rtol=1e-11)
+    np.testing.assert_allclose(R, 500.0 * xt - xt.sum(0), rtol=1e-9, atol=1e-7)
+
+
+def test_unit_rule_accuracy_matches_span():
+    """Unit-width intervals (w = 1) and span-divided ones (w = L / ceil L, here 0.996) are
+    the same approximation up to that width ratio: e_k differ by a few percent at most and
+    keep the order e1 > e2 > e3."""
+    X = _uniform(4000, 120.5, 15)
+    E = O.repulsion_exact(X)
+    eu = [O.rel_l2(O.repulsion_ibfft(X, k, rule="unit"), E) for k in (1, 2, 3)]
+    es = [O.rel_l2(O.repulsion_ibfft(X, k, rule="span"), E) for k in (1, 2, 3)]
+    assert eu[0] > eu[1] > eu[2]
+    for a, b in zip(eu, es):
+        assert abs(a - b) <= 0.1 * b, (eu, es)
+
+
+def test_run_round_fp32_diagnostic():
+    """run(round_fp32=True) (diagnostic of the device's fp32 position storage, R14): every
+    stored position is an fp32 value and the trajectory stays within the accumulated
+    rounding (<= 1/2 ulp per update) of the fp64 one over a few iterations."""
+    w = make_config("C1")
+    rp, col = O.csr_build(w.n, w.u, w.v)
+    X0 = w.xy.astype(np.float64)
+    a = O.run(X0, rp, col, O.Params(), T=300, t_end=3, round_fp32=True)
+    b = O.run(X0, rp, col, O.Params(), T=300, t_end=3)
+    np.testing.assert_array_equal(a, a.astype(np.float32).astype(np.float64))
+    assert np.abs(a - b).max() <= 3 * 4 * np.spacing(np.float32(8.0))
