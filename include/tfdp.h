@@ -33,12 +33,12 @@ extern "C" {
 #define TFDP_VERSION_MAJOR 0
 #define TFDP_VERSION_MINOR 1
 
-typedef struct tfdp_ctx tfdp_ctx; /* opaque; owns all device memory and FFT plans */
+typedef struct tfdp_ctx tfdp_ctx; /* opaque; owns all device memory and FFT buffers */
 
 typedef enum {
   TFDP_OK = 0,
   TFDP_ERR_ARG = 1,         /* invalid argument (see each call)                          */
-  TFDP_ERR_CUDA = 2,        /* CUDA runtime / cuFFT failure                               */
+  TFDP_ERR_CUDA = 2,        /* CUDA runtime failure                                       */
   TFDP_ERR_OOM = 3,         /* device allocation failed                                   */
   TFDP_ERR_DIVERGED = 4,    /* non-finite position after a step; ctx -> errored   */
   TFDP_ERR_STATE = 5,       /* ctx is errored, or iteration t >= T under linear cooling   */
@@ -50,6 +50,7 @@ enum { TFDP_EXACT = 0, TFDP_IBFFT = 1 };                 /* repulsion path (P:45
 enum { TFDP_COOL_LINEAR = 0, TFDP_COOL_CONSTANT = 1 };    /* integrator readings R2 / R2'   */
 enum { TFDP_DIST_SPREAD_ALL = 0, TFDP_DIST_GRID_ALLREDUCE = 1 }; /* FFT path, p > 1 (§8(e)) */
 enum { TFDP_ORDER_AUTO = 0, TFDP_ORDER_KEEP = 1 };        /* internal node renumbering      */
+enum { TFDP_RULE_UNIT = 0, TFDP_RULE_SPAN = 1 };          /* interval width readings R5'/R5 */
 
 /* Warning bits (returned by tfdp_warnings; the call itself returns TFDP_OK). */
 enum {
@@ -80,6 +81,12 @@ typedef struct {
                           in Morton order of the layout (single GPU, n >= 65536) at the start
                           of each tfdp_step call; all inputs/outputs stay in the caller's
                           order.  TFDP_ORDER_KEEP: never renumber                          */
+  int32_t interval_rule; /* TFDP_RULE_UNIT (R5', default): when ceil L >= n_int_min the
+                          N_int = ceil L intervals have unit width (square of side N_int);
+                          the grid spacing h = 1/k is then constant and the kernel spectrum
+                          is recomputed only when P, k or gamma change.  TFDP_RULE_SPAN (R5):
+                          w = L / N_int always (K^ recomputed every iteration).  With
+                          n_int_fixed > 0, or N_int = n_int_min > ceil L, both use L / N_int */
 } tfdp_params;
 
 /* Multi-GPU description: one process per GPU.  nccl_uid = 128 bytes from

@@ -28,7 +28,7 @@ class tfdp_params(C.Structure):
         ("k", C.c_int32), ("n_int_min", C.c_int32), ("n_int_fixed", C.c_int32),
         ("fft_size", C.c_int32), ("step0", C.c_double), ("iterations", C.c_int32),
         ("t0", C.c_int32), ("cooling", C.c_int32), ("dist_mode", C.c_int32),
-        ("node_order", C.c_int32),
+        ("node_order", C.c_int32), ("interval_rule", C.c_int32),
     ]
 
 

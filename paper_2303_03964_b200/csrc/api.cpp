@@ -2,8 +2,8 @@
 //
 // Owns device memory, the per-iteration schedule (k_t, eta_t), the FFT geometry, the NCCL
 // communicator and the CSR/shard indexing.  Every force evaluation is enqueued as sm_100a
-// kernels (kernels_exact.cu, kernels_fft.cu) or cuFFT on the context stream; there is no
-// host compute path.  Citations as in include/tfdp.h.
+// kernels (kernels_exact.cu, kernels_fft.cu, kernels_fftconv.cu) on the context stream;
+// there is no host compute path and no library FFT.  Citations as in include/tfdp.h.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
@@ -81,6 +81,7 @@ struct tfdp_ctx {
   BoxKeys* box_part = nullptr;  // per-block partial boxes (bbox / fused update epilogue)
   int n_part = 0;               // partials written by the last producer
   GridGeom* geom = nullptr;
+  tfdp::KspecKey* kkey = nullptr;  // (P, h, gamma) of the spectrum held in kh (device)
   bool box_valid = false;
   // ibFFT
   int nint_cap = 0;
@@ -312,6 +313,10 @@ tfdp_status validate_params(const tfdp_params* p, uint32_t* warn, std::string* m
     *msg = "unknown dist_mode";
     return TFDP_ERR_ARG;
   }
+  if (p->interval_rule != TFDP_RULE_UNIT && p->interval_rule != TFDP_RULE_SPAN) {
+    *msg = "unknown interval_rule";
+    return TFDP_ERR_ARG;
+  }
   if (p->n_int_min < 1 || p->n_int_fixed < 0 || p->fft_size < 0) {
     *msg = "n_int_min >= 1, n_int_fixed >= 0, fft_size >= 0";
     return TFDP_ERR_ARG;
@@ -430,7 +435,7 @@ tfdp_status configure_fft(tfdp_ctx* c, float L) {
   for (int k = 1; k <= 3; ++k) {
     if (!k_used(c, k)) continue;
     ca = std::max<int64_t>(ca, 3LL * (c->P_of_k[k] / 2 + 1) * capitch);
-    ka = std::max<int64_t>(ka, (int64_t)(c->P_of_k[k] / 2 + 1) * cpitch);
+    ka = std::max<int64_t>(ka, (int64_t)(c->P_of_k[k] / 2 + 1) * (c->P_of_k[k] / 2 + 1));
     kh = std::max<int64_t>(kh, (int64_t)(c->P_of_k[k] / 2 + 2) * c->P_of_k[k]);
   }
   if (planes > c->alloc_planes || ca > c->alloc_ca || ka > c->alloc_ka || kh > c->alloc_kh) {
@@ -453,6 +458,9 @@ tfdp_status configure_fft(tfdp_ctx* c, float L) {
     c->alloc_ca = ca;
     c->alloc_ka = ka;
     c->alloc_kh = kh;
+    // a new kh holds no spectrum (the key also carries P, so a same-buffer re-plan to another
+    // P invalidates itself)
+    CUDA_TRY(c, cudaMemsetAsync(c->kkey, 0, sizeof(tfdp::KspecKey), c->stream));
   }
   c->cpitch = cpitch;
   c->ca_pitch = capitch;
@@ -519,6 +527,9 @@ tfdp_status evaluate(tfdp_ctx* c, int update, float eta, int k) {
                                 c->stream);
     }
   } else {
+    const bool allreduce = c->world > 1 && c->p.dist_mode == TFDP_DIST_GRID_ALLREDUCE;
+    if (allreduce && !c->comm)  // before any charge is spread (the grid stays all-zero)
+      return fail(c, TFDP_ERR_UNSUPPORTED, "grid all-reduce needs an NCCL communicator");
     const int P = c->P_of_k[k];
     const int mcap = c->cap_of_k[k] * k;
     static const int pdl_max = [] {  // TFDP_PDL_MAX_FFT overrides the threshold (A/B runs)
@@ -535,11 +546,13 @@ tfdp_status evaluate(tfdp_ctx* c, int update, float eta, int k) {
     {
       Scope sc(c, K_SETUP);
       tfdp::launch_setup(c->box_part, c->n_part, c->keys, c->geom, k, c->p.n_int_min,
-                         c->p.n_int_fixed, c->cap_of_k[k],
-                         P, c->cpitch, c->capped, c->stream);
+                         c->p.n_int_fixed, c->cap_of_k[k], P, c->cpitch, c->capped,
+                         c->p.interval_rule, c->fa.gamma, c->kkey, c->stream);
     }
     // The kernel spectrum needs only the geometry: fork it onto the side stream so it overlaps
-    // spread + rows_fwd (both latency-bound); cols joins on it.
+    // spread + rows_fwd (both latency-bound); cols joins on it.  Its kernels exit at once
+    // unless setup found the held spectrum stale (a new P, h or gamma: under R5' h = 1/k,
+    // so a run recomputes it when k switches or the grid is re-planned).
     // (in line while kspec itself is being timed, so that its events measure the kernel
     // rather than its wait for SMs)
     const bool overlap = c->kspec_overlap && !((c->prof_mask >> K_KSPEC) & 1u);
@@ -550,14 +563,11 @@ tfdp_status evaluate(tfdp_ctx* c, int update, float eta, int k) {
     }
     {
       Scope sc(c, K_KSPEC, ks, 2);  // kspec_rows + kspec_cols
-#ifndef TFDP_DEV_SKIP_KSPEC  // developer timing experiment only (stale K^: wrong forces)
-      tfdp::launch_kspec(c->geom, P, mcap, c->fa, tw, c->ka, c->cpitch, c->kh, ks);
-#endif
+      tfdp::launch_kspec(c->geom, P, c->fa, tw, c->ka, c->kh, ks);
     }
     if (overlap) CUDA_TRY(c, cudaEventRecord(c->ev_join, c->side));
     // The charges are all-zero here: they start zeroed and rows_inv clears the rows rows_fwd
     // consumed (no separate zeroing pass).
-    const bool allreduce = c->world > 1 && c->p.dist_mode == TFDP_DIST_GRID_ALLREDUCE;
     float4* grid4 = reinterpret_cast<float4*>(c->grid);
     {
       Scope sc(c, K_SPREAD);
@@ -567,12 +577,15 @@ tfdp_status evaluate(tfdp_ctx* c, int update, float eta, int k) {
         tfdp::launch_spread(xy, 0, c->n, c->geom, k, grid4, c->stream);
     }
     if (allreduce) {
-      if (!c->comm)
-        return fail(c, TFDP_ERR_UNSUPPORTED, "grid all-reduce needs an NCCL communicator");
       Scope sc(c, K_COMM);
-      // rows [0, M_cap) of the interleaved charges (they live in [0, M) x [0, M))
-      NCCL_TRY(c, c->nccl->AllReduce(c->grid, c->grid, (size_t)mcap * c->cpitch * 4, ncclFloat,
-                                     ncclSum, c->comm, c->stream));
+      // rows [0, M_cap) of the interleaved charges (they live in [0, M) x [0, M)); a failed
+      // reduction leaves charges in the grid: the context is errored (no zero-grid invariant)
+      ncclResult_t r = c->nccl->AllReduce(c->grid, c->grid, (size_t)mcap * c->cpitch * 4,
+                                          ncclFloat, ncclSum, c->comm, c->stream);
+      if (r != ncclSuccess) {
+        c->errored = true;
+        return fail(c, TFDP_ERR_NCCL, "grid all-reduce: %s", c->nccl->GetErrorString(r));
+      }
     }
     {
       Scope sc(c, K_ROWS_FWD);
@@ -615,6 +628,11 @@ int k_at(const tfdp_ctx* c, int t) {
 // Reads the divergence word, the grid-cap flag and the last grid geometry (the only host
 // sync of a step call).
 tfdp_status check_status(tfdp_ctx* c, bool* capped) {
+  // p > 1: every rank sees the smallest divergence word of all ranks, so that all of them
+  // stop at the same block instead of one blocking in the next exchange
+  if (c->world > 1 && c->comm)
+    NCCL_TRY(c, c->nccl->AllReduce(c->diverge, c->diverge, 1, ncclUint64, ncclMin, c->comm,
+                                   c->stream));
   CUDA_TRY(c, cudaMemcpyAsync(c->h_status, c->diverge, sizeof(unsigned long long),
                               cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaMemcpyAsync(c->h_status + 1, c->capped, sizeof(int), cudaMemcpyDeviceToHost,
@@ -884,6 +902,7 @@ tfdp_status tfdp_init(tfdp_ctx** out, int64_t n, const int64_t* row_ptr, const i
   ALLOC(c->keys, sizeof(BoxKeys));
   ALLOC(c->box_part, tfdp::kBoxSlots * sizeof(BoxKeys));
   ALLOC(c->geom, sizeof(GridGeom));
+  ALLOC(c->kkey, sizeof(tfdp::KspecKey));
   if (cudaMallocHost((void**)&c->h_status, 2 * sizeof(unsigned long long) + sizeof(GridGeom)) !=
       cudaSuccess)
     return bail(fail(c, TFDP_ERR_OOM, "cudaMallocHost failed"));
@@ -1039,6 +1058,9 @@ tfdp_status tfdp_set_layout(tfdp_ctx* c, const float* xy) {
     c->launches++;
   }
   c->box_valid = false;
+  // a new layout may need a larger grid: re-plan now (one bbox + a host sync) rather than
+  // run up to 32 iterations below the N_int rule (R5) before the in-step check
+  if (c->p.solver == TFDP_IBFFT && c->p.n_int_fixed == 0) return replan_from_device(c);
   return TFDP_OK;
 }
 
@@ -1235,6 +1257,7 @@ tfdp_status tfdp_pivot_mds(tfdp_ctx* c, int32_t n_pivots, uint64_t seed, int32_t
   c->box_valid = false;
   if (pivots)
     for (int j = 0; j < p; ++j) pivots[j] = piv[j];
+  if (c->p.solver == TFDP_IBFFT && c->p.n_int_fixed == 0) return replan_from_device(c);  // as set_layout
   return TFDP_OK;
 }
 
@@ -1379,6 +1402,7 @@ void tfdp_destroy(tfdp_ctx* c) {
   cudaFree(c->np_keys);
   cudaFree(c->np_sum);
   cudaFree(c->geom);
+  cudaFree(c->kkey);
   if (c->h_status) cudaFreeHost(c->h_status);
   if (c->comm && c->nccl) c->nccl->CommDestroy(c->comm);
   if (c->side) {

@@ -1,6 +1,7 @@
 // ibFFT path kernels — sm_100a.
 //   bbox          exact fp32 min/max of the positions (ordered-uint keys, block partials)
-//   setup         box -> (lo, L, N_int, w, h, centre) on the device, no host sync (R5/R6/R19)
+//   setup         box -> (lo, L, N_int, w, h, centre) on the device, no host sync
+//                 (R5/R5'/R6/R19); decides whether the kernel spectrum is stale
 //   spread        step 1: Lagrange charges {1, x~, y~} onto the k x k nodes of each
 //                 node's own interval; fp32 v4 reductions into L2
 //   gather_update step 3 + assemble + attraction + update,
@@ -149,7 +150,8 @@ void launch_box_reduce(BoxKeys* part, int n_part, BoxKeys* keys, cudaStream_t s,
 // ------------------------------------------------------------------ setup
 __global__ void __launch_bounds__(64)
 setup_kernel(BoxKeys* part, int n_part, BoxKeys* keys, GridGeom* geom, int k,
-             int n_int_min, int n_int_fixed, int n_int_cap, int P, int pitch, int* capped_flag) {
+             int n_int_min, int n_int_fixed, int n_int_cap, int P, int pitch, int* capped_flag,
+             int rule, float gamma, KspecKey* kkey) {
   pdl_wait();
   pdl_trigger();
   const BoxKeys kb = block_reduce_partials(part, n_part);
@@ -157,7 +159,7 @@ setup_kernel(BoxKeys* part, int n_part, BoxKeys* keys, GridGeom* geom, int k,
   *keys = kb;
   const float mnx = key2f(kb.minx), mny = key2f(kb.miny);
   const float mxx = key2f(kb.maxx), mxy = key2f(kb.maxy);
-  // R6: bounding square anchored at (min x, min y), side L = max(span_x, span_y) (fp32, R19)
+  // R6: bounding square anchored at (min x, min y), L = max(span_x, span_y) (fp32, R19)
   float L = fmaxf(__fsub_rn(mxx, mnx), __fsub_rn(mxy, mny));
   float lox = mnx, loy = mny;
   if (L == 0.0f) {  // all points coincident: unit square centred on them
@@ -167,6 +169,7 @@ setup_kernel(BoxKeys* part, int n_part, BoxKeys* keys, GridGeom* geom, int k,
   }
   int nint;
   int capped = 0;
+  bool unit = false;
   if (n_int_fixed > 0) {
     nint = n_int_fixed;
   } else {
@@ -176,35 +179,44 @@ setup_kernel(BoxKeys* part, int n_part, BoxKeys* keys, GridGeom* geom, int k,
       capped = 1;
     } else {
       nint = max(n_int_min, (int)cl);
+      // R5': the span sets the count -> unit-width intervals, square of side N_int
+      unit = rule == 0 && (int)cl >= n_int_min;
     }
   }
   if (nint > n_int_cap) {
     nint = n_int_cap;
     capped = 1;
+    unit = false;
   }
   GridGeom g;
   g.lo_x = lox;
   g.lo_y = loy;
   g.L = L;
-  g.w = __fdiv_rn(L, (float)nint);
+  g.w = unit ? 1.0f : __fdiv_rn(L, (float)nint);
   g.h = __fdiv_rn(g.w, (float)k);
-  g.cx = __fmaf_rn(0.5f, L, lox);
-  g.cy = __fmaf_rn(0.5f, L, loy);
+  const float side = unit ? (float)nint : L;
+  g.cx = __fmaf_rn(0.5f, side, lox);
+  g.cy = __fmaf_rn(0.5f, side, loy);
   g.n_int = nint;
   g.k = k;
   g.M = nint * k;
   g.P = P;
   g.capped = capped;
   g.pitch = pitch;
+  // K^ = FFT of the periodic kernel samples K(h d): a function of (P, h, gamma) only
+  const KspecKey kk = *kkey;
+  const unsigned hb = __float_as_uint(g.h), gb = __float_as_uint(gamma);
+  g.kspec = !(kk.valid == 1 && kk.P == P && kk.h_bits == hb && kk.gamma_bits == gb);
+  if (g.kspec) *kkey = KspecKey{P, hb, gb, 1};
   *geom = g;
   if (capped) atomicOr(capped_flag, 1);
 }
 
 void launch_setup(BoxKeys* part, int n_part, BoxKeys* keys, GridGeom* geom, int k,
                   int n_int_min, int n_int_fixed, int n_int_cap, int P, int pitch,
-                  int* capped_flag, cudaStream_t s) {
+                  int* capped_flag, int rule, float gamma, KspecKey* kkey, cudaStream_t s) {
   launch_chained(setup_kernel, 1, 64, 0, s, part, n_part, keys, geom, k, n_int_min, n_int_fixed,
-                 n_int_cap, P, pitch, capped_flag);
+                 n_int_cap, P, pitch, capped_flag, rule, gamma, kkey);
 }
 
 // ------------------------------------------------------------------ interval coords

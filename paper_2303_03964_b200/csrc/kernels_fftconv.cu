@@ -2,9 +2,11 @@
 //
 // Replaces a zero-padded P x P 2-D R2C -> x K^ -> C2R by five passes that never transform
 // the zero padding and never store outputs that are discarded:
-//   kspec_rows  K rows dy = 0..M-1 generated on the fly (K is even in x and y, so each row
-//               spectrum is real), four rows per block: KA[q][dy], q = 0..P/2
+//   kspec_rows  K rows dy = 0..P/2 of the periodic kernel generated on the fly (K is even
+//               in x and y, so each row spectrum is real), four rows per block: KA[q][dy]
 //   kspec_cols  four K^ columns per block (real-even): KH[q][u] (real), u = 0..P-1
+//               (both skip unless setup found the held spectrum stale: K^ depends on
+//               (P, h, gamma) only, and h = 1/k is constant under reading R5')
 //   rows_fwd    four charge rows per block, two per complex FFT (a + i b), of one channel of
 //               the interleaved charges, untangled into the half spectra CA[c][q][row] (32
 //               contiguous bytes per q)
@@ -426,62 +428,66 @@ __device__ __forceinline__ float ksample(float s, float neg_gamma, int gi) {
   pdl_trigger();
 
 // ---------------------------------------------------------------- K spectrum: rows
-// four rows dy0..dy0+3 per block: lane A = row dy0 + i row dy0+1, lane B = rows dy0+2, +3;
-// the real-even row spectra (q <= P/2) leave from the last stage
+// The kernel is sampled over the whole periodic P x P range, K(h d(x), h d(y)) with
+// d(x) = x for x <= P/2 and x - P above: the kept outputs of the circular convolution only
+// ever use offsets |d| <= M - 1 (charges and outputs both live in [0, M), P >= 2M - 1, R9),
+// so the other samples are free — and with them K^ depends on (P, h, gamma) alone, not on
+// M: setup decides (geom->kspec) whether the spectrum held in KH is still the right one.
+// four rows dy0..dy0+3 (dy <= P/2; rows P - dy are the same by evenness) per block: lane A =
+// row dy0 + i row dy0+1, lane B = rows dy0+2, +3; the real-even row spectra (q <= P/2) leave
+// from the last stage
 TFDP_FFT_KERNEL(kspec_rows_kernel)(const GridGeom* __restrict__ geom, float neg_gamma, int gi,
-                                   const float2* __restrict__ tw, float* __restrict__ KA,
-                                   int ka_pitch) {
+                                   const float2* __restrict__ tw, float* __restrict__ KA) {
+  if (!geom->kspec) return;  // spectrum of this (P, h, gamma) already in KH
   TFDP_FFT_PROLOGUE
-  const GridGeom g = *geom;
-  const int M = g.M;
+  constexpr int half = P / 2;
+  constexpr int ka_pitch = half + 1;
+  const float h = geom->h;
   const int dy0 = 4 * blockIdx.x;
-  if (dy0 >= M) return;
-  const float h2 = g.h * g.h;
+  if (dy0 > half) return;
+  const float h2 = h * h;
   const float scale = 1.0f / ((float)P * (float)P);
   for (int x = threadIdx.x; x < P; x += T) {
-    const int dx = (x <= M - 1) ? x : ((x >= P - (M - 1)) ? x - P : INT32_MAX);
+    const int dx = x <= half ? x : x - P;
+    const float dx2 = (float)(dx * dx);
     float v[4] = {0.f, 0.f, 0.f, 0.f};
-    if (dx != INT32_MAX) {
-      const float dx2 = (float)(dx * dx);
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int dy = dy0 + c;
-        if (dy < M) v[c] = ksample(fmaf(h2, dx2 + (float)(dy * dy), 1.0f), neg_gamma, gi) * scale;
-      }
+    for (int c = 0; c < 4; ++c) {
+      const int dy = dy0 + c;
+      if (dy <= half) v[c] = ksample(fmaf(h2, dx2 + (float)(dy * dy), 1.0f), neg_gamma, gi) * scale;
     }
     a[pad(x)] = make_float4(v[0], v[2], v[1], v[3]);
   }
   __syncthreads();
   auto dst = [&](int q, C2 z) {  // real-even rows: Re = even row, Im = odd row
-    if (q > P / 2) return;
+    if (q > half) return;
     float* o = KA + (int64_t)q * ka_pitch + dy0;
     const float r4[4] = {z.re.x, z.im.x, z.re.y, z.im.y};
 #pragma unroll
     for (int c = 0; c < 4; ++c)
-      if (dy0 + c < M) o[c] = r4[c];
+      if (dy0 + c <= half) o[c] = r4[c];
   };
   fft_smem<T, P, 0>(a, tws, SmemIO{}, dst);
 }
 
 // ---------------------------------------------------------------- K spectrum: columns
 // four columns q0..q0+3 per block (lane A = q0 + i q0+1, lane B = q0+2 + i q0+3), each the
-// real-even mirror of dy = 0..M-1, read by the first stage; KH written by the last
+// real-even mirror of dy = 0..P/2, read by the first stage; KH written by the last
 TFDP_FFT_KERNEL(kspec_cols_kernel)(const GridGeom* __restrict__ geom,
-                                   const float* __restrict__ KA, int ka_pitch,
-                                   const float2* __restrict__ tw, float* __restrict__ KH) {
+                                   const float* __restrict__ KA, const float2* __restrict__ tw,
+                                   float* __restrict__ KH) {
+  if (!geom->kspec) return;  // (geom was written by setup, before kspec_rows started)
   TFDP_FFT_PROLOGUE
-  const int M = geom->M;
   constexpr int half = P / 2;
+  constexpr int ka_pitch = half + 1;
   const int q0 = 4 * blockIdx.x;
   __syncthreads();  // twiddle table
   auto src = [&](int u) {
-    const int dy = (u <= M - 1) ? u : ((u >= P - (M - 1)) ? P - u : -1);
+    const int dy = u <= half ? u : P - u;
     float v[4] = {0.f, 0.f, 0.f, 0.f};
-    if (dy >= 0) {
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
-        if (q0 + c <= half) v[c] = KA[(int64_t)(q0 + c) * ka_pitch + dy];
-    }
+    for (int c = 0; c < 4; ++c)
+      if (q0 + c <= half) v[c] = KA[(int64_t)(q0 + c) * ka_pitch + dy];
     return C2{make_float2(v[0], v[2]), make_float2(v[1], v[3])};
   };
   auto dst = [&](int u, C2 z) {
@@ -978,15 +984,15 @@ void launch_twiddles(float2* tw, int P, cudaStream_t s) {
   twiddle_kernel<<<(tw_len(P) + 255) / 256, 256, 0, s>>>(tw, P);
 }
 
-void launch_kspec(const GridGeom* geom, int P, int Mcap, ForceArgs fa, const float2* tw,
-                  float* KA, int ka_pitch, float* KH, cudaStream_t s) {
+void launch_kspec(const GridGeom* geom, int P, ForceArgs fa, const float2* tw, float* KA,
+                  float* KH, cudaStream_t s) {
   const size_t sm = fftconv_smem_bytes(P);
 #define TFDP_KS(S)                                                                          \
   case S:                                                                                   \
-    kspec_rows_kernel<S><<<(unsigned)((Mcap + 3) / 4), fft_threads_c(S), sm, s>>>(          \
-        geom, -fa.gamma, fa.gamma_int, tw, KA, ka_pitch);                                   \
+    kspec_rows_kernel<S><<<(unsigned)((S / 2 + 4) / 4), fft_threads_c(S), sm, s>>>(         \
+        geom, -fa.gamma, fa.gamma_int, tw, KA);                                             \
     launch_chained(kspec_cols_kernel<S>, (unsigned)((S / 2 + 4) / 4), fft_threads_c(S), sm, s, \
-                   geom, KA, ka_pitch, tw, KH);                                             \
+                   geom, KA, tw, KH);                                                       \
     break;
   switch (P) { TFDP_FFT_SIZES(TFDP_KS) default: break; }
 #undef TFDP_KS

@@ -26,6 +26,16 @@ struct GridGeom {
   int P;             // FFT size (>= 2M - 1, R9)
   int capped;        // 1 if n_int was clamped to the allocated grid (warning)
   int pitch;         // row pitch (floats) of the compact charge / potential planes
+  int kspec;         // 1: the kernel spectrum must be (re)computed this evaluation
+};
+
+// Key of the kernel spectrum currently held in KH: K^ depends only on (P, h, gamma) (the
+// kernel is sampled over the whole periodic P x P range, kernels_fftconv.cu), so setup
+// compares the new geometry against it and the K-spectrum kernels skip when it matches.
+struct KspecKey {
+  int P;
+  unsigned h_bits, gamma_bits;
+  int valid;
 };
 
 // Box as order-preserving uint keys so atomicMin/atomicMax give the exact fp32 min/max.
@@ -101,9 +111,10 @@ void launch_reset_slots(BoxKeys* slots, cudaStream_t s);
 int launch_bbox(const float2* xy, int64_t n, BoxKeys* slots, cudaStream_t s);  // -> n_part
 void launch_box_reduce(BoxKeys* slots, int n_part, BoxKeys* keys, cudaStream_t s,
                        bool reset = true);
+// rule: 0 = unit-width intervals when ceil L >= n_int_min (R5'), 1 = w = L / N_int (R5)
 void launch_setup(BoxKeys* slots, int n_part, BoxKeys* keys, GridGeom* geom, int k,
                   int n_int_min, int n_int_fixed, int n_int_cap, int P, int pitch,
-                  int* capped_flag, cudaStream_t s);
+                  int* capped_flag, int rule, float gamma, KspecKey* kkey, cudaStream_t s);
 // charges: float4 {C_1, C_x~, C_y~, 0} per grid node, row pitch = GridGeom::pitch float4s
 void launch_spread(const float2* xy, int64_t lo, int64_t cnt, const GridGeom* geom, int k,
                    float4* grid, cudaStream_t s);
@@ -112,8 +123,10 @@ void launch_spread(const float2* xy, int64_t lo, int64_t cnt, const GridGeom* ge
 bool fft_size_supported(int P);  // P = 256 q, q = 2^a 3^b 5^c (b <= 2, c <= 1), P <= 8192
 cudaError_t fftconv_prepare(int P);
 void launch_twiddles(float2* tw, int P, cudaStream_t s);
-void launch_kspec(const GridGeom* geom, int P, int Mcap, ForceArgs fa, const float2* tw,
-                  float* KA, int ka_pitch, float* KH, cudaStream_t s);
+// KA: (P/2 + 1) x (P/2 + 1) floats (pitch P/2 + 1); KH: (P/2 + 1) x P floats.  No-op
+// (early exit) unless geom->kspec.
+void launch_kspec(const GridGeom* geom, int P, ForceArgs fa, const float2* tw, float* KA,
+                  float* KH, cudaStream_t s);
 void launch_rows_fwd(const GridGeom* geom, const float4* C, int cpitch, int P, int Mcap,
                      const float2* tw, float2* CA, int ca_pitch, cudaStream_t s);
 void launch_cols(const GridGeom* geom, float2* CA, int ca_pitch, const float* KH, int P,

@@ -38,6 +38,7 @@ class Params:
     cooling: str = "linear"  # "linear" (R2) | "constant" (R2')
     dist_mode: str = "spread_all"  # "spread_all" | "grid_allreduce"
     node_order: str = "auto"  # "auto" (internal Morton renumbering, ibFFT) | "keep"
+    interval_rule: str = "unit"  # "unit" (R5', unit-width intervals) | "span" (R5)
     dim: int = 2
 
     def to_c(self) -> _L.tfdp_params:
@@ -51,6 +52,7 @@ class Params:
         p.cooling = {"linear": _L.COOL_LINEAR, "constant": _L.COOL_CONSTANT}[self.cooling]
         p.dist_mode = {"spread_all": _L.DIST_SPREAD_ALL, "grid_allreduce": _L.DIST_GRID_ALLREDUCE}[self.dist_mode]
         p.node_order = {"auto": 0, "keep": 1}[self.node_order]
+        p.interval_rule = {"unit": 0, "span": 1}[self.interval_rule]
         return p
 
 

@@ -14,6 +14,7 @@ from .graphs import (  # noqa: F401
     uniform_disc,
     uniform_square,
     random_layout,
+    blob_layout,
     random_graph,
     path_graph,
     two_cluster_graph,

@@ -150,6 +150,16 @@ def random_layout(n: int, seed: int, scale: float = 1.0) -> np.ndarray:
     return (_rng(seed).standard_normal((n, 2)) * scale).astype(np.float32)
 
 
+def blob_layout(n: int, n_blobs: int, sigma: float, side: float, seed: int) -> np.ndarray:
+    """Clustered layout: n points in n_blobs Gaussian clusters (std sigma) with centres
+    uniform in [0, side]^2, random node order — many nodes per unit interval (the shape of
+    a converged layout's dense clusters)."""
+    g = _rng(seed)
+    centres = g.random((n_blobs, 2)) * side
+    which = g.integers(0, n_blobs, n)
+    return (centres[which] + g.standard_normal((n, 2)) * sigma).astype(np.float32)
+
+
 def path_graph(n: int):
     """Path P_n: edges (i, i+1) (SPEC S:365 refinement example P20)."""
     u = np.arange(n - 1, dtype=np.int32)

@@ -15,7 +15,7 @@ TOL = 1e-4
 
 def _case(name):
     w = make_config(name)
-    rp, col = P.csr_build(w.n, w.u, w.v)
+    rp, col = O.csr_build(w.n, w.u, w.v)
     return w, rp, col
 
 
@@ -39,7 +39,7 @@ def test_forces_ragged_sizes(n):
     """Tile / chunk / block tails: n not a multiple of 1024 sources or 1024 targets."""
     X = random_layout(n, n, 3.0 + n ** 0.5 / 2)
     u, v = random_graph(n, 3 * n, n + 1) if n > 1 else (np.zeros(0, np.int32),) * 2
-    rp, col = P.csr_build(n, u, v)
+    rp, col = O.csr_build(n, u, v)
     with P.Layout(n, rp, col, X) as L:
         R, A = L.forces()
     if n == 1:
@@ -57,7 +57,7 @@ def test_forces_parameters(gamma, rho, alpha, beta):
     n = 3000
     X = random_layout(n, 7, 20.0)
     u, v = random_graph(n, 4 * n, 8)
-    rp, col = P.csr_build(n, u, v)
+    rp, col = O.csr_build(n, u, v)
     prm = P.Params(gamma=gamma, rho=rho, alpha=alpha, beta=beta)
     with P.Layout(n, rp, col, X, prm) as L:
         R, A = L.forces()
@@ -73,7 +73,7 @@ def test_coincident_and_isolated_nodes():
     X = random_layout(n, 11, 5.0)
     X[10:20] = X[5]  # coincident cluster
     u, v = random_graph(n, 300, 12)  # many isolated nodes
-    rp, col = P.csr_build(n, u, v)
+    rp, col = O.csr_build(n, u, v)
     with P.Layout(n, rp, col, X) as L:
         R, A = L.forces()
     _check(R, A, X, rp, col)
@@ -95,7 +95,7 @@ def test_virtual_shards_bitwise(world):
     n = 5000
     X = random_layout(n, 21, 15.0)
     u, v = random_graph(n, 5 * n, 22)
-    rp, col = P.csr_build(n, u, v)
+    rp, col = O.csr_build(n, u, v)
     with P.Layout(n, rp, col, X) as L:
         R1, A1 = L.forces()
     for r in range(world):

@@ -8,15 +8,26 @@ import pytest
 
 import oracle as O
 import paper_2303_03964_b200 as P
-from synth import make_config, random_graph, random_layout
+from synth import blob_layout, make_config, random_graph, random_layout
 
 pytestmark = pytest.mark.gpu
 TOL_IB = 1e-3
+# Per-node bars (DESIGN.md §2 "per-node tolerance").  (a) VERDICT r1's measure
+# e_i = |R_i - Ro_i| / (|Ro_i| + med |Ro|) at the 99.9th percentile and the worst node, on
+# the dense (unit-density, clustered, bench-shaped) layouts.  (b) everywhere, the error
+# relative to the two terms whose difference is F_i (R11: F = rho (x~ psi_1 - psi_x~)):
+# c_i = |R_i - Ro_i| / (rho |(|x~_i| psi_1 + |psi_x~|, |y~_i| psi_1 + |psi_y~|)|), the
+# cancellation fp32 can resolve — on sparse layouts (|x~| ~ 500, |F_i| << |x~_i| psi_1)
+# (a) measures that cancellation, not the kernels.
+TOL_NODE_Q = 5e-3
+TOL_NODE_MAX = 2e-2
+TOL_COND_Q = 2e-5
+TOL_COND_MAX = 3e-4
 
 
 def _case(name):
     w = make_config(name)
-    rp, col = P.csr_build(w.n, w.u, w.v)
+    rp, col = O.csr_build(w.n, w.u, w.v)
     return w, rp, col
 
 
@@ -25,6 +36,45 @@ def _fft_forces(w_n, rp, col, X, k, **kw):
         R, A = L.forces()
         geo = L.fft_geometry()
     return R, A, geo
+
+
+def pernode(R, Ro):
+    """(99.9th percentile, max) of e_i = |R_i - Ro_i| / (|Ro_i| + median_j |Ro_j|): a global
+    rel-L2 can hide a handful of wrong nodes (e.g. a mis-assigned interval); this cannot."""
+    a = np.linalg.norm(np.asarray(R, np.float64) - Ro, axis=1)
+    m = np.linalg.norm(Ro, axis=1)
+    e = a / (m + np.median(m))
+    return float(np.quantile(e, 0.999)), float(e.max())
+
+
+def percond(R, Ro, X, info, rho=1.0):
+    """(99.9th percentile, max) of c_i (see above) from the oracle's psi and box."""
+    psi, xt = info["psi"], np.asarray(X, np.float64) - info["box"].center
+    s = rho * np.hypot(np.abs(xt[:, 0] * psi[0]) + np.abs(psi[1]), np.abs(xt[:, 1] * psi[0]) + np.abs(psi[2]))
+    c = np.linalg.norm(np.asarray(R, np.float64) - Ro, axis=1) / s
+    return float(np.quantile(c, 0.999)), float(c.max())
+
+
+def oracle_ib(X, k, **kw):
+    """Oracle ibFFT forces + the info percond needs."""
+    Ro, info = O.repulsion_ibfft(np.asarray(X, np.float64), k, return_info=True, **kw)
+    return Ro, (X, info, kw.get("rho", 1.0))
+
+
+def check_ib(R, Ro, tag="", cond=None, dense=True):
+    """Global rel-L2 <= TOL_IB; per-node (a) on dense layouts; per-node (b) given cond."""
+    if isinstance(Ro, tuple):
+        Ro, cond = Ro
+    e = O.rel_l2(R, Ro)
+    q, mx = pernode(R, Ro)
+    cq, cmx = percond(R, Ro, *cond) if cond else (float("nan"), float("nan"))
+    print(f"[parity] {tag} rel_l2={e:.3e} node_q999={q:.3e} node_max={mx:.3e} "
+          f"cond_q999={cq:.3e} cond_max={cmx:.3e}")
+    assert e <= TOL_IB, (tag, e)
+    if dense:
+        assert q <= TOL_NODE_Q and mx <= TOL_NODE_MAX, (tag, q, mx)
+    if cond:
+        assert cq <= TOL_COND_Q and cmx <= TOL_COND_MAX, (tag, cq, cmx)
 
 
 @pytest.mark.parametrize("name", ["C2", "C2rgg"])
@@ -38,11 +88,10 @@ def test_c2_vs_oracle_ibfft_and_exact(name, k):
     assert np.float32(geo["L"]) == box.L and np.float32(geo["w"]) == box.w
     assert (np.float32(geo["lo"][0]), np.float32(geo["lo"][1])) == (box.lo[0], box.lo[1])
     assert geo["P"] >= 2 * box.n_int * k - 1
-    Ro = O.repulsion_ibfft(X, k)
+    Ro, cond = oracle_ib(X, k)
     Re = O.repulsion_exact(X)
-    e_ib = O.rel_l2(R, Ro)
     e_k = O.rel_l2(Ro, Re)
-    assert e_ib <= TOL_IB, (e_ib, e_k)
+    check_ib(R, Ro, f"{name} k={k}", cond)
     assert O.rel_l2(R, Re) <= e_k + 1e-3
     assert O.rel_l2(A, O.attraction(X, rp, col)) <= 1e-4
 
@@ -53,7 +102,7 @@ def test_fixed_grid_and_fft_size(k):
     n = 4000
     X = random_layout(n, 31, 8.0)
     u, v = random_graph(n, 4 * n, 32)
-    rp, col = P.csr_build(n, u, v)
+    rp, col = O.csr_build(n, u, v)
     Ro = O.repulsion_ibfft(X.astype(np.float64), k, n_int_fixed=64)
     outs = []
     for P_ in (0, {1: 512, 2: 768, 3: 1280}[k]):
@@ -69,15 +118,71 @@ def test_c3_snapshot_all_k():
     X = w.xy.astype(np.float64)
     for k in (1, 3):
         R, A, geo = _fft_forces(w.n, rp, col, w.xy, k)
-        assert geo["n_int"] == O.box_rule(w.xy).n_int
-        assert O.rel_l2(R, O.repulsion_ibfft(X, k)) <= TOL_IB
+        box = O.box_rule(w.xy)
+        assert geo["n_int"] == box.n_int and np.float32(geo["w"]) == box.w == 1.0  # R5'
+        check_ib(R, oracle_ib(X, k), f"C3 k={k}")
+
+
+@pytest.mark.parametrize("k", [1, 3])
+def test_c3_span_rule(k):
+    """interval_rule='span' (reading R5, w = L / N_int) against the oracle's rule='span'."""
+    w, rp, col = _case("C3")
+    R, _, geo = _fft_forces(w.n, rp, col, w.xy, k, interval_rule="span")
+    box = O.box_rule(w.xy, rule="span")
+    assert geo["n_int"] == box.n_int and np.float32(geo["w"]) == box.w != 1.0
+    check_ib(R, oracle_ib(w.xy, k, rule="span"), f"C3 span k={k}")
+
+
+def test_kernel_spectrum_reuse_and_invalidation():
+    """The kernel spectrum is recomputed only when (P, h, gamma) change (setup's key):
+    every evaluation must match the oracle across gamma changes, a grid re-plan, small
+    layouts whose w = L / 50 (h) changes with every layout, and k switches."""
+    n = 20000
+    u, v = random_graph(n, 4 * n, 51)
+    rp, col = O.csr_build(n, u, v)
+    X = (np.random.default_rng(52).random((n, 2)) * 180.0).astype(np.float32)
+    with P.Layout(n, rp, col, X, P.Params(solver="ibfft", k=1)) as L:
+        for rep in range(2):  # the second evaluation reuses the spectrum
+            R, _ = L.forces()
+            check_ib(R, oracle_ib(X, 1), f"reuse {rep}")
+        for g in (3.0, 2.0):
+            L.set_params(P.Params(solver="ibfft", k=1, gamma=g))
+            R, _ = L.forces()
+            check_ib(R, oracle_ib(X, 1, gamma=g), f"gamma {g}")
+        for scale in (0.2, 0.23, 2.5):  # L ~ 36, 41 (w = L/50 differs) then a re-plan
+            Xs = (X * scale).astype(np.float32)
+            L.set_layout(Xs)
+            for _ in range(2):
+                R, _ = L.forces()
+            check_ib(R, oracle_ib(Xs, 1), f"scale {scale}")
+        for k in (2, 3, 1):
+            L.set_params(P.Params(solver="ibfft", k=k))
+            R, _ = L.forces()
+            check_ib(R, oracle_ib(Xs, k), f"k {k}")
+
+
+@pytest.mark.parametrize("layout", ["c3", "blobs"])
+@pytest.mark.parametrize("k", [2, 3])
+def test_morton_ordered_k23_forces(layout, k):
+    """Forces after the internal Morton renumbering at k = 2, 3: the only node order in
+    which the spread's warp pre-aggregation forms groups (same-interval lanes).  On C3
+    (unit density) ~60 % of a warp's nodes share an interval; the clustered layout puts up
+    to 32 lanes in one interval.  Compared with the oracle at the layout the context holds."""
+    w, rp, col = _case("C3")
+    X0 = w.xy if layout == "c3" else blob_layout(w.n, 60, 2.0, 300.0, 53)
+    with P.Layout(w.n, rp, col, X0, P.Params(solver="ibfft", k=k, step0=1e-4)) as L:
+        L.step(8)  # renumbers (n >= 65536) at the first step call
+        R, A = L.forces()
+        X = L.layout().astype(np.float64)
+    check_ib(R, oracle_ib(X, k), f"morton {layout} k={k}")
+    assert O.rel_l2(A, O.attraction(X, rp, col)) <= 1e-4
 
 
 def test_coincident_and_degenerate():
     n = 300
     X = np.tile(np.array([[2.5, -1.0]], np.float32), (n, 1))
     u, v = random_graph(n, 600, 3)
-    rp, col = P.csr_build(n, u, v)
+    rp, col = O.csr_build(n, u, v)
     R, A, geo = _fft_forces(n, rp, col, X, 3)
     assert geo["L"] == 1.0 and geo["n_int"] == 50  # unit square (S:295)
     assert np.abs(R).max() < 1e-4 and np.abs(A).max() == 0
@@ -112,34 +217,49 @@ def test_step_and_dynamic_schedule():
     assert O.rel_l2(Xg - w.xy, Xo - w.xy) < 1e-2  # chaotic amplification is small over 19 steps
 
 
-def test_grid_cap_replans():
-    """A layout that outgrows the preallocated grid: warning + re-plan, still correct."""
+def test_grid_replans():
+    """A layout that outgrows the preallocated grid: tfdp_set_layout re-plans at once (no
+    capped iteration), and a layout that grows while stepping is re-planned by
+    the in-step check; forces stay on the oracle's rule."""
     n = 2000
     X = random_layout(n, 41, 3.0)
     u, v = random_graph(n, 2 * n, 42)
-    rp, col = P.csr_build(n, u, v)
+    rp, col = O.csr_build(n, u, v)
     with P.Layout(n, rp, col, X, P.Params(solver="ibfft", k=1)) as L:
         big = (X * 60.0).astype(np.float32)  # span ~ 1000 >> initial cap
         L.set_layout(big)
-        L.forces()  # runs capped, then re-plans
-        assert L.warnings & 4
         R, _ = L.forces()
+        assert not L.warnings & 4
         geo = L.fft_geometry()
-    box = O.box_rule(big)
-    assert geo["n_int"] == box.n_int
-    assert O.rel_l2(R, O.repulsion_ibfft(big.astype(np.float64), 1)) <= TOL_IB
+        box = O.box_rule(big)
+        assert geo["n_int"] == box.n_int
+        check_ib(R, oracle_ib(big, 1), "set_layout replan", dense=False)  # 2000 nodes, span 1000
+        # strong repulsion expands the layout by far more than the 8-interval headroom
+        L.set_params(P.Params(solver="ibfft", k=1, rho=50.0, iterations=300))
+        L.set_layout(X)
+        L.step(96)
+        Xg = L.layout()
+        R, _ = L.forces()
+        assert L.fft_geometry()["n_int"] == O.box_rule(Xg).n_int > O.box_rule(X).n_int
+    check_ib(R, oracle_ib(Xg, 1, rho=50.0), "grown", dense=False)
 
 
 @pytest.mark.slow
-def test_c4_forces_vs_oracle():
-    """1M-node RGG at the bench configuration, k = 1 and 3."""
+@pytest.mark.parametrize("k", [1, 2, 3])
+def test_c4_forces_vs_oracle(k):
+    """1M-node RGG at the bench configuration, every k (P = 2048 / 4096 / 6144: the three
+    FFT specialisations the bench runs), in the Morton order the bench runs (after 8
+    iterations at a tiny step) and in the caller's order."""
     w, rp, col = _case("C4")
     X = w.xy.astype(np.float64)
-    for k in (1, 3):
-        R, A, geo = _fft_forces(w.n, rp, col, w.xy, k)
-        assert geo["n_int"] == O.box_rule(w.xy).n_int
-        e = O.rel_l2(R, O.repulsion_ibfft(X, k))
-        assert e <= TOL_IB, (k, e)
+    R, A, geo = _fft_forces(w.n, rp, col, w.xy, k)
+    assert geo["n_int"] == O.box_rule(w.xy).n_int and geo["P"] == {1: 2048, 2: 4096, 3: 6144}[k]
+    check_ib(R, oracle_ib(X, k), f"C4 k={k}")
+    with P.Layout(w.n, rp, col, w.xy, P.Params(solver="ibfft", k=k, step0=1e-5)) as L:
+        L.step(8)
+        R, _ = L.forces()
+        Xm = L.layout().astype(np.float64)
+    check_ib(R, oracle_ib(Xm, k), f"C4 morton k={k}")
 
 
 @pytest.mark.slow
@@ -161,20 +281,21 @@ def test_full_run_np1_C3():
     assert max(ngs) - min(ngs) <= 0.03, ngs
 
 
-def test_internal_node_order_is_invisible():
+@pytest.mark.parametrize("k", [1, 2, 3])
+def test_internal_node_order_is_invisible(k):
     """n >= 65536 triggers the internal Morton renumbering at the first tfdp_step call of
     >= 8 iterations.  Afterwards tfdp_set_layout / tfdp_forces / tfdp_layout must still speak
     the caller's node order: forces at a caller-supplied layout match the oracle and the
     node_order='keep' context, and the layout round-trips."""
     w, rp, col = _case("C3")
     X = w.xy.astype(np.float64)
-    Ro, Ao = O.repulsion_ibfft(X, 1), O.attraction(X, rp, col)
+    Ro, Ao = oracle_ib(X, k), O.attraction(X, rp, col)
     out = {}
     # step0 = 1e-3: at the default 0.1 the first iterations of C3 are chaotic enough that two
     # identical node_order='keep' runs already differ by ~2% in displacement after 8
     # iterations (fp32 atomics, R15); a small step keeps the trajectory comparison meaningful.
     for order in ("auto", "keep"):
-        prm = P.Params(solver="ibfft", k=1, node_order=order, step0=1e-3)
+        prm = P.Params(solver="ibfft", k=k, node_order=order, step0=1e-3)
         with P.Layout(w.n, rp, col, w.xy, prm) as L:
             L.step(8)  # renumbers (auto) and moves the layout
             moved = L.layout()
@@ -182,14 +303,16 @@ def test_internal_node_order_is_invisible():
             L.set_layout(w.xy)  # back to the caller's input layout
             np.testing.assert_array_equal(L.layout(), w.xy)
             R, A = L.forces()
-        assert O.rel_l2(R, Ro) <= TOL_IB, order
+        check_ib(R, Ro, f"order {order} k={k}")
         assert O.rel_l2(A, Ao) <= 1e-4, order
         out[order] = (R, A, moved)
     # fp32 spread atomics (R15): two node_order='keep' runs already differ by ~3e-5 at C3
-    assert O.rel_l2(out["auto"][0], out["keep"][0]) <= 1e-4
+    # and k = 1; the noise floor grows with the k^2 contributions per node (1.1e-4 / 1.4e-4
+    # measured at k = 2 / 3, each run within 2.2e-4 of the oracle)
+    assert O.rel_l2(out["auto"][0], out["keep"][0]) <= {1: 1e-4, 2: 3e-4, 3: 3e-4}[k]
     # the 8 iterations themselves agree up to fp32 summation order (atomics, R15), and with
     # the oracle's 8 ibFFT iterations
-    Xo = O.run(w.xy, rp, col, O.Params(), T=300, eta0=1e-3, solver="ibfft", k=1, t_end=8)
+    Xo = O.run(w.xy, rp, col, O.Params(), T=300, eta0=1e-3, solver="ibfft", k=k, t_end=8)
     da, dk, do = out["auto"][2] - w.xy, out["keep"][2] - w.xy, Xo - w.xy
     assert O.rel_l2(da, dk) <= 1e-3
     # vs the fp64 oracle: the device keeps positions in fp32 (R14), so each of the 8 updates

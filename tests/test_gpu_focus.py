@@ -16,7 +16,7 @@ BOOSTS = [(4.0, 2.0, 2.0), (1.0, 3.0, 1.0), (2.0, 1.0, 5.0)]
 
 def _case(name):
     w = make_config(name)
-    rp, col = P.csr_build(w.n, w.u, w.v)
+    rp, col = O.csr_build(w.n, w.u, w.v)
     return w, rp, col
 
 
@@ -115,7 +115,7 @@ def test_reordered_context_c3():
 
 def test_star_center_pulls_leaves_on_device():
     n = 31
-    rp, col = P.csr_build(n, np.zeros(n - 1, np.int32), np.arange(1, n, dtype=np.int32))
+    rp, col = O.csr_build(n, np.zeros(n - 1, np.int32), np.arange(1, n, dtype=np.int32))
     from synth import uniform_disc
     with P.Layout(n, rp, col, uniform_disc(n, 4.0, 21)) as L:
         L.step(300)

@@ -27,7 +27,7 @@ def test_hand_examples():
     ]
     for n, e, X, np1, hits in cases:
         u, v = np.array(e, np.int32).T
-        rp, col = P.csr_build(n, u, v)
+        rp, col = O.csr_build(n, u, v)
         val, h = _gpu_hits(n, rp, col, np.array(X, np.float32))
         assert h.tolist() == hits and val == pytest.approx(np1, abs=1e-15)
 
@@ -35,7 +35,7 @@ def test_hand_examples():
 @pytest.mark.parametrize("name", ["C1", "C2", "C2rgg"])
 def test_small_configs_bit_exact(name):
     w = make_config(name)
-    rp, col = P.csr_build(w.n, w.u, w.v)
+    rp, col = O.csr_build(w.n, w.u, w.v)
     val, h = _gpu_hits(w.n, rp, col, w.xy)
     ho = O.np1_hits(w.xy, rp, col, dist="fp32")
     np.testing.assert_array_equal(h, ho)
@@ -48,7 +48,7 @@ def test_ragged_and_isolated(n, m, scale):
     """Sizes off every block / warp multiple; m < n leaves degree-0 nodes (contribute 1)."""
     X = random_layout(n, n + 5, scale)
     u, v = random_graph(n, m, n + 6) if m else (np.zeros(0, np.int32),) * 2
-    rp, col = P.csr_build(n, u, v)
+    rp, col = O.csr_build(n, u, v)
     val, h = _gpu_hits(n, rp, col, X)
     ho = O.np1_hits(X, rp, col, dist="fp32")
     np.testing.assert_array_equal(h, ho)
@@ -64,7 +64,7 @@ def test_lattice_ties_and_coincident_points():
     u, v = random_graph(n, 4 * n, 9)
     hub_u = np.zeros(n - 1, np.int32)
     hub_v = np.arange(1, n, dtype=np.int32)
-    rp, col = P.csr_build(n, np.concatenate([u, hub_u]), np.concatenate([v, hub_v]))
+    rp, col = O.csr_build(n, np.concatenate([u, hub_u]), np.concatenate([v, hub_v]))
     val, h = _gpu_hits(n, rp, col, X)
     ho = O.np1_hits(X, rp, col, dist="fp32")
     np.testing.assert_array_equal(h, ho)
@@ -72,7 +72,7 @@ def test_lattice_ties_and_coincident_points():
     # all points coincident: every distance ties at 0 -> the k lowest other ids
     Xc = np.zeros((500, 2), np.float32)
     u, v = random_graph(500, 1500, 10)
-    rp, col = P.csr_build(500, u, v)
+    rp, col = O.csr_build(500, u, v)
     val, h = _gpu_hits(500, rp, col, Xc)
     np.testing.assert_array_equal(h, O.np1_hits(Xc, rp, col, dist="fp32"))
 
@@ -81,7 +81,7 @@ def test_c3_sampled_and_value():
     """C3 (n = 1e5, RGG, random node order): 2000 sampled nodes bit-exact against the
     brute-force oracle; the NP1 value against the oracle's fp64 KD-tree NP1."""
     w = make_config("C3")
-    rp, col = P.csr_build(w.n, w.u, w.v)
+    rp, col = O.csr_build(w.n, w.u, w.v)
     val, h = _gpu_hits(w.n, rp, col, w.xy)
     idx = np.random.default_rng(3).choice(w.n, 2000, replace=False)
     np.testing.assert_array_equal(h[idx], O.np1_hits(w.xy, rp, col, nodes=idx, dist="fp32"))
@@ -93,7 +93,7 @@ def test_reordered_context_and_shards():
     """Internal Morton renumbering (ibFFT, n >= 65536) keeps the caller's order and ids for
     the tie rule; virtual shards partition the hits and the value."""
     w = make_config("C3")
-    rp, col = P.csr_build(w.n, w.u, w.v)
+    rp, col = O.csr_build(w.n, w.u, w.v)
     with P.Layout(w.n, rp, col, w.xy, P.Params(solver="ibfft", k=1, iterations=20)) as L:
         L.step(10)  # renumbers at the first step call
         X = L.layout()

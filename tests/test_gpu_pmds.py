@@ -19,7 +19,7 @@ def _gpu_pmds(n, rp, col, p, seed, **kw):
 
 
 def test_path_exact():
-    rp, col = P.csr_build(10, np.arange(9, dtype=np.int32), np.arange(1, 10, dtype=np.int32))
+    rp, col = O.csr_build(10, np.arange(9, dtype=np.int32), np.arange(1, 10, dtype=np.int32))
     X, piv = _gpu_pmds(10, rp, col, 4, 1)
     want = np.arange(10) - 4.5
     assert np.allclose(X[:, 0] * np.sign(X[-1, 0]), want, atol=1e-5)
@@ -32,7 +32,7 @@ def test_path_exact():
 def test_pivots_and_layout_random(n, m, p, seed):
     """Random graphs, some disconnected (unreachable rule R24)."""
     u, v = random_graph(n, m, seed + 10)
-    rp, col = P.csr_build(n, u, v)
+    rp, col = O.csr_build(n, u, v)
     X, piv = _gpu_pmds(n, rp, col, p, seed)
     Xo, po = O.pivot_mds(rp, col, p, seed)
     np.testing.assert_array_equal(piv, po)
@@ -41,14 +41,14 @@ def test_pivots_and_layout_random(n, m, p, seed):
 
 def test_grid_and_rgg_layouts():
     u, v = grid_graph(30, 12)
-    rp, col = P.csr_build(360, u, v)
+    rp, col = O.csr_build(360, u, v)
     X, piv = _gpu_pmds(360, rp, col, 30, 4)
     Xo, po = O.pivot_mds(rp, col, 30, 4)
     np.testing.assert_array_equal(piv, po)
     assert O.rel_l2(X, Xo) < 1e-5
     n = 20000
     u, v, xy = rgg_graph(n, np.sqrt(8 / np.pi), np.sqrt(n), 7)
-    rp, col = P.csr_build(n, u, v)
+    rp, col = O.csr_build(n, u, v)
     X, piv = _gpu_pmds(n, rp, col, 20, 11)
     Xo, po = O.pivot_mds(rp, col, 20, 11)
     np.testing.assert_array_equal(piv, po)
@@ -62,7 +62,7 @@ def test_grid_and_rgg_layouts():
 def test_reordered_context_and_errors():
     n = 70000  # >= 65536: the ibFFT context renumbers nodes internally
     u, v, xy = rgg_graph(n, np.sqrt(8 / np.pi), np.sqrt(n), 8)
-    rp, col = P.csr_build(n, u, v)
+    rp, col = O.csr_build(n, u, v)
     X1, p1 = _gpu_pmds(n, rp, col, 16, 3)
     with P.Layout(n, rp, col, xy, P.Params(solver="ibfft", k=1, iterations=20)) as L:
         L.step(10)  # renumbered

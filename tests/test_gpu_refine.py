@@ -14,7 +14,7 @@ pytestmark = pytest.mark.gpu
 
 def _case(name):
     w = make_config(name)
-    rp, col = P.csr_build(w.n, w.u, w.v)
+    rp, col = O.csr_build(w.n, w.u, w.v)
     return w, rp, col
 
 
@@ -75,7 +75,7 @@ def test_global_refine_ibfft_short():
 def test_refinement_effects_on_device():
     """The paired statistics of the oracle pins, measured on the GPU path."""
     u, v = path_graph(20)
-    rp, col = P.csr_build(20, u, v)
+    rp, col = O.csr_build(20, u, v)
     with P.Layout(20, rp, col, uniform_disc(20, 5.0, 11)) as L:
         L.step(300)
         Xb = L.layout()
@@ -87,7 +87,7 @@ def test_refinement_effects_on_device():
 
     u, v, lab = two_cluster_graph(100, 0.1, 0.002, 12)
     n = 200
-    rp, col = P.csr_build(n, u, v)
+    rp, col = O.csr_build(n, u, v)
     with P.Layout(n, rp, col, uniform_disc(n, 8.0, 13)) as L:
         L.step(300)
         Xb = L.layout().astype(np.float64)

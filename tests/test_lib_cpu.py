@@ -25,6 +25,7 @@ def test_params_default_matches_paper():
     assert P.lib().tfdp_params_default(C.byref(p)) == 0
     assert (p.dim, p.alpha, p.beta, p.gamma, p.rho) == (2, 0.1, 8.0, 2.0, 1.0)
     assert (p.n_int_min, p.step0, p.iterations, p.k) == (50, 0.1, 300, 0)  # P:540, R3
+    assert p.interval_rule == 0  # reading R5' (unit-width intervals)
     assert P.lib().tfdp_params_default(None) == 1
 
 
@@ -44,6 +45,17 @@ def test_csr_build_configs_bit_exact():
         rp, col = P.csr_build(w.n, w.u, w.v)
         rp2, col2 = O.csr_build(w.n, w.u, w.v)
         assert np.array_equal(rp, rp2) and np.array_equal(col, col2), name
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["C4", "C5"])
+def test_csr_build_bench_configs_bit_exact(name):
+    """The bench's graphs (C4: 8.0M, C5: 69.3M directed entries) build bit-identically."""
+    w = make_config(name)
+    rp, col = P.csr_build(w.n, w.u, w.v)
+    rp2, col2 = O.csr_build(w.n, w.u, w.v)
+    assert np.array_equal(rp, rp2) and np.array_equal(col, col2), name
+    del w, rp, col, rp2, col2
 
 
 def test_csr_build_errors():
