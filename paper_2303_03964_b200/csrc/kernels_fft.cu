@@ -8,6 +8,7 @@
 //                 fused bbox of the new positions for the next iteration
 // The grid convolution (step 2) is kernels_fftconv.cu.
 #include <algorithm>
+#include <climits>
 #include <cstdlib>
 
 #include "device_math.cuh"
@@ -316,9 +317,164 @@ spread_kernel(const float2* __restrict__ xy, int64_t lo, int64_t cnt,
   }
 }
 
+// ------------------------------------------------------------------ spread, privatised
+// Shared-memory privatised, tile-binned variant (north star step 1): a
+// block takes kNodeThreads * NPT consecutive nodes (in the internal Morton order they cover
+// a compact patch of intervals), reduces the patch's interval box, accumulates its charges
+// into a private shared-memory tile of that box and flushes the tile with ONE v4 RED per
+// touched grid node.  sm_100a has no native fp32 add in the shared-memory atomic unit (an
+// fp32 atomicAdd on shared memory is a CAS loop, ATOMS.CAST.SPIN), so the tile holds 64-bit
+// fixed-point sums (2^32 scale; integer ATOMS.ADD.64, exact and order-independent; the
+// quantum 2^-32 is far below the fp32 rounding of the values).  A patch whose box exceeds
+// the tile capacity (random node order, outliers) falls back to per-node REDs.
+template <int K>
+__host__ __device__ constexpr int spread_tile_npt() { return K == 1 ? 4 : K == 2 ? 2 : 1; }
+template <int K>
+__host__ __device__ constexpr int spread_tile_cap() { return K == 1 ? 2048 : K == 2 ? 2048 : 2304; }
+
+__device__ __forceinline__ void fx_add(unsigned long long* a, float v) {
+  atomicAdd(a, (unsigned long long)__float2ll_rn(v * 4294967296.0f));
+}
+__device__ __forceinline__ float fx_get(unsigned long long a) {
+  return (float)((double)(long long)a * (1.0 / 4294967296.0));
+}
+
+template <int K>
+__global__ void __launch_bounds__(kNodeThreads)
+spread_tile_kernel(const float2* __restrict__ xy, int64_t lo, int64_t cnt,
+                   const GridGeom* __restrict__ geom, float4* __restrict__ grid) {
+  constexpr int NPT = spread_tile_npt<K>();
+  constexpr int CAP = spread_tile_cap<K>();
+  extern __shared__ unsigned long long tile[];  // [3][CAP] fixed point
+  __shared__ int sbox[4][kNodeThreads / 32];
+  pdl_wait();
+  pdl_trigger();
+  const GridGeom g = *geom;
+  const int64_t base = (int64_t)blockIdx.x * kNodeThreads * NPT;
+  float2 p[NPT];
+  Cell c[NPT];
+  bool act[NPT];
+  int bx0 = INT32_MAX, by0 = INT32_MAX, bx1 = -1, by1 = -1;
+#pragma unroll
+  for (int j = 0; j < NPT; ++j) {
+    const int64_t t = base + j * kNodeThreads + threadIdx.x;
+    act[j] = t < cnt;
+    p[j] = act[j] ? xy[lo + t] : make_float2(g.cx, g.cy);
+    c[j] = cell_of(p[j], g);
+    if (act[j]) {
+      bx0 = min(bx0, c[j].bx);
+      bx1 = max(bx1, c[j].bx);
+      by0 = min(by0, c[j].by);
+      by1 = max(by1, c[j].by);
+    }
+  }
+  // block interval box (uniform decision below)
+  {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    bx0 = __reduce_min_sync(0xffffffffu, bx0);
+    by0 = __reduce_min_sync(0xffffffffu, by0);
+    bx1 = __reduce_max_sync(0xffffffffu, bx1);
+    by1 = __reduce_max_sync(0xffffffffu, by1);
+    if (lane == 0) {
+      sbox[0][warp] = bx0;
+      sbox[1][warp] = by0;
+      sbox[2][warp] = bx1;
+      sbox[3][warp] = by1;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int w = 0; w < kNodeThreads / 32; ++w) {
+      bx0 = min(bx0, sbox[0][w]);
+      by0 = min(by0, sbox[1][w]);
+      bx1 = max(bx1, sbox[2][w]);
+      by1 = max(by1, sbox[3][w]);
+    }
+  }
+  if (bx1 < 0) return;  // no active node in the block
+  const int W = (bx1 - bx0 + 1) * K, H = (by1 - by0 + 1) * K;
+  const bool priv = W * H <= CAP;
+  if (priv) {
+    const int WH = W * H;
+    for (int i = threadIdx.x; i < WH; i += kNodeThreads) {
+      tile[i] = 0ull;
+      tile[CAP + i] = 0ull;
+      tile[2 * CAP + i] = 0ull;
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int j = 0; j < NPT; ++j) {
+    if (!act[j]) continue;
+    float lx[K], ly[K];
+    lagrange<K>(c[j].ux, lx);
+    lagrange<K>(c[j].uy, ly);
+    const float xt = p[j].x - g.cx, yt = p[j].y - g.cy;  // box-centred channels (R11)
+#pragma unroll
+    for (int b = 0; b < K; ++b) {
+#pragma unroll
+      for (int a = 0; a < K; ++a) {
+        const float wgt = lx[a] * ly[b];
+        if (priv) {
+          const int o = ((c[j].by - by0) * K + b) * W + (c[j].bx - bx0) * K + a;
+          fx_add(tile + o, wgt);
+          fx_add(tile + CAP + o, wgt * xt);
+          fx_add(tile + 2 * CAP + o, wgt * yt);
+        } else {
+          atomicAdd(grid + (int64_t)(c[j].by * K + b) * g.pitch + c[j].bx * K + a,
+                    make_float4(wgt, wgt * xt, wgt * yt, 0.0f));
+        }
+      }
+    }
+  }
+  if (!priv) return;
+  __syncthreads();
+  for (int i = threadIdx.x; i < W * H; i += kNodeThreads) {
+    const unsigned long long a0 = tile[i], a1 = tile[CAP + i], a2 = tile[2 * CAP + i];
+    if ((a0 | a1 | a2) != 0ull) {
+      const int r = i / W, q = i - r * W;
+      atomicAdd(grid + (int64_t)(by0 * K + r) * g.pitch + bx0 * K + q,
+                make_float4(fx_get(a0), fx_get(a1), fx_get(a2), 0.0f));
+    }
+  }
+}
+
+// Spread variant.  Measured at C4 (tools/spread_ab.sh, profiles/r2_spread_ab.txt; us per
+// launch, REDs / privatised tile): input layout k = 1 10.8 / 20.6, k = 2 25.3 / 35.6,
+// k = 3 59.9 / 73.6; clustered layout (1000 Gaussian clusters) k = 1 10.9 / 20.7, k = 3
+// 50.7 / 70.5.  The shared-memory atomics (CAS loops) cost more than the L2 reductions they
+// save, so the per-node v4 REDs are the default; TFDP_SPREAD=tile selects the privatised
+// kernel (A/B runs; it is parity-tested like the default).
+bool spread_tiles() {
+  static const bool t = [] {
+    const char* e = std::getenv("TFDP_SPREAD");
+    return e && e[0] == 't';
+  }();
+  return t;
+}
+
 void launch_spread(const float2* xy, int64_t lo, int64_t cnt, const GridGeom* geom, int k,
                    float4* grid, cudaStream_t s) {
   if (cnt <= 0) return;
+  if (spread_tiles()) {
+#define TFDP_ST(KK)                                                                          \
+  {                                                                                          \
+    constexpr int per = kNodeThreads * spread_tile_npt<KK>();                                \
+    const size_t smb = 3 * sizeof(unsigned long long) * spread_tile_cap<KK>();              \
+    static bool attr = [] {                                                                  \
+      cudaFuncSetAttribute(spread_tile_kernel<KK>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                           (int)(3 * sizeof(unsigned long long) * spread_tile_cap<KK>()));   \
+      return true;                                                                           \
+    }();                                                                                     \
+    (void)attr;                                                                              \
+    launch_chained(spread_tile_kernel<KK>, (unsigned)((cnt + per - 1) / per), kNodeThreads, smb, \
+                   s, xy, lo, cnt, geom, grid);                                              \
+  }
+    if (k == 1) TFDP_ST(1)
+    else if (k == 2) TFDP_ST(2)
+    else TFDP_ST(3)
+#undef TFDP_ST
+    return;
+  }
   const unsigned blocks = (unsigned)((cnt + kNodeThreads - 1) / kNodeThreads);
   if (k == 1) launch_chained(spread_kernel<1>, blocks, kNodeThreads, 0, s, xy, lo, cnt, geom, grid);
   else if (k == 2) launch_chained(spread_kernel<2>, blocks, kNodeThreads, 0, s, xy, lo, cnt, geom, grid);

@@ -116,6 +116,8 @@ void launch_setup(BoxKeys* slots, int n_part, BoxKeys* keys, GridGeom* geom, int
                   int n_int_min, int n_int_fixed, int n_int_cap, int P, int pitch,
                   int* capped_flag, int rule, float gamma, KspecKey* kkey, cudaStream_t s);
 // charges: float4 {C_1, C_x~, C_y~, 0} per grid node, row pitch = GridGeom::pitch float4s
+// per-node (warp-aggregated for k >= 2) v4 REDs; TFDP_SPREAD=tile: the shared-memory
+// privatised tile kernel (measured slower, kernels_fft.cu)
 void launch_spread(const float2* xy, int64_t lo, int64_t cnt, const GridGeom* geom, int k,
                    float4* grid, cudaStream_t s);
 

@@ -3,6 +3,8 @@ step-by-step ibFFT at identical (box, N_int, k) — the box and interval index a
 fp32 on both sides (R19) — and vs the exact oracle within the oracle's own ibFFT error.
 Bar: (i) rel-L2 <= 1e-3 vs oracle-ibFFT; (ii) <= e_k + 1e-3 vs exact; full-run NP1 within
 0.01 (C3, dynamic k, T=300)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -264,21 +266,21 @@ def test_c4_forces_vs_oracle(k):
 
 @pytest.mark.slow
 def test_full_run_np1_C3():
-    """C3: 300 iterations, dynamic k; NP1 of the GPU layouts within 0.01 of the oracle's.
-    The trajectory is chaotic and the spread's fp32 atomics make every GPU run a different
-    (equally valid, R15) trajectory: single runs scatter with std ~0.003 in NP1 (measured
-    over 8 runs: 0.840 - 0.848, mean 0.843, vs oracle 0.836; tools/np1_spread_c3.py), so the
-    bar is applied to the mean of eight runs (std of the mean ~0.001)."""
+    """C3: 300 iterations, dynamic k; the NP1 of EVERY GPU run within 0.01 of the fp64
+    oracle's (north star).  Measured under reading R5' (tools/np1_spread_c3.py,
+    tools/np1_offset_c3.py): 8 GPU runs 0.8470 - 0.8477 (std 0.0002) vs the oracle's 0.8469;
+    the oracle with fp32-stored positions 0.8470 and from 1e-7-perturbed inputs 0.8472 +-
+    0.0003 (R22')."""
     w, rp, col = _case("C3")
     ngs = []
-    for _ in range(8):
+    for _ in range(3):
         with P.Layout(w.n, rp, col, w.xy, P.Params(solver="ibfft", k=0)) as L:
             L.step(300)
             ngs.append(O.np1(L.layout(), rp, col))
     Xo = O.run(w.xy, rp, col, O.Params(), T=300, solver="ibfft", k=0)
     no = O.np1(Xo, rp, col)
-    assert abs(float(np.mean(ngs)) - no) <= 0.01, (ngs, no)
-    assert max(ngs) - min(ngs) <= 0.03, ngs
+    print(f"[np1] gpu {ngs} oracle {no}")
+    assert all(abs(g - no) <= 0.01 for g in ngs), (ngs, no)
 
 
 @pytest.mark.parametrize("k", [1, 2, 3])
@@ -345,3 +347,29 @@ def test_charges_cleared_between_evaluations():
         Rf, _, _ = _fft_forces(w.n, rp, col, Xs, k)
         assert O.rel_l2(Rs, Rf) <= 1e-4, k
     assert O.rel_l2(R1, O.repulsion_ibfft(w.xy.astype(np.float64), 1)) <= TOL_IB
+
+
+def test_spread_tile_variant_subprocess():
+    """The shared-memory privatised spread (TFDP_SPREAD=tile, measured slower and kept as an
+    A/B variant) is parity-tested too: Morton-ordered C3 and clustered layouts, k = 1, 3,
+    including the per-node fallback of random-order contexts."""
+    import subprocess
+    import sys
+    code = r"""
+import numpy as np, oracle as O, paper_2303_03964_b200 as P
+from synth import make_config, blob_layout
+w = make_config("C3"); rp, col = O.csr_build(w.n, w.u, w.v)
+for X0 in (w.xy, blob_layout(w.n, 60, 2.0, 300.0, 53)):
+    for k in (1, 3):
+        for order in ("auto", "keep"):
+            with P.Layout(w.n, rp, col, X0, P.Params(solver="ibfft", k=k, step0=1e-4, node_order=order)) as L:
+                L.step(8); R, _ = L.forces(); X = L.layout().astype(np.float64)
+            e = O.rel_l2(R, O.repulsion_ibfft(X, k))
+            print(k, order, e); assert e <= 1e-3, (k, order, e)
+print("tile ok")
+"""
+    env = dict(os.environ, TFDP_SPREAD="tile")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    print(r.stdout, r.stderr[-2000:])
+    assert r.returncode == 0 and "tile ok" in r.stdout
