@@ -48,7 +48,16 @@ typedef enum {
 
 enum { TFDP_EXACT = 0, TFDP_IBFFT = 1 };                 /* repulsion path (P:454 / P:488) */
 enum { TFDP_COOL_LINEAR = 0, TFDP_COOL_CONSTANT = 1 };    /* integrator readings R2 / R2'   */
-enum { TFDP_DIST_SPREAD_ALL = 0, TFDP_DIST_GRID_ALLREDUCE = 1 }; /* FFT path, p > 1 (§8(e)) */
+/* FFT path at p > 1:
+ *   TFDP_DIST_SLAB (default): the grid convolution is distributed like a slab-decomposed
+ *     2-D FFT — every rank spreads the nodes of its grid-row slab (from the full positions),
+ *     transforms those rows, transposes (NCCL send/recv), runs the column pass on its chunk
+ *     of half-spectrum columns, transposes back, inverse-transforms its rows and broadcasts
+ *     its potential rows; gather / attraction / update of its own node shard, position
+ *     all-gather.  Nodes are renumbered in Morton order identically on every rank.
+ *   TFDP_DIST_SPREAD_ALL: every rank spreads all nodes and runs the whole convolution.
+ *   TFDP_DIST_GRID_ALLREDUCE: own nodes spread, charge grid all-reduced, whole convolution. */
+enum { TFDP_DIST_SPREAD_ALL = 0, TFDP_DIST_GRID_ALLREDUCE = 1, TFDP_DIST_SLAB = 2 };
 enum { TFDP_ORDER_AUTO = 0, TFDP_ORDER_KEEP = 1 };        /* internal node renumbering      */
 enum { TFDP_RULE_UNIT = 0, TFDP_RULE_SPAN = 1 };          /* interval width readings R5'/R5 */
 
@@ -76,7 +85,8 @@ typedef struct {
   int32_t t0;          /* first iteration index (resume), default 0                        */
   int32_t cooling;     /* TFDP_COOL_LINEAR (eta_t = eta0 (1 - t/T), R2, default) |
                           TFDP_COOL_CONSTANT (eta_t = eta0, R2')                           */
-  int32_t dist_mode;   /* TFDP_DIST_SPREAD_ALL (default) | TFDP_DIST_GRID_ALLREDUCE        */
+  int32_t dist_mode;   /* TFDP_DIST_SLAB (default) | TFDP_DIST_SPREAD_ALL |
+                          TFDP_DIST_GRID_ALLREDUCE (ibFFT path at p > 1)                   */
   int32_t node_order;  /* TFDP_ORDER_AUTO (default): the ibFFT path renumbers nodes internally
                           in Morton order of the layout (single GPU, n >= 65536) at the start
                           of each tfdp_step call; all inputs/outputs stay in the caller's
@@ -91,9 +101,12 @@ typedef struct {
 
 /* Multi-GPU description: one process per GPU.  nccl_uid = 128 bytes from
  * tfdp_nccl_unique_id() on rank 0, broadcast by the caller (e.g. over torch.distributed).
- * nccl_uid == NULL with world > 1 is a "virtual shard": no communicator, the context
- * evaluates rank's shard [lo, hi) on one GPU (tfdp_forces only; tfdp_step returns
- * TFDP_ERR_UNSUPPORTED) — used to test the shard rule and determinism on one device. */
+ * nccl_uid == NULL with world > 1 is a "virtual rank": no communicator.  Alone it evaluates
+ * its shard [lo, hi) on one GPU with tfdp_forces (exact path and the SPREAD_ALL mode;
+ * tfdp_step returns TFDP_ERR_UNSUPPORTED); all p virtual ranks of a world together run
+ * every mode, tfdp_step included, through tfdp_group_step / tfdp_group_forces, with device
+ * copies on their shared stream in place of NCCL — the same kernels, phases, layouts and
+ * message boundaries as the NCCL path (one device: correctness, not scaling). */
 typedef struct {
   int32_t rank, world, device;
   const unsigned char* nccl_uid;
@@ -146,6 +159,27 @@ tfdp_status tfdp_step(tfdp_ctx* ctx, int32_t n_iters);
  * (either may be NULL).  The ibFFT path uses k = params.k, or the schedule's k at the
  * current iteration when params.k == 0.  Parity entry point of the tests. */
 tfdp_status tfdp_forces(tfdp_ctx* ctx, float* rep_xy, float* att_xy);
+
+/* The virtual ranks 0..p-1 of one world (contexts created with tfdp_dist {r, p, device,
+ * NULL}, one stream, one problem, same iteration t), driven in lockstep on one device:
+ * tfdp_group_step = tfdp_step of every rank, tfdp_group_forces = tfdp_forces of every rank
+ * (rep_xy[r] / att_xy[r]: rank r's output, host or device float32[2 (hi_r - lo_r)], arrays
+ * or entries may be NULL).  Every exchange of the multi-GPU path (position all-gather,
+ * renumbering broadcast, slab transposes, potential rows) is a device copy between the
+ * contexts' buffers.  TFDP_ERR_ARG if the contexts do not form such a group (1 <= p <= 64);
+ * otherwise the errors of tfdp_step / tfdp_forces. */
+tfdp_status tfdp_group_step(tfdp_ctx* const* ctxs, int32_t p, int32_t n_iters);
+tfdp_status tfdp_group_forces(tfdp_ctx* const* ctxs, int32_t p, float* const* rep_xy,
+                              float* const* att_xy);
+
+/* Slab plan of the TFDP_DIST_SLAB mode (host only, no GPU): for `rows` grid rows
+ * (N_int cap x k) and FFT size fft_size split over world ranks, rank r owns grid rows
+ * [row0[r], row0[r+1]) (multiples of 24, row0[world] = rows rounded up to 24) and
+ * half-spectrum columns [q0[r], q0[r+1]) (even starts, q0[world] = fft_size/2 + 1).
+ * row0, q0: host int32[world + 1].  TFDP_ERR_ARG unless rows >= 1, fft_size even >= 2,
+ * 1 <= world <= 64. */
+tfdp_status tfdp_slab_plan(int32_t rows, int32_t fft_size, int32_t world, int32_t* row0,
+                           int32_t* q0);
 
 /* Copies the full current layout (all n nodes, every rank) to xy_out (host or device
  * float32[2n]). */

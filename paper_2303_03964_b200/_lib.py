@@ -17,7 +17,7 @@ STATUS = {0: "TFDP_OK", 1: "TFDP_ERR_ARG", 2: "TFDP_ERR_CUDA", 3: "TFDP_ERR_OOM"
           7: "TFDP_ERR_UNSUPPORTED"}
 EXACT, IBFFT = 0, 1
 COOL_LINEAR, COOL_CONSTANT = 0, 1
-DIST_SPREAD_ALL, DIST_GRID_ALLREDUCE = 0, 1
+DIST_SPREAD_ALL, DIST_GRID_ALLREDUCE, DIST_SLAB = 0, 1, 2
 WARN_ALPHA_BETA, WARN_GAMMA, WARN_NINT_CAPPED = 1, 2, 4
 
 
@@ -47,6 +47,9 @@ _SIGS = {
                             C.POINTER(tfdp_dist), _P]),
     "tfdp_step": (C.c_int, [_P, C.c_int32]),
     "tfdp_forces": (C.c_int, [_P, _P, _P]),
+    "tfdp_group_step": (C.c_int, [_P, C.c_int32, C.c_int32]),
+    "tfdp_group_forces": (C.c_int, [_P, C.c_int32, _P, _P]),
+    "tfdp_slab_plan": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, _P, _P]),
     "tfdp_layout": (C.c_int, [_P, _P]),
     "tfdp_set_layout": (C.c_int, [_P, _P]),
     "tfdp_set_iteration": (C.c_int, [_P, C.c_int32]),

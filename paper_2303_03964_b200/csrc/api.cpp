@@ -98,6 +98,14 @@ struct tfdp_ctx {
   int64_t alloc_kh = 0;
   float2* tw[4] = {nullptr, nullptr, nullptr, nullptr};  // twiddles per k (length P_k)
   int tw_P[4] = {0, 0, 0, 0};
+  // multi-GPU slab mode (TFDP_DIST_SLAB, kernels_dist.cu): per-k row slabs / column chunks,
+  // xa = exchange-1 send / exchange-2 receive, xb = exchange-1 receive (column pass in place)
+  bool slab = false;
+  tfdp::SlabPlan plan[4];
+  float2* xa = nullptr;
+  float2* xb = nullptr;
+  int64_t alloc_xa = 0, alloc_xb = 0;
+  float2* fbuf = nullptr;  // n float2: forces of all ranks (tfdp_forces of a reordered shard)
   // schedule
   int t = 0;
   std::vector<int32_t> ksched;
@@ -309,7 +317,8 @@ tfdp_status validate_params(const tfdp_params* p, uint32_t* warn, std::string* m
     *msg = "unknown cooling";
     return TFDP_ERR_ARG;
   }
-  if (p->dist_mode != TFDP_DIST_SPREAD_ALL && p->dist_mode != TFDP_DIST_GRID_ALLREDUCE) {
+  if (p->dist_mode != TFDP_DIST_SPREAD_ALL && p->dist_mode != TFDP_DIST_GRID_ALLREDUCE &&
+      p->dist_mode != TFDP_DIST_SLAB) {
     *msg = "unknown dist_mode";
     return TFDP_ERR_ARG;
   }
@@ -429,7 +438,9 @@ tfdp_status configure_fft(tfdp_ctx* c, float L) {
   }
   c->nint_cap = need;
   const int cpitch = mcap;
-  const int capitch = (mcap + 31) & ~31;  // multiple of the CA row tile (kernels_fftconv.cu)
+  // CA rows: a multiple of the CA row tile (kernels_fftconv.cu); slab mode: of 96 (whole
+  // 24-row slab units of every k, kernels_dist.cu)
+  const int capitch = c->slab ? (mcap + 95) / 96 * 96 : (mcap + 31) & ~31;
   // charges: one float4 {C_1, C_x~, C_y~, 0} per grid node; potentials: 3 planes
   int64_t planes = 4LL * cpitch * cpitch, ca = 0, ka = 0, kh = 0;
   for (int k = 1; k <= 3; ++k) {
@@ -479,16 +490,68 @@ tfdp_status configure_fft(tfdp_ctx* c, float L) {
   }
   for (int k = 1; k <= 3; ++k)
     if (k_used(c, k)) CUDA_TRY(c, tfdp::fftconv_prepare(c->P_of_k[k]));
+  if (c->slab) {  // per-k slabs over [0, cap_k k) and column chunks of P_k / 2 + 1
+    int64_t xa = 1, xb = 1;
+    for (int k = 1; k <= 3; ++k) {
+      if (!k_used(c, k)) continue;
+      tfdp::SlabPlan& pl = c->plan[k];
+      tfdp::slab_plan(c->world, c->rank, c->cap_of_k[k] * k, c->P_of_k[k], &pl);
+      const int64_t rows_me = pl.row0[c->rank + 1] - pl.row0[c->rank];
+      const int64_t nq_me = pl.q0[c->rank + 1] - pl.q0[c->rank];
+      xa = std::max<int64_t>(xa, 3 * rows_me * pl.H);
+      xb = std::max<int64_t>(xb, 3LL * pl.R * nq_me);
+    }
+    if (xa > c->alloc_xa || xb > c->alloc_xb) {
+      cudaStreamSynchronize(c->stream);
+      cudaFree(c->xa);
+      cudaFree(c->xb);
+      c->xa = c->xb = nullptr;
+      CUDA_TRY(c, cudaMalloc(&c->xa, xa * sizeof(float2)));
+      CUDA_TRY(c, cudaMalloc(&c->xb, xb * sizeof(float2)));
+      c->alloc_xa = xa;
+      c->alloc_xb = xb;
+    }
+  }
   CUDA_TRY(c, cudaGetLastError());
   return TFDP_OK;
 }
 
-// ---------------------------------------------------------------- exchange (p > 1)
-tfdp_status exchange_positions(tfdp_ctx* c, float2* xy) {
+// ---------------------------------------------------------------- groups of ranks
+// A Group is the set of ranks one call drives: {self} for a normal context (one process per
+// GPU), whose exchanges are NCCL calls; or all p virtual ranks of one process on one device
+// (tfdp_group_step / tfdp_group_forces), whose exchanges are device copies on their shared
+// stream.  Either way the same kernels run in the same phases.
+struct Group {
+  tfdp_ctx** c;
+  int p;
+  tfdp_ctx* operator[](int i) const { return c[i]; }
+  bool virt() const { return p > 1; }
+};
+
+// d2d copy on the ctx stream (virtual exchanges; NCCL self-messages)
+tfdp_status dcopy(tfdp_ctx* c, void* dst, const void* src, size_t bytes) {
+  if (bytes == 0) return TFDP_OK;
+  CUDA_TRY(c, cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, c->stream));
+  return TFDP_OK;
+}
+
+// Position all-gather: every rank's own slice [lo, hi) of xy (the update's output buffer)
+// to every other rank.
+tfdp_status exchange_positions(const Group& G, int buf) {
+  tfdp_ctx* c = G[0];
   if (c->world == 1) return TFDP_OK;
+  if (G.virt()) {
+    for (int r = 0; r < G.p; ++r)
+      for (int s = 0; s < G.p; ++s)
+        if (s != r)
+          TRY(dcopy(G[s], G[s]->xy[buf] + G[r]->lo, G[r]->xy[buf] + G[r]->lo,
+                    (G[r]->hi - G[r]->lo) * sizeof(float2)));
+    return TFDP_OK;
+  }
   if (!c->comm)
     return fail(c, TFDP_ERR_UNSUPPORTED,
-                "virtual shard context (no NCCL id): only tfdp_forces is available");
+                "virtual shard context (no NCCL id): use tfdp_group_step / tfdp_group_forces");
+  float2* xy = c->xy[buf];
   Scope sc(c, K_COMM);
   NCCL_TRY(c, c->nccl->GroupStart());
   for (int r = 0; r < c->world; ++r) {
@@ -502,18 +565,177 @@ tfdp_status exchange_positions(tfdp_ctx* c, float2* xy) {
   return TFDP_OK;
 }
 
-// ---------------------------------------------------------------- one evaluation
-// update = 1: x_{t+1} into xy[cur^1] (own shard), exchange; update = 0: forces to rep/att.
-tfdp_status evaluate(tfdp_ctx* c, int update, float eta, int k) {
-  const int64_t n_local = c->hi - c->lo;
-  float2* xy = c->xy[c->cur];
-  float2* xyn = c->xy[c->cur ^ 1];
+// Same for an int array (the new permutation of a renumbering, root rank 0 only).
+tfdp_status exchange_perm(const Group& G) {
+  tfdp_ctx* c = G[0];
+  if (c->world == 1) return TFDP_OK;
+  if (G.virt()) {
+    for (int s = 1; s < G.p; ++s) TRY(dcopy(G[s], G[s]->perm2, G[0]->perm2, c->n * sizeof(int)));
+    return TFDP_OK;
+  }
+  Scope sc(c, K_COMM);
+  NCCL_TRY(c, c->nccl->Broadcast(c->perm2, c->perm2, (size_t)c->n, ncclInt32, 0, c->comm, c->stream));
+  return TFDP_OK;
+}
+
+// ---- slab mode layout helpers (kernels_dist.cu): float2 offsets
+int64_t slab_nrt(const tfdp::SlabPlan& pl, int r) { return (pl.row0[r + 1] - pl.row0[r]) / 8; }
+int64_t slab_nq(const tfdp::SlabPlan& pl, int s) { return pl.q0[s + 1] - pl.q0[s]; }
+// xa segment (dest s, channel ch) of a rank whose slab has nrt row tiles
+int64_t xa_seg(const tfdp::SlabPlan& pl, int64_t nrt, int s, int ch) {
+  return 3 * nrt * 8 * pl.q0[s] + ch * nrt * slab_nq(pl, s) * 8;
+}
+// xb block (rows of rank r, channel ch) of column-chunk owner me
+int64_t xb_blk(const tfdp::SlabPlan& pl, int me, int r, int ch) {
+  return ((int64_t)ch * (pl.R / 8) + pl.row0[r] / 8) * slab_nq(pl, me) * 8;
+}
+
+// Exchange 1 (dir = 0): row-pass output segments xa -> column-chunk blocks xb.
+// Exchange 2 (dir = 1): column-pass output blocks xb -> segments xa of the row owners.
+// Message (src r -> dst s, channel ch) holds nrt(row rank) x nq(column rank) x 8 float2.
+tfdp_status exchange_slabs(const Group& G, int k, int dir) {
+  tfdp_ctx* c = G[0];
+  const int p = c->world;
+  auto msg = [&](tfdp_ctx* cr, tfdp_ctx* cs, int r, int s, int ch, float2** src, float2** dst,
+                 int64_t* cnt) {
+    const tfdp::SlabPlan& pl = c->plan[k];
+    if (dir == 0) {  // r = row owner, s = column owner
+      *cnt = slab_nrt(pl, r) * slab_nq(pl, s) * 8;
+      *src = cr ? cr->xa + xa_seg(pl, slab_nrt(pl, r), s, ch) : nullptr;
+      *dst = cs ? cs->xb + xb_blk(pl, s, r, ch) : nullptr;
+    } else {  // r = column owner, s = row owner
+      *cnt = slab_nrt(pl, s) * slab_nq(pl, r) * 8;
+      *src = cr ? cr->xb + xb_blk(pl, r, s, ch) : nullptr;
+      *dst = cs ? cs->xa + xa_seg(pl, slab_nrt(pl, s), r, ch) : nullptr;
+    }
+  };
+  if (G.virt()) {
+    for (int r = 0; r < p; ++r)
+      for (int s = 0; s < p; ++s)
+        for (int ch = 0; ch < 3; ++ch) {
+          float2 *src, *dst;
+          int64_t cnt;
+          msg(G[r], G[s], r, s, ch, &src, &dst, &cnt);
+          TRY(dcopy(G[s], dst, src, cnt * sizeof(float2)));
+        }
+    return TFDP_OK;
+  }
+  const int me = c->rank;
+  Scope sc(c, K_COMM);
+  for (int ch = 0; ch < 3; ++ch) {  // self-message: a device copy
+    float2 *src, *dst;
+    int64_t cnt;
+    msg(c, c, me, me, ch, &src, &dst, &cnt);
+    TRY(dcopy(c, dst, src, cnt * sizeof(float2)));
+  }
+  NCCL_TRY(c, c->nccl->GroupStart());
+  for (int o = 0; o < p; ++o) {
+    if (o == me) continue;
+    for (int ch = 0; ch < 3; ++ch) {
+      float2 *src, *dst;
+      int64_t cnt;
+      msg(c, nullptr, me, o, ch, &src, &dst, &cnt);  // me -> o
+      if (cnt > 0) NCCL_TRY(c, c->nccl->Send(src, (size_t)cnt * 2, ncclFloat, o, c->comm, c->stream));
+      msg(nullptr, c, o, me, ch, &src, &dst, &cnt);  // o -> me
+      if (cnt > 0) NCCL_TRY(c, c->nccl->Recv(dst, (size_t)cnt * 2, ncclFloat, o, c->comm, c->stream));
+    }
+  }
+  NCCL_TRY(c, c->nccl->GroupEnd());
+  return TFDP_OK;
+}
+
+// Exchange 3: every rank's slab rows of the three potential planes to every rank (the
+// gather of a rank's nodes may read any row).
+tfdp_status exchange_phi(const Group& G, int k) {
+  tfdp_ctx* c = G[0];
+  const tfdp::SlabPlan& pl = c->plan[k];
+  const int64_t plane = (int64_t)c->cpitch * c->cpitch;
+  auto rows = [&](int r) {
+    return std::max<int64_t>(0, std::min<int64_t>(pl.row0[r + 1], c->cpitch) - pl.row0[r]);
+  };
+  if (G.virt()) {
+    for (int r = 0; r < G.p; ++r)
+      for (int s = 0; s < G.p; ++s)
+        if (s != r)
+          for (int ch = 0; ch < 3; ++ch) {
+            const int64_t off = ch * plane + (int64_t)pl.row0[r] * c->cpitch;
+            TRY(dcopy(G[s], G[s]->phi + off, G[r]->phi + off, rows(r) * c->cpitch * sizeof(float)));
+          }
+    return TFDP_OK;
+  }
+  Scope sc(c, K_COMM);
+  NCCL_TRY(c, c->nccl->GroupStart());
+  for (int r = 0; r < c->world; ++r)
+    for (int ch = 0; ch < 3; ++ch) {
+      const int64_t cnt = rows(r) * c->cpitch;
+      float* b = c->phi + ch * plane + (int64_t)pl.row0[r] * c->cpitch;
+      if (cnt > 0) NCCL_TRY(c, c->nccl->Broadcast(b, b, (size_t)cnt, ncclFloat, r, c->comm, c->stream));
+    }
+  NCCL_TRY(c, c->nccl->GroupEnd());
+  return TFDP_OK;
+}
+
+int pdl_max_fft() {
+  static const int v = [] {  // TFDP_PDL_MAX_FFT overrides the threshold (A/B runs)
+    const char* e = getenv("TFDP_PDL_MAX_FFT");
+    return e ? atoi(e) : tfdp::kPdlMaxFft;
+  }();
+  return v;
+}
+
+// bbox (when the box is not known) + setup + the kernel spectrum forked on the side stream
+void fft_prologue(tfdp_ctx* c, int k, bool* overlap) {
+  const int P = c->P_of_k[k];
+  tfdp::set_pdl_active(P <= pdl_max_fft());
+  if (!c->box_valid || c->world > 1) {
+    Scope sc(c, K_BBOX, nullptr, 2);  // reset_slots + bbox
+    tfdp::launch_reset_slots(c->box_part, c->stream);
+    c->n_part = tfdp::launch_bbox(c->xy[c->cur], c->n, c->box_part, c->stream);
+  }
+  {
+    Scope sc(c, K_SETUP);
+    tfdp::launch_setup(c->box_part, c->n_part, c->keys, c->geom, k, c->p.n_int_min,
+                       c->p.n_int_fixed, c->cap_of_k[k], P, c->cpitch, c->capped,
+                       c->p.interval_rule, c->fa.gamma, c->kkey, c->stream);
+  }
+  // The kernel spectrum needs only the geometry: fork it onto the side stream so it overlaps
+  // spread + rows_fwd (both latency-bound); cols joins on it.  Its kernels exit at once
+  // unless setup found the held spectrum stale (a new P, h or gamma: under R5' h = 1/k,
+  // so a run recomputes it when k switches or the grid is re-planned).
+  // (in line while kspec itself is being timed, so that its events measure the kernel
+  // rather than its wait for SMs)
+  *overlap = c->kspec_overlap && !((c->prof_mask >> K_KSPEC) & 1u);
+  cudaStream_t ks = *overlap ? c->side : c->stream;
+  if (*overlap) {
+    cudaEventRecord(c->ev_fork, c->stream);
+    cudaStreamWaitEvent(c->side, c->ev_fork, 0);
+  }
+  {
+    Scope sc(c, K_KSPEC, ks, 2);  // kspec_rows + kspec_cols
+    tfdp::launch_kspec(c->geom, P, c->fa, c->tw[k], c->ka, c->kh, ks);
+  }
+  if (*overlap) cudaEventRecord(c->ev_join, c->side);
+}
+
+tfdp::FocusArgs focus_prologue(tfdp_ctx* c) {
   tfdp::FocusArgs fo{nullptr, nullptr, 1.f, 1.f, 1.f};
   if (c->focus_on) {  // exact repulsion sum over the focal region's sources (R23)
-    tfdp::launch_focus_s1(xy, c->lo, n_local, c->region_slot, c->region_m, c->fa, c->s1, c->stream);
+    tfdp::launch_focus_s1(c->xy[c->cur], c->lo, c->hi - c->lo, c->region_slot, c->region_m, c->fa,
+                          c->s1, c->stream);
     c->launches++;
     fo = tfdp::FocusArgs{c->label_slot, c->s1, c->fo_la, c->fo_lf, c->fo_ls};
   }
+  return fo;
+}
+
+// ---------------------------------------------------------------- one evaluation, one rank
+// update = 1: x_{t+1} into xy[cur^1] (own shard); update = 0: forces to rep/att.  (The
+// position exchange and the buffer flip are the caller's, evaluate().)
+tfdp_status evaluate_one(tfdp_ctx* c, int update, float eta, int k) {
+  const int64_t n_local = c->hi - c->lo;
+  float2* xy = c->xy[c->cur];
+  float2* xyn = c->xy[c->cur ^ 1];
+  const tfdp::FocusArgs fo = focus_prologue(c);
   if (c->p.solver == TFDP_EXACT) {
     {
       Scope sc(c, K_EXACT_PARTIAL);
@@ -532,40 +754,9 @@ tfdp_status evaluate(tfdp_ctx* c, int update, float eta, int k) {
       return fail(c, TFDP_ERR_UNSUPPORTED, "grid all-reduce needs an NCCL communicator");
     const int P = c->P_of_k[k];
     const int mcap = c->cap_of_k[k] * k;
-    static const int pdl_max = [] {  // TFDP_PDL_MAX_FFT overrides the threshold (A/B runs)
-      const char* e = getenv("TFDP_PDL_MAX_FFT");
-      return e ? atoi(e) : tfdp::kPdlMaxFft;
-    }();
-    tfdp::set_pdl_active(P <= pdl_max);
     const float2* tw = c->tw[k];
-    if (!c->box_valid || c->world > 1) {
-      Scope sc(c, K_BBOX, nullptr, 2);  // reset_slots + bbox
-      tfdp::launch_reset_slots(c->box_part, c->stream);
-      c->n_part = tfdp::launch_bbox(xy, c->n, c->box_part, c->stream);
-    }
-    {
-      Scope sc(c, K_SETUP);
-      tfdp::launch_setup(c->box_part, c->n_part, c->keys, c->geom, k, c->p.n_int_min,
-                         c->p.n_int_fixed, c->cap_of_k[k], P, c->cpitch, c->capped,
-                         c->p.interval_rule, c->fa.gamma, c->kkey, c->stream);
-    }
-    // The kernel spectrum needs only the geometry: fork it onto the side stream so it overlaps
-    // spread + rows_fwd (both latency-bound); cols joins on it.  Its kernels exit at once
-    // unless setup found the held spectrum stale (a new P, h or gamma: under R5' h = 1/k,
-    // so a run recomputes it when k switches or the grid is re-planned).
-    // (in line while kspec itself is being timed, so that its events measure the kernel
-    // rather than its wait for SMs)
-    const bool overlap = c->kspec_overlap && !((c->prof_mask >> K_KSPEC) & 1u);
-    cudaStream_t ks = overlap ? c->side : c->stream;
-    if (overlap) {
-      CUDA_TRY(c, cudaEventRecord(c->ev_fork, c->stream));
-      CUDA_TRY(c, cudaStreamWaitEvent(c->side, c->ev_fork, 0));
-    }
-    {
-      Scope sc(c, K_KSPEC, ks, 2);  // kspec_rows + kspec_cols
-      tfdp::launch_kspec(c->geom, P, c->fa, tw, c->ka, c->kh, ks);
-    }
-    if (overlap) CUDA_TRY(c, cudaEventRecord(c->ev_join, c->side));
+    bool overlap;
+    fft_prologue(c, k, &overlap);
     // The charges are all-zero here: they start zeroed and rows_inv clears the rows rows_fwd
     // consumed (no separate zeroing pass).
     float4* grid4 = reinterpret_cast<float4*>(c->grid);
@@ -589,17 +780,18 @@ tfdp_status evaluate(tfdp_ctx* c, int update, float eta, int k) {
     }
     {
       Scope sc(c, K_ROWS_FWD);
-      tfdp::launch_rows_fwd(c->geom, grid4, c->cpitch, P, mcap, tw, c->ca, c->ca_pitch, c->stream);
+      tfdp::launch_rows_fwd(c->geom, grid4, c->cpitch, P, 0, mcap, tw, c->ca, c->ca_pitch,
+                            c->stream);
     }
     if (overlap) CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_join, 0));
     {
       Scope sc(c, K_COLS);
-      tfdp::launch_cols(c->geom, c->ca, c->ca_pitch, c->kh, P, tw, c->stream);
+      tfdp::launch_cols(c->geom, c->ca, c->ca_pitch, c->kh, P, tw, 0, P / 2 + 1, c->stream);
     }
     {
       Scope sc(c, K_ROWS_INV);
-      tfdp::launch_rows_inv(c->geom, c->ca, c->ca_pitch, P, mcap, tw, c->phi, c->cpitch, grid4,
-                            c->stream);
+      tfdp::launch_rows_inv(c->geom, c->ca, c->ca_pitch, P, 0, mcap, tw, c->phi, c->cpitch,
+                            grid4, c->stream);
     }
     {
       Scope sc(c, K_GATHER_UPDATE);
@@ -612,9 +804,85 @@ tfdp_status evaluate(tfdp_ctx* c, int update, float eta, int k) {
     c->box_valid = update && c->world == 1;
   }
   CUDA_TRY(c, cudaGetLastError());
+  return TFDP_OK;
+}
+
+// ---------------------------------------------------------------- slab mode (p > 1, ibFFT)
+// Per iteration, every rank r: box + setup from the full positions; spread of
+// the nodes in its grid-row slab; row FFTs of that slab; transpose 1; column pass on its
+// column chunk; transpose 2; inverse row FFTs of its slab -> potentials of its slab rows;
+// potential exchange; gather + attraction + update of its own node shard; position
+// all-gather.  Each phase runs on every rank of the group before the next exchange.
+tfdp_status evaluate_slab(const Group& G, int update, float eta, int k) {
+  bool overlap[tfdp::kMaxWorld];
+  for (int i = 0; i < G.p; ++i) {  // phase A: ... rows_fwd of the slab, pack
+    tfdp_ctx* c = G[i];
+    const tfdp::SlabPlan& pl = c->plan[k];
+    const int P = c->P_of_k[k], r = c->rank;
+    fft_prologue(c, k, &overlap[i]);
+    float4* grid4 = reinterpret_cast<float4*>(c->grid);
+    {
+      Scope sc(c, K_SPREAD);
+      tfdp::launch_spread(c->xy[c->cur], 0, c->n, c->geom, k, grid4, c->stream,
+                          pl.row0[r] / k, pl.row0[r + 1] / k);
+    }
+    {
+      Scope sc(c, K_ROWS_FWD);
+      tfdp::launch_rows_fwd(c->geom, grid4, c->cpitch, P, pl.row0[r], pl.row0[r + 1], c->tw[k],
+                            c->ca, c->ca_pitch, c->stream);
+      tfdp::launch_pack_slab(c->ca, c->ca_pitch, pl, c->xa, c->stream);
+      c->launches++;
+    }
+  }
+  TRY(exchange_slabs(G, k, 0));
+  for (int i = 0; i < G.p; ++i) {  // phase B: column pass on the chunk (in place in xb)
+    tfdp_ctx* c = G[i];
+    const tfdp::SlabPlan& pl = c->plan[k];
+    if (overlap[i]) CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+    Scope sc(c, K_COLS);
+    tfdp::launch_cols(c->geom, c->xb, pl.R, c->kh, c->P_of_k[k], c->tw[k], pl.q0[c->rank],
+                      pl.q0[c->rank + 1], c->stream);
+  }
+  TRY(exchange_slabs(G, k, 1));
+  for (int i = 0; i < G.p; ++i) {  // phase C: unpack, inverse rows of the slab -> Phi rows
+    tfdp_ctx* c = G[i];
+    const tfdp::SlabPlan& pl = c->plan[k];
+    const int r = c->rank;
+    Scope sc(c, K_ROWS_INV);
+    tfdp::launch_unpack_slab(c->xa, pl, c->ca, c->ca_pitch, c->stream);
+    c->launches++;
+    tfdp::launch_rows_inv(c->geom, c->ca, c->ca_pitch, c->P_of_k[k], pl.row0[r], pl.row0[r + 1],
+                          c->tw[k], c->phi, c->cpitch, reinterpret_cast<float4*>(c->grid),
+                          c->stream);
+  }
+  TRY(exchange_phi(G, k));
+  for (int i = 0; i < G.p; ++i) {  // phase D: gather + attraction + update of the own nodes
+    tfdp_ctx* c = G[i];
+    const tfdp::FocusArgs fo = focus_prologue(c);
+    Scope sc(c, K_GATHER_UPDATE);
+    tfdp::launch_gather_update(c->xy[c->cur], c->xy[c->cur ^ 1], c->lo, c->hi - c->lo, c->geom, k,
+                               c->phi, c->row_ptr, c->col, c->fa, fo, eta, c->t, update, c->rep,
+                               c->att, c->diverge, nullptr, c->stream);
+    c->box_valid = false;
+    CUDA_TRY(c, cudaGetLastError());
+  }
+  return TFDP_OK;
+}
+
+// One evaluation of the whole group (+ the position exchange and buffer flip on update).
+tfdp_status evaluate(const Group& G, int update, float eta, int k) {
+  tfdp_ctx* c0 = G[0];
+  if (c0->p.solver == TFDP_IBFFT && c0->slab) {
+    if (!G.virt() && !c0->comm)
+      return fail(c0, TFDP_ERR_UNSUPPORTED,
+                  "slab mode of a virtual shard context: use tfdp_group_step / tfdp_group_forces");
+    TRY(evaluate_slab(G, update, eta, k));
+  } else {
+    for (int i = 0; i < G.p; ++i) TRY(evaluate_one(G[i], update, eta, k));
+  }
   if (update) {
-    TRY(exchange_positions(c, xyn));
-    c->cur ^= 1;
+    TRY(exchange_positions(G, c0->cur ^ 1));
+    for (int i = 0; i < G.p; ++i) G[i]->cur ^= 1;
   }
   return TFDP_OK;
 }
@@ -657,31 +925,42 @@ tfdp_status check_status(tfdp_ctx* c, bool* capped) {
 }
 
 // Internal Morton renumbering of the nodes (kernels_reorder.cu): box -> keys -> counting
-// sort -> positions, permutation and CSR rebuilt in the new order.  Stream-ordered, no sync.
-tfdp_status reorder_nodes(tfdp_ctx* c) {
-  Scope sc(c, K_REORDER);
-  if (!c->box_valid) {  // else the slots already hold the box of the current positions
-    tfdp::launch_reset_slots(c->box_part, c->stream);
-    tfdp::launch_bbox(c->xy[c->cur], c->n, c->box_part, c->stream);
-    c->launches += 2;
+// sort -> the new permutation (rank 0; broadcast at p > 1 so that every rank holds the same
+// internal order) -> positions, inverse and CSR rebuilt in the new order.  Stream-ordered.
+tfdp_status reorder_nodes(const Group& G) {
+  for (int i = 0; i < G.p; ++i) {
+    tfdp_ctx* c = G[i];
+    if (c->rank != 0) continue;
+    Scope sc(c, K_REORDER);
+    if (!c->box_valid) {  // else the slots already hold the box of the current positions
+      tfdp::launch_reset_slots(c->box_part, c->stream);
+      tfdp::launch_bbox(c->xy[c->cur], c->n, c->box_part, c->stream);
+      c->launches += 2;
+    }
+    // reduce without consuming: the box is permutation invariant, the next setup reuses it
+    tfdp::launch_box_reduce(c->box_part, tfdp::kBoxSlots, c->keys, c->stream, /*reset=*/false);
+    c->launches += tfdp::launch_reorder_perm(c->xy[c->cur], c->keys, c->perm, c->perm2, c->n,
+                                             c->rscratch, c->stream);
   }
-  // reduce without consuming: the box is permutation invariant, the next setup reuses it
-  tfdp::launch_box_reduce(c->box_part, tfdp::kBoxSlots, c->keys, c->stream, /*reset=*/false);
-  const int nk = tfdp::launch_reorder(c->xy[c->cur], c->xy[c->cur ^ 1], c->keys, c->perm, c->perm2,
-                                      c->inv2, c->row_ptr_o, c->col_o, c->row_ptr, c->col, c->n,
-                                      c->rscratch, c->stream);
-  c->launches += nk;  // (the scope counts box_reduce)
-  std::swap(c->perm, c->perm2);
-  std::swap(c->inv, c->inv2);
-  c->cur ^= 1;
-  if (c->focus_on) {  // the mask follows the renumbering
-    tfdp::launch_focus_slots(c->label_caller, c->perm, c->inv, c->n, c->region_caller,
-                             c->region_m, c->label_slot, c->region_slot, c->stream);
-    c->launches += c->region_m > 0 ? 2 : 1;
+  TRY(exchange_perm(G));
+  for (int i = 0; i < G.p; ++i) {
+    tfdp_ctx* c = G[i];
+    Scope sc(c, K_REORDER, nullptr, 0);
+    c->launches += tfdp::launch_reorder_apply(c->xy[c->cur], c->xy[c->cur ^ 1], c->inv, c->perm2,
+                                              c->inv2, c->row_ptr_o, c->col_o, c->row_ptr, c->col,
+                                              c->n, c->rscratch, c->stream);
+    std::swap(c->perm, c->perm2);
+    std::swap(c->inv, c->inv2);
+    c->cur ^= 1;
+    if (c->focus_on) {  // the mask follows the renumbering
+      tfdp::launch_focus_slots(c->label_caller, c->perm, c->inv, c->n, c->region_caller,
+                               c->region_m, c->label_slot, c->region_slot, c->stream);
+      c->launches += c->region_m > 0 ? 2 : 1;
+    }
+    c->box_valid = c->world == 1 && c->rank == 0;
+    c->n_part = tfdp::kBoxSlots;
+    CUDA_TRY(c, cudaGetLastError());
   }
-  c->box_valid = true;
-  c->n_part = tfdp::kBoxSlots;
-  CUDA_TRY(c, cudaGetLastError());
   return TFDP_OK;
 }
 
@@ -741,6 +1020,117 @@ tfdp_status maybe_replan(tfdp_ctx* c, bool capped) {
   return replan_from_device(c);
 }
 
+// ---------------------------------------------------------------- step / forces of a group
+// The iteration loop of tfdp_step (one context) and tfdp_group_step (the virtual ranks of
+// one process): the ranks advance in lockstep; every rank holds the same t and schedule.
+tfdp_status step_impl(const Group& G, int32_t n_iters) {
+  tfdp_ctx* c = G[0];
+  const int T = c->p.iterations;
+  if (c->p.cooling == TFDP_COOL_LINEAR && c->t + n_iters > T)
+    return fail(c, TFDP_ERR_STATE, "iteration %d + %d exceeds T = %d under linear cooling",
+                c->t, n_iters, T);
+  // locality: renumber at the first call, then whenever 64 iterations ran since the last one
+  if (c->reorder && n_iters >= 8 && (c->reordered_at < 0 || c->iters_run - c->reordered_at >= 64)) {
+    TRY(reorder_nodes(G));
+    for (int i = 0; i < G.p; ++i) G[i]->reordered_at = c->iters_run;
+  }
+  for (int i = 0; i < G.p; ++i) G[i]->iters_run += n_iters;
+  int done = 0;
+  while (done < n_iters) {
+    const int block = std::min(n_iters - done, 32);  // host check every 32 iterations
+    for (int b = 0; b < block; ++b) {
+      const double eta = c->p.cooling == TFDP_COOL_LINEAR
+                             ? c->p.step0 * (1.0 - (double)c->t / T)  // R2, S:352
+                             : c->p.step0;                            // R2'
+      TRY(evaluate(G, 1, (float)eta, k_at(c, c->t)));
+      for (int i = 0; i < G.p; ++i) G[i]->t++;
+    }
+    done += block;
+    for (int i = 0; i < G.p; ++i) {
+      bool capped = false;
+      TRY(check_status(G[i], &capped));
+      TRY(maybe_replan(G[i], capped));
+    }
+  }
+  return TFDP_OK;
+}
+
+// Forces of every rank's shard to outs[i] (host or device, caller order).  A renumbered
+// multi-rank context computes the internal slots [lo, hi); the caller's nodes [lo, hi) are
+// spread over all ranks: gather all shards, un-permute, cut the caller range.
+tfdp_status shard_out(const Group& G, bool att, float* const* outs) {
+  tfdp_ctx* c0 = G[0];
+  if (!(c0->reorder && c0->world > 1)) {
+    for (int i = 0; i < G.p; ++i)
+      if (outs[i]) TRY(copy_out(G[i], att ? G[i]->att : G[i]->rep, outs[i], G[i]->hi - G[i]->lo));
+    return TFDP_OK;
+  }
+  for (int i = 0; i < G.p; ++i)
+    if (!G[i]->fbuf) CUDA_TRY(G[i], cudaMalloc(&G[i]->fbuf, G[i]->n * sizeof(float2)));
+  if (G.virt()) {
+    for (int r = 0; r < G.p; ++r)
+      for (int s = 0; s < G.p; ++s)
+        TRY(dcopy(G[s], G[s]->fbuf + G[r]->lo, att ? G[r]->att : G[r]->rep,
+                  (G[r]->hi - G[r]->lo) * sizeof(float2)));
+  } else {
+    tfdp_ctx* c = c0;
+    TRY(dcopy(c, c->fbuf + c->lo, att ? c->att : c->rep, (c->hi - c->lo) * sizeof(float2)));
+    NCCL_TRY(c, c->nccl->GroupStart());
+    for (int r = 0; r < c->world; ++r) {
+      int64_t lo, hi;
+      tfdp_shard_range(c->n, c->world, r, &lo, &hi);
+      if (hi > lo)
+        NCCL_TRY(c, c->nccl->Broadcast(c->fbuf + lo, c->fbuf + lo, (size_t)(hi - lo) * 2, ncclFloat,
+                                       r, c->comm, c->stream));
+    }
+    NCCL_TRY(c, c->nccl->GroupEnd());
+  }
+  for (int i = 0; i < G.p; ++i) {
+    tfdp_ctx* c = G[i];
+    if (!outs[i]) continue;
+    tfdp::launch_unpermute(c->fbuf, c->perm, c->n, c->iobuf, c->stream);
+    c->launches++;
+    const bool d = is_device_ptr(outs[i]);
+    CUDA_TRY(c, cudaMemcpyAsync(outs[i], c->iobuf + c->lo, (c->hi - c->lo) * sizeof(float2),
+                                d ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->stream));
+    if (!d) CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  }
+  return TFDP_OK;
+}
+
+tfdp_status forces_impl(const Group& G, float* const* rep, float* const* att) {
+  tfdp_ctx* c = G[0];
+  TRY(evaluate(G, 0, 0.f, k_at(c, c->t)));
+  for (int i = 0; i < G.p; ++i) G[i]->box_valid = false;  // setup consumed the box keys
+  TRY(shard_out(G, false, rep));
+  TRY(shard_out(G, true, att));
+  for (int i = 0; i < G.p; ++i) {
+    bool capped = false;
+    TRY(check_status(G[i], &capped));
+    TRY(maybe_replan(G[i], capped));
+    G[i]->box_valid = false;
+  }
+  return TFDP_OK;
+}
+
+// Validates the virtual ranks of a group call: all contexts of one world, in rank order,
+// without a communicator, on one stream, of one problem.
+tfdp_status group_check(tfdp_ctx* const* ctxs, int32_t p) {
+  if (!ctxs || p < 1 || p > tfdp::kMaxWorld || !ctxs[0])
+    return fail(nullptr, TFDP_ERR_ARG, "group: need 1 <= p <= %d contexts", tfdp::kMaxWorld);
+  for (int i = 0; i < p; ++i) {
+    tfdp_ctx* c = ctxs[i];
+    if (!c) return fail(ctxs[0], TFDP_ERR_ARG, "group: context %d is NULL", i);
+    if (c->errored) return fail(ctxs[0], TFDP_ERR_STATE, "context %d is errored: %s", i, c->err.c_str());
+    if (c->world != p || c->rank != i || c->comm)
+      return fail(ctxs[0], TFDP_ERR_ARG, "group: context %d must be virtual rank %d of world %d", i, i, p);
+    if (c->stream != ctxs[0]->stream || c->n != ctxs[0]->n || c->p.solver != ctxs[0]->p.solver ||
+        c->p.dist_mode != ctxs[0]->p.dist_mode || c->t != ctxs[0]->t)
+      return fail(ctxs[0], TFDP_ERR_ARG, "group: contexts must share stream, n, solver, dist_mode, t");
+  }
+  return TFDP_OK;
+}
+
 }  // namespace
 
 // =============================================================================== C ABI
@@ -763,7 +1153,7 @@ tfdp_status tfdp_params_default(tfdp_params* p) {
   p->iterations = 300;
   p->t0 = 0;
   p->cooling = TFDP_COOL_LINEAR;
-  p->dist_mode = TFDP_DIST_SPREAD_ALL;
+  p->dist_mode = TFDP_DIST_SLAB;
   p->node_order = TFDP_ORDER_AUTO;
   return TFDP_OK;
 }
@@ -914,8 +1304,13 @@ tfdp_status tfdp_init(tfdp_ctx** out, int64_t n, const int64_t* row_ptr, const i
     c->n_chunks = (int)((n + ch - 1) / ch);
     ALLOC(c->part, (size_t)c->n_chunks * std::max<int64_t>(n_local, 1) * sizeof(double2));
   }
-  c->reorder = p.solver == TFDP_IBFFT && p.node_order == TFDP_ORDER_AUTO && c->world == 1 &&
-               n >= 65536;
+  c->slab = c->world > 1 && p.solver == TFDP_IBFFT && p.dist_mode == TFDP_DIST_SLAB;
+  if (c->slab && c->world > tfdp::kMaxWorld)
+    return bail(fail(c, TFDP_ERR_ARG, "slab mode supports world <= %d", tfdp::kMaxWorld));
+  // internal renumbering: one GPU, or the slab mode (every rank renumbers identically: rank
+  // 0's permutation is broadcast)
+  c->reorder = p.solver == TFDP_IBFFT && p.node_order == TFDP_ORDER_AUTO && n >= 65536 &&
+               (c->world == 1 || c->slab);
   if (c->reorder) {
     ALLOC(c->perm, n * sizeof(int));
     ALLOC(c->inv, n * sizeof(int));
@@ -987,47 +1382,49 @@ tfdp_status tfdp_step(tfdp_ctx* c, int32_t n_iters) {
   if (c->errored) return fail(c, TFDP_ERR_STATE, "context is errored: %s", c->err.c_str());
   if (n_iters < 0) return fail(c, TFDP_ERR_ARG, "n_iters < 0");
   cudaSetDevice(c->device);
-  const int T = c->p.iterations;
-  if (c->p.cooling == TFDP_COOL_LINEAR && c->t + n_iters > T)
-    return fail(c, TFDP_ERR_STATE, "iteration %d + %d exceeds T = %d under linear cooling",
-                c->t, n_iters, T);
-  // locality: renumber at the first call, then whenever 64 iterations ran since the last one
-  if (c->reorder && n_iters >= 8 && (c->reordered_at < 0 || c->iters_run - c->reordered_at >= 64)) {
-    TRY(reorder_nodes(c));
-    c->reordered_at = c->iters_run;
-  }
-  c->iters_run += n_iters;
-  int done = 0;
-  while (done < n_iters) {
-    const int block = std::min(n_iters - done, 32);  // host check every 32 iterations
-    for (int b = 0; b < block; ++b) {
-      const double eta = c->p.cooling == TFDP_COOL_LINEAR
-                             ? c->p.step0 * (1.0 - (double)c->t / T)  // R2, S:352
-                             : c->p.step0;                            // R2'
-      TRY(evaluate(c, 1, (float)eta, k_at(c, c->t)));
-      c->t++;
-    }
-    done += block;
-    bool capped = false;
-    TRY(check_status(c, &capped));
-    TRY(maybe_replan(c, capped));
-  }
-  return TFDP_OK;
+  tfdp_ctx* one[1] = {c};
+  return step_impl(Group{one, 1}, n_iters);
 }
 
 tfdp_status tfdp_forces(tfdp_ctx* c, float* rep_xy, float* att_xy) {
   if (!c) return fail(nullptr, TFDP_ERR_ARG, "ctx is NULL");
   if (c->errored) return fail(c, TFDP_ERR_STATE, "context is errored: %s", c->err.c_str());
   cudaSetDevice(c->device);
-  TRY(evaluate(c, 0, 0.f, k_at(c, c->t)));
-  c->box_valid = false;  // setup consumed the box keys without an update
-  const int64_t n_local = c->hi - c->lo;
-  if (rep_xy) TRY(copy_out(c, c->rep, rep_xy, n_local));
-  if (att_xy) TRY(copy_out(c, c->att, att_xy, n_local));
-  bool capped = false;
-  TRY(check_status(c, &capped));
-  TRY(maybe_replan(c, capped));
-  c->box_valid = false;
+  tfdp_ctx* one[1] = {c};
+  float* r[1] = {rep_xy};
+  float* a[1] = {att_xy};
+  return forces_impl(Group{one, 1}, r, a);
+}
+
+tfdp_status tfdp_group_step(tfdp_ctx* const* ctxs, int32_t p, int32_t n_iters) {
+  TRY(group_check(ctxs, p));
+  if (n_iters < 0) return fail(ctxs[0], TFDP_ERR_ARG, "n_iters < 0");
+  cudaSetDevice(ctxs[0]->device);
+  return step_impl(Group{const_cast<tfdp_ctx**>(ctxs), p}, n_iters);
+}
+
+tfdp_status tfdp_group_forces(tfdp_ctx* const* ctxs, int32_t p, float* const* rep_xy,
+                              float* const* att_xy) {
+  TRY(group_check(ctxs, p));
+  cudaSetDevice(ctxs[0]->device);
+  std::vector<float*> r(p, nullptr), a(p, nullptr);
+  for (int i = 0; i < p; ++i) {
+    if (rep_xy) r[i] = rep_xy[i];
+    if (att_xy) a[i] = att_xy[i];
+  }
+  return forces_impl(Group{const_cast<tfdp_ctx**>(ctxs), p}, r.data(), a.data());
+}
+
+tfdp_status tfdp_slab_plan(int32_t rows, int32_t fft_size, int32_t world, int32_t* row0,
+                           int32_t* q0) {
+  if (rows < 1 || fft_size < 2 || fft_size % 2 || world < 1 || world > tfdp::kMaxWorld || !row0 || !q0)
+    return fail(nullptr, TFDP_ERR_ARG, "tfdp_slab_plan: bad arguments");
+  tfdp::SlabPlan pl;
+  tfdp::slab_plan(world, 0, rows, fft_size, &pl);
+  for (int r = 0; r <= world; ++r) {
+    row0[r] = pl.row0[r];
+    q0[r] = pl.q0[r];
+  }
   return TFDP_OK;
 }
 
@@ -1120,6 +1517,8 @@ tfdp_status tfdp_np1(tfdp_ctx* c, double* np1, int32_t* hits) {
     CUDA_TRY(c, cudaMalloc(&c->np_keys, sizeof(BoxKeys)));
     CUDA_TRY(c, cudaMalloc(&c->np_sum, sizeof(double)));
   }
+  if (hits && c->reorder && c->world > 1)
+    return fail(c, TFDP_ERR_UNSUPPORTED, "per-node hits of a renumbered multi-rank context");
   const float2* xy = c->xy[c->cur];
   tfdp::launch_reset_slots(c->np_slots, c->stream);
   const int np = tfdp::launch_bbox(xy, c->n, c->np_slots, c->stream);
@@ -1395,6 +1794,9 @@ void tfdp_destroy(tfdp_ctx* c) {
   cudaFree(c->region_caller);
   cudaFree(c->region_slot);
   cudaFree(c->s1);
+  cudaFree(c->xa);
+  cudaFree(c->xb);
+  cudaFree(c->fbuf);
   cudaFree(c->np_scratch);
   cudaFree(c->np_hits);
   cudaFree(c->np_hits2);

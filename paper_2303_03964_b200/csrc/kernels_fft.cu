@@ -255,16 +255,22 @@ __device__ __forceinline__ Cell cell_of(float2 p, const GridGeom& g) {
 template <int K>
 __global__ void __launch_bounds__(kNodeThreads)
 spread_kernel(const float2* __restrict__ xy, int64_t lo, int64_t cnt,
-              const GridGeom* __restrict__ geom, float4* __restrict__ grid) {
+              const GridGeom* __restrict__ geom, float4* __restrict__ grid, int by_lo,
+              int by_hi) {
   constexpr bool kAgg = K >= 2;
   pdl_wait();
   pdl_trigger();
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool active = t < cnt;
-  if (kAgg ? __all_sync(0xffffffffu, !active) : !active) return;
+  const bool in = t < cnt;
+  if (kAgg ? __all_sync(0xffffffffu, !in) : !in) return;
   const GridGeom g = *geom;
-  const float2 p = active ? xy[lo + t] : make_float2(g.cx, g.cy);
+  const float2 p = in ? xy[lo + t] : make_float2(g.cx, g.cy);
   const Cell c = cell_of(p, g);
+  // interval-row filter: the multi-GPU slab mode spreads, from all positions, exactly the
+  // nodes whose interval row lies in this rank's grid-row slab (by_lo = 0, by_hi = INT_MAX
+  // on one GPU)
+  const bool active = in && c.by >= by_lo && c.by < by_hi;
+  if (!kAgg && !active) return;
   float lx[K], ly[K];
   lagrange<K>(c.ux, lx);
   lagrange<K>(c.uy, ly);
@@ -453,9 +459,9 @@ bool spread_tiles() {
 }
 
 void launch_spread(const float2* xy, int64_t lo, int64_t cnt, const GridGeom* geom, int k,
-                   float4* grid, cudaStream_t s) {
+                   float4* grid, cudaStream_t s, int by_lo, int by_hi) {
   if (cnt <= 0) return;
-  if (spread_tiles()) {
+  if (spread_tiles() && by_lo == 0 && by_hi == INT32_MAX) {
 #define TFDP_ST(KK)                                                                          \
   {                                                                                          \
     constexpr int per = kNodeThreads * spread_tile_npt<KK>();                                \
@@ -476,9 +482,12 @@ void launch_spread(const float2* xy, int64_t lo, int64_t cnt, const GridGeom* ge
     return;
   }
   const unsigned blocks = (unsigned)((cnt + kNodeThreads - 1) / kNodeThreads);
-  if (k == 1) launch_chained(spread_kernel<1>, blocks, kNodeThreads, 0, s, xy, lo, cnt, geom, grid);
-  else if (k == 2) launch_chained(spread_kernel<2>, blocks, kNodeThreads, 0, s, xy, lo, cnt, geom, grid);
-  else launch_chained(spread_kernel<3>, blocks, kNodeThreads, 0, s, xy, lo, cnt, geom, grid);
+  if (k == 1)
+    launch_chained(spread_kernel<1>, blocks, kNodeThreads, 0, s, xy, lo, cnt, geom, grid, by_lo, by_hi);
+  else if (k == 2)
+    launch_chained(spread_kernel<2>, blocks, kNodeThreads, 0, s, xy, lo, cnt, geom, grid, by_lo, by_hi);
+  else
+    launch_chained(spread_kernel<3>, blocks, kNodeThreads, 0, s, xy, lo, cnt, geom, grid, by_lo, by_hi);
 }
 
 // ------------------------------------------------------------------ gather + update

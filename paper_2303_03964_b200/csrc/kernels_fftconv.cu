@@ -507,11 +507,13 @@ TFDP_FFT_KERNEL(kspec_cols_kernel)(const GridGeom* __restrict__ geom,
 // the inverse) in its last; the inverse FFT writes rows 0..M-1 from its last stage.
 TFDP_FFT_KERNEL(cols_kernel)(const GridGeom* __restrict__ geom, float2* __restrict__ CA,
                              int ca_pitch, const float* __restrict__ KH,
-                             const float2* __restrict__ tw) {
+                             const float2* __restrict__ tw, int q_base, int Hl) {
   TFDP_FFT_PROLOGUE
   const int M = geom->M;
   constexpr int half = P / 2;
-  const int u2 = blockIdx.x / 3, sub = blockIdx.x % 3;
+  // columns [q_base, q_base + Hl) live in CA (q_base even; the whole half spectrum on one
+  // GPU, a column chunk of it per rank in the multi-GPU slab mode)
+  const int u2 = q_base / 2 + blockIdx.x / 3, sub = blockIdx.x % 3;
   int chA, qA, chB, qB;
   if (sub == 0) {
     chA = 0, qA = 2 * u2, chB = 0, qB = 2 * u2 + 1;
@@ -519,11 +521,11 @@ TFDP_FFT_KERNEL(cols_kernel)(const GridGeom* __restrict__ geom, float2* __restri
     const int q = 2 * u2 + sub - 1;
     chA = 1, qA = q, chB = 2, qB = q;
   }
-  if (qA > half) return;
-  const bool hB = qB <= half;
-  constexpr int H = half + 1;
-  float2* colA = CA + ca_col_base(chA, qA, H, ca_pitch);
-  float2* colB = CA + ca_col_base(chB, hB ? qB : qA, H, ca_pitch);
+  if (qA > half || qA >= q_base + Hl) return;
+  const bool hB = qB <= half && qB < q_base + Hl;
+  const int H = Hl;
+  float2* colA = CA + ca_col_base(chA, qA - q_base, H, ca_pitch);
+  float2* colB = CA + ca_col_base(chB, (hB ? qB : qA) - q_base, H, ca_pitch);
   const float* khA = KH + (int64_t)qA * P;
   const float* khB = KH + (int64_t)(hB ? qB : qA) * P;
   __syncthreads();  // twiddle table
@@ -794,7 +796,7 @@ constexpr int rows_min_blocks() {
 template <int P, int RB>
 __global__ void __launch_bounds__(fft_threads_c(P) * RB, (rows_min_blocks<P, RB>()))
 rows_fwd_kernel(const GridGeom* __restrict__ geom, const float4* __restrict__ C, int cpitch,
-                const float2* __restrict__ tw, float2* __restrict__ CA, int ca_pitch) {
+                const float2* __restrict__ tw, float2* __restrict__ CA, int ca_pitch, int row0) {
   constexpr int T = fft_threads_c(P);
   constexpr int NT = T * RB;
   constexpr int PL = padded_len(P);
@@ -807,7 +809,7 @@ rows_fwd_kernel(const GridGeom* __restrict__ geom, const float4* __restrict__ C,
   // the three channel blocks of a row group are adjacent in launch order: they read the
   // same interleaved charge sectors close together in time (L2 hits)
   const int ch = blockIdx.x % 3;
-  const int p0 = (blockIdx.x / 3) * RB;  // first row pair of the block
+  const int p0 = row0 / 2 + (blockIdx.x / 3) * RB;  // first row pair of the block
   if (2 * p0 >= M) return;
   const int g = threadIdx.x / T, lt = threadIdx.x - g * T;
   const int ra = 2 * (p0 + g), rb = ra + 1;
@@ -852,7 +854,7 @@ template <int P, int RB>
 __global__ void __launch_bounds__(fft_threads_c(P) * RB, (rows_min_blocks<P, RB>()))
 rows_inv_kernel(const GridGeom* __restrict__ geom, const float2* __restrict__ CA, int ca_pitch,
                 const float2* __restrict__ tw, float* __restrict__ Phi, int cpitch,
-                float4* __restrict__ C) {
+                float4* __restrict__ C, int row0) {
   constexpr int T = fft_threads_c(P);
   constexpr int NT = T * RB;
   constexpr int PL = padded_len(P);
@@ -863,7 +865,7 @@ rows_inv_kernel(const GridGeom* __restrict__ geom, const float2* __restrict__ CA
   pdl_trigger();
   const int M = geom->M;
   const int ch = blockIdx.x % 3;  // channel blocks of a row group adjacent (as rows_fwd)
-  const int p0 = (blockIdx.x / 3) * RB;
+  const int p0 = row0 / 2 + (blockIdx.x / 3) * RB;
   if (2 * p0 >= M) return;
   const int rows_here = min(2 * RB, M - 2 * p0);
   constexpr int half = P / 2;
@@ -1003,7 +1005,7 @@ void launch_kspec(const GridGeom* geom, int P, ForceArgs fa, const float2* tw, f
   {                                                                                           \
     const int rb = rows_rb(S);                                                                \
     const size_t smb = rows_smem_bytes(S, rb);                                                \
-    const dim3 grid((unsigned)(3 * (((Mcap + 1) / 2 + rb - 1) / rb)));                        \
+    const dim3 grid((unsigned)(3 * (((row1 - row0 + 1) / 2 + rb - 1) / rb)));                 \
     if (rb == 4) {                                                                            \
       if constexpr (fft_threads_c(S) * 4 <= 1024)                                             \
         launch_chained(KERN<S, 4>, grid, fft_threads_c(S) * 4, smb, s, __VA_ARGS__);          \
@@ -1015,33 +1017,37 @@ void launch_kspec(const GridGeom* geom, int P, ForceArgs fa, const float2* tw, f
     }                                                                                         \
   }
 
-void launch_rows_fwd(const GridGeom* geom, const float4* C, int cpitch, int P, int Mcap,
-                     const float2* tw, float2* CA, int ca_pitch, cudaStream_t s) {
+void launch_rows_fwd(const GridGeom* geom, const float4* C, int cpitch, int P, int row0,
+                     int row1, const float2* tw, float2* CA, int ca_pitch, cudaStream_t s) {
+  if (row1 <= row0) return;
 #define TFDP_RF(S)                                                                          \
   case S:                                                                                   \
-    TFDP_ROWS_DISPATCH(S, aos::rows_fwd_kernel, geom, C, cpitch, tw, CA, ca_pitch)          \
+    TFDP_ROWS_DISPATCH(S, aos::rows_fwd_kernel, geom, C, cpitch, tw, CA, ca_pitch, row0)    \
     break;
   switch (P) { TFDP_FFT_SIZES(TFDP_RF) default: break; }
 #undef TFDP_RF
 }
 
 void launch_cols(const GridGeom* geom, float2* CA, int ca_pitch, const float* KH, int P,
-                 const float2* tw, cudaStream_t s) {
+                 const float2* tw, int q0, int q1, cudaStream_t s) {
+  if (q1 <= q0) return;
   const size_t sm = fftconv_smem_bytes(P);
 #define TFDP_CO(S)                                                                          \
   case S:                                                                                   \
-    cols_kernel<S><<<(unsigned)(3 * ((S / 2 + 2) / 2)), fft_threads_c(S), sm, s>>>(         \
-        geom, CA, ca_pitch, KH, tw);                                                        \
+    cols_kernel<S><<<(unsigned)(3 * ((q1 - q0 + 1) / 2)), fft_threads_c(S), sm, s>>>(      \
+        geom, CA, ca_pitch, KH, tw, q0, q1 - q0);                                           \
     break;
   switch (P) { TFDP_FFT_SIZES(TFDP_CO) default: break; }
 #undef TFDP_CO
 }
 
-void launch_rows_inv(const GridGeom* geom, const float2* CA, int ca_pitch, int P, int Mcap,
-                     const float2* tw, float* Phi, int cpitch, float4* C, cudaStream_t s) {
+void launch_rows_inv(const GridGeom* geom, const float2* CA, int ca_pitch, int P, int row0,
+                     int row1, const float2* tw, float* Phi, int cpitch, float4* C,
+                     cudaStream_t s) {
+  if (row1 <= row0) return;
 #define TFDP_RI(S)                                                                          \
   case S:                                                                                   \
-    TFDP_ROWS_DISPATCH(S, aos::rows_inv_kernel, geom, CA, ca_pitch, tw, Phi, cpitch, C)        \
+    TFDP_ROWS_DISPATCH(S, aos::rows_inv_kernel, geom, CA, ca_pitch, tw, Phi, cpitch, C, row0) \
     break;
   switch (P) { TFDP_FFT_SIZES(TFDP_RI) default: break; }
 #undef TFDP_RI

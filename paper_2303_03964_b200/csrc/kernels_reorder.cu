@@ -112,13 +112,10 @@ scan_add_kernel(long long* __restrict__ out, int64_t n, const long long* __restr
   if (i < n) out[i] += sums[blockIdx.x];
 }
 
-// slot i (old internal order) -> new position; positions, permutation moved along
+// slot i (old internal order) -> new position of its caller id in the new permutation
 __global__ void __launch_bounds__(256)
 scatter_kernel(const int* __restrict__ keys, long long* __restrict__ offs, int64_t n,
-               const float2* __restrict__ xy_old, float2* __restrict__ xy_new,
-               const int* __restrict__ perm_old, int* __restrict__ perm_new,
-               int* __restrict__ inv_new, const int64_t* __restrict__ row_ptr_o,
-               long long* __restrict__ deg_new) {
+               const int* __restrict__ perm_old, int* __restrict__ perm_new) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int key = keys[i];
@@ -131,9 +128,20 @@ scatter_kernel(const int* __restrict__ keys, long long* __restrict__ offs, int64
     base = atomicAdd(reinterpret_cast<unsigned long long*>(offs + key), (unsigned long long)__popc(grp));
   base = __shfl_sync(grp, base, leader);
   const long long pos = (long long)base + __popc(grp & ((1u << lane) - 1u));
-  xy_new[pos] = xy_old[i];
-  const int o = perm_old[i];
-  perm_new[pos] = o;
+  perm_new[pos] = perm_old[i];
+}
+
+// Applies a new permutation (computed here, or by rank 0 and broadcast so that every rank
+// holds the same internal order): positions, inverse and degrees in the new order.
+__global__ void __launch_bounds__(256)
+apply_perm_kernel(const int* __restrict__ perm_new, const int* __restrict__ inv_old, int64_t n,
+                  const float2* __restrict__ xy_old, float2* __restrict__ xy_new,
+                  int* __restrict__ inv_new, const int64_t* __restrict__ row_ptr_o,
+                  long long* __restrict__ deg_new) {
+  const int64_t pos = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (pos >= n) return;
+  const int o = perm_new[pos];
+  xy_new[pos] = xy_old[inv_old[o]];
   inv_new[o] = (int)pos;
   deg_new[pos] = row_ptr_o[o + 1] - row_ptr_o[o];
 }
@@ -201,30 +209,49 @@ void launch_iota(int* perm, int* inv, int64_t n, cudaStream_t s) {
   iota_kernel<<<blocks_for(n, 256), 256, 0, s>>>(perm, inv, n);
 }
 
-int launch_reorder(const float2* xy_old, float2* xy_new, const BoxKeys* box, const int* perm_old,
-                   int* perm_new, int* inv_new, const int64_t* row_ptr_o, const int32_t* col_o,
-                   int64_t* row_ptr_p, int32_t* col_p, int64_t n, void* scratch, cudaStream_t s) {
-  const int64_t nbins = kBins;
+namespace {
+struct Scratch {
+  int* keys;
+  long long *hist, *offs, *deg, *sums;
+};
+Scratch carve(void* scratch, int64_t n) {
   char* p = static_cast<char*>(scratch);
-  int* keys = reinterpret_cast<int*>(p);
+  Scratch q;
+  q.keys = reinterpret_cast<int*>(p);
   p += ((size_t)n * 4 + 255) / 256 * 256;
-  long long* hist = reinterpret_cast<long long*>(p);
-  p += nbins * 8;
-  long long* offs = reinterpret_cast<long long*>(p);
-  p += nbins * 8;
-  long long* deg = reinterpret_cast<long long*>(p);
+  q.hist = reinterpret_cast<long long*>(p);
+  p += (size_t)kBins * 8;
+  q.offs = reinterpret_cast<long long*>(p);
+  p += (size_t)kBins * 8;
+  q.deg = reinterpret_cast<long long*>(p);
   p += (size_t)(n + 1) * 8;
-  long long* sums = reinterpret_cast<long long*>(p);
-  cudaMemsetAsync(hist, 0, nbins * 8, s);
-  morton_keys_kernel<<<blocks_for(n, 256), 256, 0, s>>>(xy_old, n, box, keys, hist);
-  exclusive_scan(hist, offs, nbins, sums, s);
-  cudaMemsetAsync(deg + n, 0, sizeof(long long), s);
-  scatter_kernel<<<blocks_for(n, 256), 256, 0, s>>>(keys, offs, n, xy_old, xy_new, perm_old,
-                                                    perm_new, inv_new, row_ptr_o, deg);
-  exclusive_scan(deg, reinterpret_cast<long long*>(row_ptr_p), n + 1, sums, s);
+  q.sums = reinterpret_cast<long long*>(p);
+  return q;
+}
+}  // namespace
+
+int launch_reorder_perm(const float2* xy_old, const BoxKeys* box, const int* perm_old,
+                        int* perm_new, int64_t n, void* scratch, cudaStream_t s) {
+  const Scratch q = carve(scratch, n);
+  cudaMemsetAsync(q.hist, 0, (size_t)kBins * 8, s);
+  morton_keys_kernel<<<blocks_for(n, 256), 256, 0, s>>>(xy_old, n, box, q.keys, q.hist);
+  exclusive_scan(q.hist, q.offs, kBins, q.sums, s);
+  scatter_kernel<<<blocks_for(n, 256), 256, 0, s>>>(q.keys, q.offs, n, perm_old, perm_new);
+  return 5;
+}
+
+int launch_reorder_apply(const float2* xy_old, float2* xy_new, const int* inv_old,
+                         const int* perm_new, int* inv_new, const int64_t* row_ptr_o,
+                         const int32_t* col_o, int64_t* row_ptr_p, int32_t* col_p, int64_t n,
+                         void* scratch, cudaStream_t s) {
+  const Scratch q = carve(scratch, n);
+  cudaMemsetAsync(q.deg + n, 0, sizeof(long long), s);
+  apply_perm_kernel<<<blocks_for(n, 256), 256, 0, s>>>(perm_new, inv_old, n, xy_old, xy_new,
+                                                       inv_new, row_ptr_o, q.deg);
+  exclusive_scan(q.deg, reinterpret_cast<long long*>(row_ptr_p), n + 1, q.sums, s);
   remap_cols_kernel<<<blocks_for(n * 8, 256), 256, 0, s>>>(perm_new, inv_new, row_ptr_o, col_o,
                                                              row_ptr_p, col_p, n);
-  return 9;  // kernel launches issued (memsets excluded)
+  return 5;
 }
 
 void launch_unpermute(const float2* in, const int* perm, int64_t n, float2* out, cudaStream_t s) {

@@ -30,6 +30,8 @@ const NcclApi* nccl_api(const char** err) {
     TFDP_SYM(GroupEnd, "ncclGroupEnd");
     TFDP_SYM(Broadcast, "ncclBroadcast");
     TFDP_SYM(AllReduce, "ncclAllReduce");
+    TFDP_SYM(Send, "ncclSend");
+    TFDP_SYM(Recv, "ncclRecv");
     TFDP_SYM(GetErrorString, "ncclGetErrorString");
 #undef TFDP_SYM
     api.loaded = true;

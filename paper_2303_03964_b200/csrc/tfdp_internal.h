@@ -118,8 +118,9 @@ void launch_setup(BoxKeys* slots, int n_part, BoxKeys* keys, GridGeom* geom, int
 // charges: float4 {C_1, C_x~, C_y~, 0} per grid node, row pitch = GridGeom::pitch float4s
 // per-node (warp-aggregated for k >= 2) v4 REDs; TFDP_SPREAD=tile: the shared-memory
 // privatised tile kernel (measured slower, kernels_fft.cu)
+// [by_lo, by_hi): only nodes whose interval row lies in it are spread (slab mode)
 void launch_spread(const float2* xy, int64_t lo, int64_t cnt, const GridGeom* geom, int k,
-                   float4* grid, cudaStream_t s);
+                   float4* grid, cudaStream_t s, int by_lo = 0, int by_hi = 0x7fffffff);
 
 // hand-written FFT convolution (kernels_fftconv.cu)
 bool fft_size_supported(int P);  // P = 256 q, q = 2^a 3^b 5^c (b <= 2, c <= 1), P <= 8192
@@ -129,19 +130,49 @@ void launch_twiddles(float2* tw, int P, cudaStream_t s);
 // (early exit) unless geom->kspec.
 void launch_kspec(const GridGeom* geom, int P, ForceArgs fa, const float2* tw, float* KA,
                   float* KH, cudaStream_t s);
-void launch_rows_fwd(const GridGeom* geom, const float4* C, int cpitch, int P, int Mcap,
-                     const float2* tw, float2* CA, int ca_pitch, cudaStream_t s);
+// row passes over grid rows [row0, row1) (row0 even; rows >= M are skipped on the device)
+void launch_rows_fwd(const GridGeom* geom, const float4* C, int cpitch, int P, int row0,
+                     int row1, const float2* tw, float2* CA, int ca_pitch, cudaStream_t s);
+// column pass over half-spectrum columns [q0, q1) (q0 even), which CA holds as columns
+// 0 .. q1 - q0 - 1 (the whole half spectrum on one GPU: q0 = 0, q1 = P/2 + 1)
 void launch_cols(const GridGeom* geom, float2* CA, int ca_pitch, const float* KH, int P,
-                 const float2* tw, cudaStream_t s);
-// rows_inv also re-zeroes the charge rows [0, M) x [0, M) of C (consumed by rows_fwd)
-void launch_rows_inv(const GridGeom* geom, const float2* CA, int ca_pitch, int P, int Mcap,
-                     const float2* tw, float* Phi, int cpitch, float4* C, cudaStream_t s);
+                 const float2* tw, int q0, int q1, cudaStream_t s);
+// rows_inv also re-zeroes the charge rows it covers (consumed by rows_fwd)
+void launch_rows_inv(const GridGeom* geom, const float2* CA, int ca_pitch, int P, int row0,
+                     int row1, const float2* tw, float* Phi, int cpitch, float4* C,
+                     cudaStream_t s);
+// multi-GPU slab mode (kernels_dist.cu): rank r owns grid rows
+// [row0[r], row0[r+1]) of the row passes (multiples of 24: whole CA row tiles of 8 and whole
+// intervals at every k) and half-spectrum columns [q0[r], q0[r+1]) of the column pass (even
+// starts: the column pass works on column pairs).
+constexpr int kMaxWorld = 64;
+struct SlabPlan {
+  int world, rank;
+  int R;  // rows of the slab domain (cap_k k rounded up to 24)
+  int H;  // half-spectrum columns P/2 + 1
+  int row0[kMaxWorld + 1];
+  int q0[kMaxWorld + 1];
+};
+void slab_plan(int world, int rank, int rows, int P, SlabPlan* pl);
+// exchange-1 send / exchange-2 receive layout: [s][ch][rt - rt0(me)][q - q0(s)][8] float2,
+// i.e. segment (s, ch) starts at 3 * nrt * 8 * q0[s] + ch * nrt * nq(s) * 8
+// pack: this rank's slab rows of CA ([ch][ca_pitch / 8][H][8]) -> xa;  unpack: xa -> CA
+void launch_pack_slab(const float2* CA, int ca_pitch, const SlabPlan& pl, float2* xa,
+                      cudaStream_t s);
+void launch_unpack_slab(const float2* xa, const SlabPlan& pl, float2* CA, int ca_pitch,
+                        cudaStream_t s);
+
 // internal node renumbering (kernels_reorder.cu)
 size_t reorder_scratch_bytes(int64_t n);
 void launch_iota(int* perm, int* inv, int64_t n, cudaStream_t s);
-int launch_reorder(const float2* xy_old, float2* xy_new, const BoxKeys* box, const int* perm_old,
-                   int* perm_new, int* inv_new, const int64_t* row_ptr_o, const int32_t* col_o,
-                   int64_t* row_ptr_p, int32_t* col_p, int64_t n, void* scratch, cudaStream_t s);
+// new permutation (Morton order of the box): perm_new[new slot] = caller id
+int launch_reorder_perm(const float2* xy_old, const BoxKeys* box, const int* perm_old,
+                        int* perm_new, int64_t n, void* scratch, cudaStream_t s);
+// positions, inverse and CSR in the new order (every rank, from the same perm_new)
+int launch_reorder_apply(const float2* xy_old, float2* xy_new, const int* inv_old,
+                         const int* perm_new, int* inv_new, const int64_t* row_ptr_o,
+                         const int32_t* col_o, int64_t* row_ptr_p, int32_t* col_p, int64_t n,
+                         void* scratch, cudaStream_t s);
 void launch_unpermute(const float2* in, const int* perm, int64_t n, float2* out, cudaStream_t s);
 void launch_permute(const float2* in, const int* perm, int64_t n, float2* out, cudaStream_t s);
 

@@ -36,7 +36,7 @@ class Params:
     iterations: int = 300
     t0: int = 0
     cooling: str = "linear"  # "linear" (R2) | "constant" (R2')
-    dist_mode: str = "spread_all"  # "spread_all" | "grid_allreduce"
+    dist_mode: str = "slab"  # "slab" | "spread_all" | "grid_allreduce" (ibFFT, p > 1)
     node_order: str = "auto"  # "auto" (internal Morton renumbering, ibFFT) | "keep"
     interval_rule: str = "unit"  # "unit" (R5', unit-width intervals) | "span" (R5)
     dim: int = 2
@@ -50,7 +50,8 @@ class Params:
         p.k, p.n_int_min, p.n_int_fixed, p.fft_size = self.k, self.n_int_min, self.n_int_fixed, self.fft_size
         p.step0, p.iterations, p.t0 = self.step0, self.iterations, self.t0
         p.cooling = {"linear": _L.COOL_LINEAR, "constant": _L.COOL_CONSTANT}[self.cooling]
-        p.dist_mode = {"spread_all": _L.DIST_SPREAD_ALL, "grid_allreduce": _L.DIST_GRID_ALLREDUCE}[self.dist_mode]
+        p.dist_mode = {"spread_all": _L.DIST_SPREAD_ALL, "grid_allreduce": _L.DIST_GRID_ALLREDUCE,
+                       "slab": _L.DIST_SLAB}[self.dist_mode]
         p.node_order = {"auto": 0, "keep": 1}[self.node_order]
         p.interval_rule = {"unit": 0, "span": 1}[self.interval_rule]
         return p
@@ -92,6 +93,32 @@ def shard_range(n: int, world: int, rank: int):
     lo, hi = C.c_int64(), C.c_int64()
     check(lib().tfdp_shard_range(n, world, rank, C.byref(lo), C.byref(hi)))
     return lo.value, hi.value
+
+
+def slab_plan(rows: int, fft_size: int, world: int):
+    """tfdp_slab_plan: (row0, q0) int lists of world + 1 entries (host only)."""
+    r0 = (C.c_int32 * (world + 1))()
+    q0 = (C.c_int32 * (world + 1))()
+    check(lib().tfdp_slab_plan(int(rows), int(fft_size), int(world), C.cast(r0, C.c_void_p),
+                               C.cast(q0, C.c_void_p)))
+    return list(r0), list(q0)
+
+
+def group_step(layouts, n_iters: int = 1):
+    """tfdp_group_step over the virtual ranks 0..p-1 (Layout objects in rank order)."""
+    arr = (C.c_void_p * len(layouts))(*[L._ctx.value for L in layouts])
+    check(lib().tfdp_group_step(C.cast(arr, C.c_void_p), len(layouts), int(n_iters)), layouts[0]._ctx)
+
+
+def group_forces(layouts):
+    """tfdp_group_forces: [(R, A)] per virtual rank (NumPy float32 (hi - lo, 2))."""
+    outs = [(np.empty((L.hi - L.lo, 2), np.float32), np.empty((L.hi - L.lo, 2), np.float32)) for L in layouts]
+    rp = (C.c_void_p * len(layouts))(*[o[0].ctypes.data for o in outs])
+    ap = (C.c_void_p * len(layouts))(*[o[1].ctypes.data for o in outs])
+    arr = (C.c_void_p * len(layouts))(*[L._ctx.value for L in layouts])
+    check(lib().tfdp_group_forces(C.cast(arr, C.c_void_p), len(layouts), C.cast(rp, C.c_void_p),
+                                  C.cast(ap, C.c_void_p)), layouts[0]._ctx)
+    return outs
 
 
 def nccl_unique_id() -> bytes:

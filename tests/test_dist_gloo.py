@@ -59,6 +59,26 @@ def _worker(rank, world, port, q):
         Xn = torch.cat(bufs).numpy()
         ref = O.step(X, rp, col, O.Params(), O.eta(0, 300))
         out["step_bitwise"] = bool(np.array_equal(Xn, ref))
+        # 5) slab mode of the ibFFT path: the library's plan is identical on
+        # every rank, partitions rows and half-spectrum columns, and the two transposes it
+        # implies (row slabs -> column chunks -> row slabs), carried over gloo here, deliver
+        # to every rank exactly its block of the half spectra
+        rows, Pf = 1003 * 3, 6144
+        row0, q0 = P.slab_plan(rows, Pf, world)
+        out["plan"] = (row0, q0)
+        R_, H = row0[-1], Pf // 2 + 1
+        full = np.random.default_rng(5).standard_normal((3, R_, H)).astype(np.float32)
+        mine_rows = slice(row0[rank], row0[rank + 1])
+        segs = {s: full[:, mine_rows, q0[s]:q0[s + 1]].copy() for s in range(world)}
+        got = [None] * world
+        dist.all_gather_object(got, segs)  # message (r -> s) = got[r][s]
+        xb = np.concatenate([got[r][rank] for r in range(world)], axis=1)
+        out["cols_ok"] = bool(np.array_equal(xb, full[:, :, q0[rank]:q0[rank + 1]]))
+        back = {r: 2.0 * xb[:, row0[r]:row0[r + 1], :] for r in range(world)}  # "column pass"
+        got = [None] * world
+        dist.all_gather_object(got, back)
+        rows_back = np.concatenate([got[s][rank] for s in range(world)], axis=2)
+        out["rows_ok"] = bool(np.array_equal(rows_back, 2.0 * full[:, mine_rows, :]))
         q.put((rank, out))
     finally:
         dist.destroy_process_group()
@@ -85,3 +105,5 @@ def test_gloo_multiprocess_path(world):
         assert res[r]["shard"] == O.shard_range(n, world, r)
         assert res[r]["max"] == float(world)
         assert res[r]["step_bitwise"]
+        assert res[r]["cols_ok"] and res[r]["rows_ok"]
+        assert res[r]["plan"] == res[0]["plan"]

@@ -197,7 +197,8 @@ def test_virtual_shards(world):
     w, rp, col = _case("C2rgg")
     R1, A1, _ = _fft_forces(w.n, rp, col, w.xy, 2)
     for r in range(world):
-        with P.Layout(w.n, rp, col, w.xy, P.Params(solver="ibfft", k=2), dist=P.Dist(r, world, 0, None)) as L:
+        prm = P.Params(solver="ibfft", k=2, dist_mode="spread_all")  # a lone virtual rank
+        with P.Layout(w.n, rp, col, w.xy, prm, dist=P.Dist(r, world, 0, None)) as L:
             R, A = L.forces()
             lo, hi = L.lo, L.hi
         assert O.rel_l2(R, R1[lo:hi]) <= 1e-5  # atomics order only (R15)

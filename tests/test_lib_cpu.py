@@ -99,3 +99,21 @@ def test_status_strings():
     L = P.lib()
     assert L.tfdp_status_string(4) == b"TFDP_ERR_DIVERGED"
     assert L.tfdp_last_error(None) is not None
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+@pytest.mark.parametrize("rows,Pf", [(1001, 2048), (2002, 4096), (3003, 6144), (150, 512)])
+def test_slab_plan(world, rows, Pf):
+    """Slab plan of the multi-GPU FFT path (host only): grid-row slabs of whole 24-row units
+    (CA row tiles of 8 and whole intervals at k = 1, 2, 3) covering [0, rows rounded up to 24),
+    even-starting half-spectrum column chunks covering [0, P/2 + 1), balanced to one unit."""
+    row0, q0 = P.slab_plan(rows, Pf, world)
+    H = Pf // 2 + 1
+    assert row0[0] == 0 and row0[-1] == (rows + 23) // 24 * 24 and q0[0] == 0 and q0[-1] == H
+    d_rows = np.diff(row0)
+    d_cols = np.diff(q0)
+    assert (d_rows >= 0).all() and (np.asarray(row0) % 24 == 0).all()
+    assert (d_cols >= 0).all() and all(q % 2 == 0 for q in q0[:-1])
+    assert d_rows.max() - d_rows.min() <= 24 and d_cols.max() - d_cols.min() <= 3
+    with pytest.raises(P.TfdpError):
+        P.slab_plan(rows, Pf, 0)
