@@ -409,6 +409,11 @@ void free_fft_buffers(tfdp_ctx* c) {
 
 bool k_used(const tfdp_ctx* c, int k) { return c->p.k == 0 || c->p.k == k; }
 
+// Row pitch of the charge / potential planes at order k: the grid points the plan holds,
+// cap_k k (the buffers are sized for the largest k; a per-k pitch keeps the planes of the
+// smaller grids compact, and their slab rows contiguous for the potential exchange).
+int pitch_k(const tfdp_ctx* c, int k) { return c->cap_of_k[k] * k; }
+
 // Grid sizing: N_need = ceil(L) + 8 (or the forced N_int);
 // P_k = smallest 2^a3^b5^c >= 2 N_need k - 1 (R9: any such P is exact); the grid then
 // holds N_int <= cap_k = floor((P_k + 1) / 2k).  Re-planned when the layout outgrows it.
@@ -649,17 +654,18 @@ tfdp_status exchange_slabs(const Group& G, int k, int dir) {
 tfdp_status exchange_phi(const Group& G, int k) {
   tfdp_ctx* c = G[0];
   const tfdp::SlabPlan& pl = c->plan[k];
-  const int64_t plane = (int64_t)c->cpitch * c->cpitch;
+  const int pk = pitch_k(c, k);
+  const int64_t plane = (int64_t)pk * pk;
   auto rows = [&](int r) {
-    return std::max<int64_t>(0, std::min<int64_t>(pl.row0[r + 1], c->cpitch) - pl.row0[r]);
+    return std::max<int64_t>(0, std::min<int64_t>(pl.row0[r + 1], pk) - pl.row0[r]);
   };
   if (G.virt()) {
     for (int r = 0; r < G.p; ++r)
       for (int s = 0; s < G.p; ++s)
         if (s != r)
           for (int ch = 0; ch < 3; ++ch) {
-            const int64_t off = ch * plane + (int64_t)pl.row0[r] * c->cpitch;
-            TRY(dcopy(G[s], G[s]->phi + off, G[r]->phi + off, rows(r) * c->cpitch * sizeof(float)));
+            const int64_t off = ch * plane + (int64_t)pl.row0[r] * pk;
+            TRY(dcopy(G[s], G[s]->phi + off, G[r]->phi + off, rows(r) * pk * sizeof(float)));
           }
     return TFDP_OK;
   }
@@ -667,8 +673,8 @@ tfdp_status exchange_phi(const Group& G, int k) {
   NCCL_TRY(c, c->nccl->GroupStart());
   for (int r = 0; r < c->world; ++r)
     for (int ch = 0; ch < 3; ++ch) {
-      const int64_t cnt = rows(r) * c->cpitch;
-      float* b = c->phi + ch * plane + (int64_t)pl.row0[r] * c->cpitch;
+      const int64_t cnt = rows(r) * pk;
+      float* b = c->phi + ch * plane + (int64_t)pl.row0[r] * pk;
       if (cnt > 0) NCCL_TRY(c, c->nccl->Broadcast(b, b, (size_t)cnt, ncclFloat, r, c->comm, c->stream));
     }
   NCCL_TRY(c, c->nccl->GroupEnd());
@@ -695,7 +701,7 @@ void fft_prologue(tfdp_ctx* c, int k, bool* overlap) {
   {
     Scope sc(c, K_SETUP);
     tfdp::launch_setup(c->box_part, c->n_part, c->keys, c->geom, k, c->p.n_int_min,
-                       c->p.n_int_fixed, c->cap_of_k[k], P, c->cpitch, c->capped,
+                       c->p.n_int_fixed, c->cap_of_k[k], P, pitch_k(c, k), c->capped,
                        c->p.interval_rule, c->fa.gamma, c->kkey, c->stream);
   }
   // The kernel spectrum needs only the geometry: fork it onto the side stream so it overlaps
@@ -771,7 +777,7 @@ tfdp_status evaluate_one(tfdp_ctx* c, int update, float eta, int k) {
       Scope sc(c, K_COMM);
       // rows [0, M_cap) of the interleaved charges (they live in [0, M) x [0, M)); a failed
       // reduction leaves charges in the grid: the context is errored (no zero-grid invariant)
-      ncclResult_t r = c->nccl->AllReduce(c->grid, c->grid, (size_t)mcap * c->cpitch * 4,
+      ncclResult_t r = c->nccl->AllReduce(c->grid, c->grid, (size_t)mcap * pitch_k(c, k) * 4,
                                           ncclFloat, ncclSum, c->comm, c->stream);
       if (r != ncclSuccess) {
         c->errored = true;
@@ -780,7 +786,7 @@ tfdp_status evaluate_one(tfdp_ctx* c, int update, float eta, int k) {
     }
     {
       Scope sc(c, K_ROWS_FWD);
-      tfdp::launch_rows_fwd(c->geom, grid4, c->cpitch, P, 0, mcap, tw, c->ca, c->ca_pitch,
+      tfdp::launch_rows_fwd(c->geom, grid4, pitch_k(c, k), P, 0, mcap, tw, c->ca, c->ca_pitch,
                             c->stream);
     }
     if (overlap) CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_join, 0));
@@ -790,7 +796,7 @@ tfdp_status evaluate_one(tfdp_ctx* c, int update, float eta, int k) {
     }
     {
       Scope sc(c, K_ROWS_INV);
-      tfdp::launch_rows_inv(c->geom, c->ca, c->ca_pitch, P, 0, mcap, tw, c->phi, c->cpitch,
+      tfdp::launch_rows_inv(c->geom, c->ca, c->ca_pitch, P, 0, mcap, tw, c->phi, pitch_k(c, k),
                             grid4, c->stream);
     }
     {
@@ -828,7 +834,7 @@ tfdp_status evaluate_slab(const Group& G, int update, float eta, int k) {
     }
     {
       Scope sc(c, K_ROWS_FWD);
-      tfdp::launch_rows_fwd(c->geom, grid4, c->cpitch, P, pl.row0[r], pl.row0[r + 1], c->tw[k],
+      tfdp::launch_rows_fwd(c->geom, grid4, pitch_k(c, k), P, pl.row0[r], pl.row0[r + 1], c->tw[k],
                             c->ca, c->ca_pitch, c->stream);
       tfdp::launch_pack_slab(c->ca, c->ca_pitch, pl, c->xa, c->stream);
       c->launches++;
@@ -852,7 +858,7 @@ tfdp_status evaluate_slab(const Group& G, int update, float eta, int k) {
     tfdp::launch_unpack_slab(c->xa, pl, c->ca, c->ca_pitch, c->stream);
     c->launches++;
     tfdp::launch_rows_inv(c->geom, c->ca, c->ca_pitch, c->P_of_k[k], pl.row0[r], pl.row0[r + 1],
-                          c->tw[k], c->phi, c->cpitch, reinterpret_cast<float4*>(c->grid),
+                          c->tw[k], c->phi, pitch_k(c, k), reinterpret_cast<float4*>(c->grid),
                           c->stream);
   }
   TRY(exchange_phi(G, k));
