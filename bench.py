@@ -133,8 +133,8 @@ def alg_bytes(kind: str, n: int, nnz: int, M: int, P: int, n_spread: int) -> flo
         return 4 * hq * M
     if kind == "rows_fwd":
         return 12 * M * M + 24 * hq * M
-    if kind == "cols":
-        return 4 * hq * M + 48 * hq * M
+    if kind == "cols":  # CA columns read + written (3 channels x M rows x 8 B), K^ columns
+        return 48 * hq * M + 4 * hq * P
     if kind == "rows_inv":
         return 24 * hq * M + 12 * M * M
     if kind == "bbox":
@@ -291,26 +291,118 @@ def run_fft(args, rank, world, local):
     dom_ms, dom_n = prof[dom]
     traffic = ncu_traffic(dom, KS20) if args.config == "C4" else None
     total = float(np.sum(work)) if dom_n == len(work) else float(np.mean(work)) * dom_n
+    bytes_total = 0.0
+    for _ in range(args.steps):
+        for k in KS20:
+            M, Pk = N_int * k, plans[k][0]
+            bytes_total += alg_bytes(dom, n_local if dom == "gather_update" else w.n, nnz, M, Pk, w.n)
+    if dom_n != args.steps * len(KS20):
+        bytes_total = bytes_total / (args.steps * len(KS20)) * dom_n
+    achieved_gbs = bytes_total / (dom_ms / 1e3) / 1e9
+    roof = {"kernel": dom, "bound": "hbm", "achieved": round(achieved_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
+            "frac": round(achieved_gbs / hbm_peak, 4), "traffic": traffic, "peak_source": peak_src,
+            "work_per_launch": round(bytes_total / dom_n),
+            "work_unit": "algorithmic bytes (M-aware: only the M non-zero rows / kept outputs, DESIGN.md §6)"}
+    if traffic is not None:
+        roof["traffic_unit"] = "DRAM bytes per launch (ncu, profiles/r1_traffic.json)"
+    roof_flop = None
     if dom in FFT_KINDS:
         achieved = total / (dom_ms / 1e3) / 1e12
-        roof = {"kernel": dom, "bound": "alu", "achieved": round(achieved, 2), "peak": round(fp32_peak / 1e12, 2),
-                "unit": "TFLOP/s", "frac": round(achieved * 1e12 / fp32_peak, 4), "traffic": traffic,
-                "traffic_unit": "DRAM bytes per launch (ncu, profiles/r1_traffic.json)",
-                "peak_source": f"FP32 FMA peak {n_sm} SMs x 128 lanes x 2 x {f_mhz:.0f} MHz (measured clock)",
-                "work_per_launch": round(total / dom_n), "work_unit": "flop (5 N log2 N per complex FFT)"}
-    else:
-        achieved = total / (dom_ms / 1e3) / 1e9
-        roof = {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
-                "frac": round(achieved / hbm_peak, 4), "traffic": traffic, "peak_source": peak_src,
-                "work_per_launch": round(total / dom_n), "work_unit": "algorithmic bytes"}
+        roof_flop = {"kernel": dom, "bound": "alu", "achieved": round(achieved, 2), "peak": round(fp32_peak / 1e12, 2),
+                     "unit": "TFLOP/s", "frac": round(achieved * 1e12 / fp32_peak, 4),
+                     "peak_source": f"FP32 FMA peak {n_sm} SMs x 128 lanes x 2 x {f_mhz:.0f} MHz (measured clock)",
+                     "work_per_launch": round(total / dom_n), "work_unit": "flop (5 N log2 N per complex FFT)"}
     tot_all = sum(v[0] for v in prof_all.values())
     kernels = {k: {"us_per_launch": round(1e3 * v[0] / max(v[1], 1), 2), "launches": v[1],
                    "share": round(v[0] / tot_all, 4)} for k, v in prof_all.items()}
     res = dict(
         value=value, ms=ms_max, iters=iters, launches=launches, e2e=e2e, clocks=clk_s, roofline=roof,
+        roofline_flop=roof_flop, per_k=per_k_rates(L, w, rp, col, stream, world),
         kernels=kernels, n=w.n, nnz=nnz, N_int=N_int, P={k: plans[k][0] for k in plans},
         gen_s=tgen, L=L, w=w, rp=rp, col=col)
     return res
+
+
+def per_k_rates(L, w, rp, col, stream, world, iters=20):
+    """Iterations/s at each fixed k (the contexts' own schedule replaced by k = 1, 2, 3;
+    every block starts from the C4 input layout), and the schedule-weighted rate
+    1 / (0.9 t1 + 0.05 t2 + 0.05 t3) of P:545."""
+    import torch
+
+    import paper_2303_03964_b200 as P
+
+    base = L.params
+    out = {}
+    for k in (1, 2, 3):
+        L.set_params(P.Params(solver="ibfft", k=k, iterations=iters, cooling=base.cooling,
+                              dist_mode=base.dist_mode))
+        # one-time cost of this order's kernel spectrum (a plan constant under R5': computed
+        # at the first evaluation after a change of P, k or gamma): a fresh context's first
+        # evaluation, the spectrum kernels timed in line
+        with P.Layout(w.n, rp, col, w.xy, P.Params(solver="ibfft", k=k)) as Lk:
+            Lk.profile_only(["kspec_rows"])
+            Lk.forces()
+            ks_ms, _ = Lk.profile_read().get("kspec_rows", (0.0, 0))
+        for rep in range(2):  # warm-up (new plan / spectrum), then timed
+            L.set_layout(torch.from_numpy(w.xy).to(torch.cuda.current_device()))
+            L.set_iteration(0)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record(stream)
+            L.step(iters)
+            e1.record(stream)
+            torch.cuda.synchronize()
+        us = 1e3 * max_over_ranks(e0.elapsed_time(e1), world) / iters
+        out[str(k)] = {"us_per_iter": round(us, 1), "iterations_per_s": round(1e6 / us, 1),
+                       "kspec_once_us": round(1e3 * ks_ms, 1)}
+    L.set_params(base)
+    t = {k: out[str(k)]["us_per_iter"] for k in (1, 2, 3)}
+    out["schedule_weighted_iterations_per_s"] = round(1e6 / (0.9 * t[1] + 0.05 * t[2] + 0.05 * t[3]), 1)
+    out["timing"] = (f"CUDA events around {iters} tfdp_step iterations at fixed k from the C4 input "
+                     "layout; kspec_once_us: the kernel spectrum of that k, computed once per plan "
+                     "(DESIGN.md §6), timed in line")
+    return out
+
+
+def run_full_layout(w, rp, col, rank, world, local, T=300, reps=3):
+    """A whole C4 layout: tfdp_step(T) with the dynamic schedule (T = 300: 270/15/15) from the
+    input layout, end to end through the C ABI with HOST buffers (set_layout from pinned host
+    memory, layout back to host) — the paper's only timing is whole-layout time.
+    Reports N_int and the FFT size at the end of each k phase and the warning bits."""
+    import torch
+
+    import paper_2303_03964_b200 as P
+
+    xy_host = torch.from_numpy(w.xy.copy()).pin_memory()
+    out_host = torch.empty_like(xy_host).pin_memory()
+    prm = P.Params(solver="ibfft", k=0, iterations=T)
+    walls, phases = [], []
+    with P.Layout(w.n, rp, col, w.xy, prm, dist=make_dist(rank, world, local)) as L:
+        for rep in range(reps + 1):  # first pass: warm-up
+            torch.cuda.synchronize()
+            barrier(world)
+            t0 = time.perf_counter()
+            L.set_layout(xy_host)
+            L.set_iteration(0)
+            geo = []
+            for n_it in (int(0.9 * T), int(0.05 * T), T - int(0.9 * T) - int(0.05 * T)):
+                L.step(n_it)
+                if rep == reps:
+                    g = L.fft_geometry()
+                    geo.append({"k": g["k"], "N_int": g["n_int"], "P": g["P"], "L": round(g["L"], 1)})
+            L.layout(out_host)
+            wall = time.perf_counter() - t0
+            if rep:
+                walls.append(max_over_ranks(wall, world))
+            if rep == reps:
+                phases = geo
+        warn = L.warnings
+    ms = 1e3 * float(np.median(walls))
+    return {"workload": f"C4 full layout, T = {T}, dynamic k (270/15/15), linear cooling, from the input layout",
+            "ms": round(ms, 2), "iterations_per_s": round(T / (ms / 1e3), 1), "reps": reps,
+            "timing": "host wall clock around set_layout(pinned host) + tfdp_step(T) in 3 calls + layout(pinned host), median",
+            "geometry_at_phase_end": phases, "warnings": int(warn),
+            "h2d_bytes": int(xy_host.numel() * 4), "d2h_bytes": int(out_host.numel() * 4)}
 
 
 def run_np1(r, reps=5):
@@ -388,6 +480,7 @@ def run_exact(args, rank, world, local):
                      "flops_per_pair": 12, "mufu_bound_frac": kernel_pairs_per_s / mufu_pairs,
                      "peak_source": f"{n_sm} SMs x 128 FP32 lanes x 2 x {f_mhz:.0f} MHz (measured clock)"},
         "kernels": {k: {"ms_total": round(v[0], 3), "launches": v[1]} for k, v in prof.items()},
+        "_w": w,
     }
 
 
@@ -428,6 +521,41 @@ def cpu_baseline(w, rp, col, budget_s=25.0):
             "sample": f"oracle ibFFT iterations on C4 (n={w.n}): 2 x k=1, 1 x k=2, 1 x k=3, "
                       f"schedule-weighted (s/iter k1={t[1]:.2f} k2={t[2]:.2f} k3={t[3]:.2f}); "
                       "NumPy fp64, single-threaded pocketfft/np.add.at"}
+
+
+def _exact_chunk(args):
+    import oracle as O
+
+    X, idx = args
+    return O.repulsion_exact(X, targets=idx)
+
+
+def cpu_baseline_exact(w, per_core=16, seed=0):
+    """The oracle's exact repulsion (plain fp64 NumPy, as it stands) on sampled C5 targets
+    against all n sources, on 1 core and on all cores (a process pool over target blocks),
+    extrapolated linearly to pair-interactions/s."""
+    import multiprocessing as mp
+
+    import oracle as O
+
+    cores = len(os.sched_getaffinity(0))
+    X = w.xy.astype(np.float64)
+    g = np.random.default_rng(seed)
+    idx1 = g.choice(w.n, per_core, replace=False)
+    t0 = time.perf_counter()
+    O.repulsion_exact(X, targets=idx1)
+    t1 = time.perf_counter() - t0
+    n_all = min(1024, per_core * cores)
+    idx = g.choice(w.n, n_all, replace=False)
+    t0 = time.perf_counter()
+    with mp.get_context("fork").Pool(cores) as pool:
+        pool.map(_exact_chunk, [(X, b) for b in np.array_split(idx, cores)])
+    ta = time.perf_counter() - t0
+    return {"value": per_core * w.n / t1, "unit": "pair-interactions/s", "cores": 1, "kind": "oracle",
+            "sample": f"oracle repulsion_exact (fp64 NumPy) for {per_core} sampled C5 targets x all {w.n} "
+                      f"sources, extrapolated to n targets ({t1:.1f} s)",
+            "all_cores": {"value": n_all * w.n / ta, "cores": cores,
+                          "sample": f"{n_all} sampled targets over a {cores}-process pool ({ta:.1f} s), extrapolated"}}
 
 
 def cpu_model():
@@ -487,6 +615,7 @@ def main():
     ap.add_argument("--exact-warmup", type=int, default=1)
     ap.add_argument("--no-exact", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-full", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "tfdp":
@@ -502,7 +631,13 @@ def main():
     r = run_fft(args, rank, world, local)
     npm = run_np1(r)
     pm = run_pmds(r) if rank == 0 else None
+    full = None if args.no_full else run_full_layout(r["w"], r["rp"], r["col"], rank, world, local)
     exact = None if args.no_exact else run_exact(args, rank, world, local)
+    if exact is not None:
+        wx = exact.pop("_w")
+        if rank == 0 and world == 1 and not args.no_cpu_baseline:
+            exact["cpu_baseline"] = cpu_baseline_exact(wx)
+        del wx
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         import oracle as O
@@ -523,7 +658,8 @@ def main():
                 "l2": f"working set > 126 MB L2 (grid+FFT buffers at P={ws} and CSR: ~{(48 * ws * ws + 12 * r['nnz']) / 1e6:.0f} MB)",
             },
             "e2e": r["e2e"], "gpu_launches": r["launches"], "clocks": r["clocks"],
-            "roofline": r["roofline"], "cpu_baseline": cpu, "kernels": r["kernels"],
+            "roofline": r["roofline"], "roofline_flop": r["roofline_flop"], "cpu_baseline": cpu,
+            "per_k": r["per_k"], "full_layout": full, "kernels": r["kernels"],
             "exact": exact, "np1": npm, "pmds": pm,
         }
         print(json.dumps(line), flush=True)

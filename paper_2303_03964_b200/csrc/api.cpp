@@ -81,7 +81,7 @@ struct tfdp_ctx {
   BoxKeys* box_part = nullptr;  // per-block partial boxes (bbox / fused update epilogue)
   int n_part = 0;               // partials written by the last producer
   GridGeom* geom = nullptr;
-  tfdp::KspecKey* kkey = nullptr;  // (P, h, gamma) of the spectrum held in kh (device)
+  tfdp::KspecKey* kkey = nullptr;  // [4]: (P, h, gamma) of the spectrum held in kh[k] (device)
   bool box_valid = false;
   // ibFFT
   int nint_cap = 0;
@@ -94,8 +94,10 @@ struct tfdp_ctx {
   float* phi = nullptr;   // potentials Phi (gather source)
   float2* ca = nullptr;   // row half-spectra, transformed in place by the column pass
   float* ka = nullptr;    // kernel row spectra KA[q][dy]
-  float* kh = nullptr;    // kernel spectrum columns KH[q][u] (real)
-  int64_t alloc_kh = 0;
+  // kernel spectrum columns KH[q][u] (real), one per k: K^ is a plan constant of (P_k, h, gamma)
+  // under R5', so each order keeps its own across the k switches of the schedule
+  float* kh[4] = {nullptr, nullptr, nullptr, nullptr};
+  int64_t alloc_kh[4] = {0, 0, 0, 0};
   float2* tw[4] = {nullptr, nullptr, nullptr, nullptr};  // twiddles per k (length P_k)
   int tw_P[4] = {0, 0, 0, 0};
   // multi-GPU slab mode (TFDP_DIST_SLAB, kernels_dist.cu): per-k row slabs / column chunks,
@@ -396,10 +398,14 @@ void free_fft_buffers(tfdp_ctx* c) {
   cudaFree(c->phi);
   cudaFree(c->ca);
   cudaFree(c->ka);
-  cudaFree(c->kh);
-  c->grid = c->phi = c->ka = c->kh = nullptr;
+  c->grid = c->phi = c->ka = nullptr;
   c->ca = nullptr;
-  c->alloc_planes = c->alloc_ca = c->alloc_ka = c->alloc_kh = 0;
+  c->alloc_planes = c->alloc_ca = c->alloc_ka = 0;
+  for (int k = 0; k < 4; ++k) {
+    cudaFree(c->kh[k]);
+    c->kh[k] = nullptr;
+    c->alloc_kh[k] = 0;
+  }
   for (int k = 0; k < 4; ++k) {
     cudaFree(c->tw[k]);
     c->tw[k] = nullptr;
@@ -447,36 +453,43 @@ tfdp_status configure_fft(tfdp_ctx* c, float L) {
   // 24-row slab units of every k, kernels_dist.cu)
   const int capitch = c->slab ? (mcap + 95) / 96 * 96 : (mcap + 31) & ~31;
   // charges: one float4 {C_1, C_x~, C_y~, 0} per grid node; potentials: 3 planes
-  int64_t planes = 4LL * cpitch * cpitch, ca = 0, ka = 0, kh = 0;
+  int64_t planes = 4LL * cpitch * cpitch, ca = 0, ka = 0;
   for (int k = 1; k <= 3; ++k) {
     if (!k_used(c, k)) continue;
     ca = std::max<int64_t>(ca, 3LL * (c->P_of_k[k] / 2 + 1) * capitch);
     ka = std::max<int64_t>(ka, (int64_t)(c->P_of_k[k] / 2 + 1) * (c->P_of_k[k] / 2 + 1));
-    kh = std::max<int64_t>(kh, (int64_t)(c->P_of_k[k] / 2 + 2) * c->P_of_k[k]);
   }
-  if (planes > c->alloc_planes || ca > c->alloc_ca || ka > c->alloc_ka || kh > c->alloc_kh) {
+  if (planes > c->alloc_planes || ca > c->alloc_ca || ka > c->alloc_ka) {
     cudaStreamSynchronize(c->stream);
     cudaFree(c->grid);
     cudaFree(c->phi);
     cudaFree(c->ca);
     cudaFree(c->ka);
-    cudaFree(c->kh);
-    c->grid = c->phi = c->ka = c->kh = nullptr;
+    c->grid = c->phi = c->ka = nullptr;
     c->ca = nullptr;
     CUDA_TRY(c, cudaMalloc(&c->grid, planes * sizeof(float)));
-    // invariant: the charge planes are zero between iterations (rows_fwd re-zeroes)
+    // invariant: the charge planes are zero between iterations (rows_inv re-zeroes)
     CUDA_TRY(c, cudaMemsetAsync(c->grid, 0, planes * sizeof(float), c->stream));
     CUDA_TRY(c, cudaMalloc(&c->phi, (planes / 4) * 3 * sizeof(float)));
     CUDA_TRY(c, cudaMalloc(&c->ca, ca * sizeof(float2)));
     CUDA_TRY(c, cudaMalloc(&c->ka, ka * sizeof(float)));
-    CUDA_TRY(c, cudaMalloc(&c->kh, kh * sizeof(float)));
     c->alloc_planes = planes;
     c->alloc_ca = ca;
     c->alloc_ka = ka;
-    c->alloc_kh = kh;
-    // a new kh holds no spectrum (the key also carries P, so a same-buffer re-plan to another
-    // P invalidates itself)
-    CUDA_TRY(c, cudaMemsetAsync(c->kkey, 0, sizeof(tfdp::KspecKey), c->stream));
+  }
+  for (int k = 1; k <= 3; ++k) {
+    if (!k_used(c, k)) continue;
+    const int64_t kh = (int64_t)(c->P_of_k[k] / 2 + 2) * c->P_of_k[k];
+    if (kh > c->alloc_kh[k]) {
+      cudaStreamSynchronize(c->stream);
+      cudaFree(c->kh[k]);
+      c->kh[k] = nullptr;
+      CUDA_TRY(c, cudaMalloc(&c->kh[k], kh * sizeof(float)));
+      c->alloc_kh[k] = kh;
+      // a new buffer holds no spectrum (the key also carries P, so a same-buffer re-plan to
+      // another P invalidates itself)
+      CUDA_TRY(c, cudaMemsetAsync(c->kkey + k, 0, sizeof(tfdp::KspecKey), c->stream));
+    }
   }
   c->cpitch = cpitch;
   c->ca_pitch = capitch;
@@ -702,7 +715,7 @@ void fft_prologue(tfdp_ctx* c, int k, bool* overlap) {
     Scope sc(c, K_SETUP);
     tfdp::launch_setup(c->box_part, c->n_part, c->keys, c->geom, k, c->p.n_int_min,
                        c->p.n_int_fixed, c->cap_of_k[k], P, pitch_k(c, k), c->capped,
-                       c->p.interval_rule, c->fa.gamma, c->kkey, c->stream);
+                       c->p.interval_rule, c->fa.gamma, c->kkey + k, c->stream);
   }
   // The kernel spectrum needs only the geometry: fork it onto the side stream so it overlaps
   // spread + rows_fwd (both latency-bound); cols joins on it.  Its kernels exit at once
@@ -718,7 +731,7 @@ void fft_prologue(tfdp_ctx* c, int k, bool* overlap) {
   }
   {
     Scope sc(c, K_KSPEC, ks, 2);  // kspec_rows + kspec_cols
-    tfdp::launch_kspec(c->geom, P, c->fa, c->tw[k], c->ka, c->kh, ks);
+    tfdp::launch_kspec(c->geom, P, c->fa, c->tw[k], c->ka, c->kh[k], ks);
   }
   if (*overlap) cudaEventRecord(c->ev_join, c->side);
 }
@@ -792,7 +805,7 @@ tfdp_status evaluate_one(tfdp_ctx* c, int update, float eta, int k) {
     if (overlap) CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_join, 0));
     {
       Scope sc(c, K_COLS);
-      tfdp::launch_cols(c->geom, c->ca, c->ca_pitch, c->kh, P, tw, 0, P / 2 + 1, c->stream);
+      tfdp::launch_cols(c->geom, c->ca, c->ca_pitch, c->kh[k], P, tw, 0, P / 2 + 1, c->stream);
     }
     {
       Scope sc(c, K_ROWS_INV);
@@ -846,7 +859,7 @@ tfdp_status evaluate_slab(const Group& G, int update, float eta, int k) {
     const tfdp::SlabPlan& pl = c->plan[k];
     if (overlap[i]) CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_join, 0));
     Scope sc(c, K_COLS);
-    tfdp::launch_cols(c->geom, c->xb, pl.R, c->kh, c->P_of_k[k], c->tw[k], pl.q0[c->rank],
+    tfdp::launch_cols(c->geom, c->xb, pl.R, c->kh[k], c->P_of_k[k], c->tw[k], pl.q0[c->rank],
                       pl.q0[c->rank + 1], c->stream);
   }
   TRY(exchange_slabs(G, k, 1));
@@ -1298,7 +1311,9 @@ tfdp_status tfdp_init(tfdp_ctx** out, int64_t n, const int64_t* row_ptr, const i
   ALLOC(c->keys, sizeof(BoxKeys));
   ALLOC(c->box_part, tfdp::kBoxSlots * sizeof(BoxKeys));
   ALLOC(c->geom, sizeof(GridGeom));
-  ALLOC(c->kkey, sizeof(tfdp::KspecKey));
+  ALLOC(c->kkey, 4 * sizeof(tfdp::KspecKey));
+  if (cudaMemsetAsync(c->kkey, 0, 4 * sizeof(tfdp::KspecKey), c->stream ? c->stream : 0) != cudaSuccess)
+    return bail(fail(c, TFDP_ERR_CUDA, "kkey memset"));
   if (cudaMallocHost((void**)&c->h_status, 2 * sizeof(unsigned long long) + sizeof(GridGeom)) !=
       cudaSuccess)
     return bail(fail(c, TFDP_ERR_OOM, "cudaMallocHost failed"));
@@ -1784,7 +1799,6 @@ void tfdp_destroy(tfdp_ctx* c) {
   cudaFree(c->att);
   cudaFree(c->diverge);
   cudaFree(c->capped);
-  cudaFree(c->kh);
   cudaFree(c->keys);
   cudaFree(c->box_part);
   cudaFree(c->perm);
