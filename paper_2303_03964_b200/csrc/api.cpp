@@ -254,8 +254,9 @@ void prof_collect(tfdp_ctx* c) {
 }
 
 // ---------------------------------------------------------------- helpers
-// Largest FFT of the shared-memory kernels (512 threads, one radix-16 butterfly each).
-constexpr int kMaxFftSize = 8192;
+// Largest FFT of the shared-memory kernels (1024 threads, one radix-16 butterfly each; the
+// AoS one-FFT-per-block kernels above 8192, kernels_fftconv.cu).
+constexpr int kMaxFftSize = 16384;
 
 // Smallest m >= target with m % 256 == 0 and m = 2^a 3^b 5^c, b <= 2, c <= 1 (the radices
 // of kernels_fftconv.cu; the first two stages are radix 16, all strides multiples of 16).

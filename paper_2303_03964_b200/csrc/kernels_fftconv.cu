@@ -263,7 +263,7 @@ __device__ __forceinline__ void twiddles(const float2* __restrict__ tw, int base
 // Threads per FFT-pair block: the smallest of {128, 256, 384, 512} >= P/16 (one radix-16
 // butterfly of both FFTs per thread).
 __host__ __device__ constexpr int fft_threads_c(int P) {
-  return P <= 2048 ? 128 : P <= 4096 ? 256 : P <= 6144 ? 384 : 512;
+  return P <= 2048 ? 128 : P <= 4096 ? 256 : P <= 6144 ? 384 : P <= 8192 ? 512 : 1024;
 }
 
 // Blocks per SM the register cap aims for.
@@ -563,7 +563,7 @@ TFDP_FFT_KERNEL(cols_kernel)(const GridGeom* __restrict__ geom, float2* __restri
 namespace aos {
 
 template <int T>
-constexpr int kMinBlocksA = T == 128 ? 8 : T == 256 ? 4 : T == 384 ? 3 : 2;
+constexpr int kMinBlocksA = T == 128 ? 8 : T == 256 ? 4 : T == 384 ? 3 : T == 512 ? 2 : 1;
 
 __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return __fadd2_rn(a, b); }
 __device__ __forceinline__ float2 csub(float2 a, float2 b) {
@@ -914,18 +914,121 @@ rows_inv_kernel(const GridGeom* __restrict__ geom, const float2* __restrict__ CA
   }
 }
 
+// ---------------------------------------------------------------- P > 8192 (AoS, one FFT)
+// The SoA pair core needs 16 B of shared memory per point (> 227 KB beyond P = 12288) and
+// ~80 registers at 1024 threads; above P = 8192 the kernel spectrum and the column pass run
+// one complex FFT per block in the AoS core (8 B per point: 139 KB at P = 16384, ~60
+// registers), reading and writing through shared memory.  These sizes serve layouts whose
+// span needs N_int k > 4096 (e.g. 4M-node unit-density layouts at k = 3).
+template <int P>
+__global__ void __launch_bounds__(fft_threads_c(P), 1)
+kspec_rows1_kernel(const GridGeom* __restrict__ geom, float neg_gamma, int gi,
+                   const float2* __restrict__ tw, float* __restrict__ KA) {
+  if (!geom->kspec) return;
+  constexpr int T = fft_threads_c(P), half = P / 2, ka_pitch = half + 1;
+  extern __shared__ float2 sm[];
+  float2* a = sm;
+  float2* tws = sm + padded_len(P);
+  load_tw(tws, tw, P);
+  const float h = geom->h, h2 = h * h, scale = 1.0f / ((float)P * (float)P);
+  const int dy0 = 2 * blockIdx.x;  // rows dy0 (real part) and dy0 + 1 (imaginary part)
+  for (int x = threadIdx.x; x < P; x += T) {
+    const int dx = x <= half ? x : x - P;
+    const float dx2 = (float)dx * (float)dx;
+    float v[2] = {0.f, 0.f};
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int dy = dy0 + c;
+      if (dy <= half) v[c] = ksample(fmaf(h2, dx2 + (float)dy * (float)dy, 1.0f), neg_gamma, gi) * scale;
+    }
+    a[pad(x)] = make_float2(v[0], v[1]);
+  }
+  __syncthreads();
+  fft_smem<T, P, 0>(a, tws);
+  for (int q = threadIdx.x; q <= half; q += T) {  // real-even rows: real spectra
+    const float2 z = a[pad(q)];
+    KA[(int64_t)q * ka_pitch + dy0] = z.x;
+    if (dy0 + 1 <= half) KA[(int64_t)q * ka_pitch + dy0 + 1] = z.y;
+  }
+}
+
+template <int P>
+__global__ void __launch_bounds__(fft_threads_c(P), 1)
+kspec_cols1_kernel(const GridGeom* __restrict__ geom, const float* __restrict__ KA,
+                   const float2* __restrict__ tw, float* __restrict__ KH) {
+  if (!geom->kspec) return;
+  constexpr int T = fft_threads_c(P), half = P / 2, ka_pitch = half + 1;
+  extern __shared__ float2 sm[];
+  float2* a = sm;
+  float2* tws = sm + padded_len(P);
+  load_tw(tws, tw, P);
+  pdl_wait();
+  const int q0 = 2 * blockIdx.x;  // columns q0 (real part) and q0 + 1 (imaginary part)
+  for (int u = threadIdx.x; u < P; u += T) {
+    const int dy = u <= half ? u : P - u;
+    const float va = KA[(int64_t)q0 * ka_pitch + dy];
+    const float vb = q0 + 1 <= half ? KA[(int64_t)(q0 + 1) * ka_pitch + dy] : 0.f;
+    a[pad(u)] = make_float2(va, vb);
+  }
+  __syncthreads();
+  fft_smem<T, P, 0>(a, tws);
+  for (int u = threadIdx.x; u < P; u += T) {
+    const float2 z = a[pad(u)];
+    KH[(int64_t)q0 * P + u] = z.x;
+    if (q0 + 1 <= half) KH[(int64_t)(q0 + 1) * P + u] = z.y;
+  }
+}
+
+// one (channel, column) per block: FFT (inputs below P/2) -> x K^ -> inverse FFT (outputs
+// below P/2), rows 0..M-1 kept; columns [q_base, q_base + Hl) held in CA (as cols_kernel)
+template <int P>
+__global__ void __launch_bounds__(fft_threads_c(P), 1)
+cols1_kernel(const GridGeom* __restrict__ geom, float2* __restrict__ CA, int ca_pitch,
+             const float* __restrict__ KH, const float2* __restrict__ tw, int q_base, int Hl) {
+  constexpr int T = fft_threads_c(P), half = P / 2;
+  extern __shared__ float2 sm[];
+  float2* a = sm;
+  float2* tws = sm + padded_len(P);
+  load_tw(tws, tw, P);
+  pdl_wait();
+  pdl_trigger();
+  const int M = geom->M;
+  const int ch = blockIdx.x % 3, q = q_base + blockIdx.x / 3;
+  if (q > half || q >= q_base + Hl) return;
+  float2* col = CA + ca_col_base(ch, q - q_base, Hl, ca_pitch);
+  for (int u = threadIdx.x; u < half; u += T)  // [P/2, P) is zero and never read
+    a[pad(u)] = u < M ? col[ca_row_off(u, Hl)] : make_float2(0.f, 0.f);
+  __syncthreads();
+  fft_smem<T, P, kZeroUpper>(a, tws);
+  const float* kh = KH + (int64_t)q * P;
+  for (int u = threadIdx.x; u < P; u += T) {  // x K^ (real), conjugated for the inverse
+    const float2 z = a[pad(u)];
+    const float k = __ldg(kh + u);
+    a[pad(u)] = make_float2(z.x * k, -z.y * k);
+  }
+  __syncthreads();
+  fft_smem<T, P, kLowOut>(a, tws);
+  for (int u = threadIdx.x; u < M; u += T) {
+    const float2 z = a[pad(u)];
+    col[ca_row_off(u, Hl)] = make_float2(z.x, -z.y);
+  }
+}
+
 }  // namespace aos
 
 }  // namespace
 
-// Supported FFT sizes: P = 256 q, q = 2^a 3^b 5^c with b <= 2, c <= 1, P <= 8192.
+// Supported FFT sizes: P = 256 q, q = 2^a 3^b 5^c with b <= 2, c <= 1, P <= 16384.  The SoA
+// kernels (kernel spectrum, column pass) up to 8192; above, their AoS one-FFT variants.
 #define TFDP_FFT_SIZES(X) \
   X(256) X(512) X(768) X(1024) X(1280) X(1536) X(2048) X(2304) X(2560) X(3072) X(3840) \
   X(4096) X(4608) X(5120) X(6144) X(7680) X(8192)
+#define TFDP_FFT_SIZES_BIG(X) X(9216) X(10240) X(11520) X(12288) X(15360) X(16384)
+#define TFDP_FFT_SIZES_ALL(X) TFDP_FFT_SIZES(X) TFDP_FFT_SIZES_BIG(X)
 
 bool fft_size_supported(int P) {
 #define TFDP_CASE(S) if (P == S) return true;
-  TFDP_FFT_SIZES(TFDP_CASE)
+  TFDP_FFT_SIZES_ALL(TFDP_CASE)
 #undef TFDP_CASE
   return false;
 }
@@ -976,7 +1079,22 @@ cudaError_t fftconv_prepare(int P) {
     TFDP_PREP_ROWS(S, 2)                                                                      \
     TFDP_PREP_ROWS(S, 4)                                                                      \
     break;
-  switch (P) { TFDP_FFT_SIZES(TFDP_PREP) default: break; }
+#define TFDP_PREP_BIG(S)                                                                      \
+  case S:                                                                                     \
+    e = cudaFuncSetAttribute(aos::kspec_rows1_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, br1); \
+    if (e == cudaSuccess)                                                                     \
+      e = cudaFuncSetAttribute(aos::kspec_cols1_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, br1); \
+    if (e == cudaSuccess)                                                                     \
+      e = cudaFuncSetAttribute(aos::cols1_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, br1); \
+    TFDP_PREP_ROWS(S, 1)                                                                      \
+    break;
+  const int br1 = (int)rows_smem_bytes(P, 1);
+  switch (P) {
+    TFDP_FFT_SIZES(TFDP_PREP)
+    TFDP_FFT_SIZES_BIG(TFDP_PREP_BIG)
+    default: break;
+  }
+#undef TFDP_PREP_BIG
 #undef TFDP_PREP
 #undef TFDP_PREP_ROWS
   return e;
@@ -996,7 +1114,20 @@ void launch_kspec(const GridGeom* geom, int P, ForceArgs fa, const float2* tw, f
     launch_chained(kspec_cols_kernel<S>, (unsigned)((S / 2 + 4) / 4), fft_threads_c(S), sm, s, \
                    geom, KA, tw, KH);                                                       \
     break;
-  switch (P) { TFDP_FFT_SIZES(TFDP_KS) default: break; }
+#define TFDP_KS_BIG(S)                                                                      \
+  case S:                                                                                   \
+    aos::kspec_rows1_kernel<S><<<(unsigned)((S / 2 + 2) / 2), fft_threads_c(S), smb1, s>>>( \
+        geom, -fa.gamma, fa.gamma_int, tw, KA);                                             \
+    launch_chained(aos::kspec_cols1_kernel<S>, (unsigned)((S / 2 + 2) / 2), fft_threads_c(S), \
+                   smb1, s, geom, KA, tw, KH);                                              \
+    break;
+  const size_t smb1 = rows_smem_bytes(P, 1);
+  switch (P) {
+    TFDP_FFT_SIZES(TFDP_KS)
+    TFDP_FFT_SIZES_BIG(TFDP_KS_BIG)
+    default: break;
+  }
+#undef TFDP_KS_BIG
 #undef TFDP_KS
 }
 
@@ -1024,7 +1155,7 @@ void launch_rows_fwd(const GridGeom* geom, const float4* C, int cpitch, int P, i
   case S:                                                                                   \
     TFDP_ROWS_DISPATCH(S, aos::rows_fwd_kernel, geom, C, cpitch, tw, CA, ca_pitch, row0)    \
     break;
-  switch (P) { TFDP_FFT_SIZES(TFDP_RF) default: break; }
+  switch (P) { TFDP_FFT_SIZES_ALL(TFDP_RF) default: break; }
 #undef TFDP_RF
 }
 
@@ -1037,7 +1168,18 @@ void launch_cols(const GridGeom* geom, float2* CA, int ca_pitch, const float* KH
     cols_kernel<S><<<(unsigned)(3 * ((q1 - q0 + 1) / 2)), fft_threads_c(S), sm, s>>>(      \
         geom, CA, ca_pitch, KH, tw, q0, q1 - q0);                                           \
     break;
-  switch (P) { TFDP_FFT_SIZES(TFDP_CO) default: break; }
+#define TFDP_CO_BIG(S)                                                                      \
+  case S:                                                                                   \
+    launch_chained(aos::cols1_kernel<S>, (unsigned)(3 * (q1 - q0)), fft_threads_c(S), smb1, s, \
+                   geom, CA, ca_pitch, KH, tw, q0, q1 - q0);                                \
+    break;
+  const size_t smb1 = rows_smem_bytes(P, 1);
+  switch (P) {
+    TFDP_FFT_SIZES(TFDP_CO)
+    TFDP_FFT_SIZES_BIG(TFDP_CO_BIG)
+    default: break;
+  }
+#undef TFDP_CO_BIG
 #undef TFDP_CO
 }
 
@@ -1049,7 +1191,7 @@ void launch_rows_inv(const GridGeom* geom, const float2* CA, int ca_pitch, int P
   case S:                                                                                   \
     TFDP_ROWS_DISPATCH(S, aos::rows_inv_kernel, geom, CA, ca_pitch, tw, Phi, cpitch, C, row0) \
     break;
-  switch (P) { TFDP_FFT_SIZES(TFDP_RI) default: break; }
+  switch (P) { TFDP_FFT_SIZES_ALL(TFDP_RI) default: break; }
 #undef TFDP_RI
 }
 
