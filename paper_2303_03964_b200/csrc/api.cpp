@@ -40,13 +40,15 @@ enum Kind {
   K_ROWS_INV,
   K_GATHER_UPDATE,
   K_COMM,
+  K_HEAVY,
   K_COUNT
 };
 const char* kKindNames[K_COUNT] = {"exact_partial", "exact_finish", "bbox",     "setup",
                                    "reorder",       "spread",       "kspec_rows", "rows_fwd",
-                                   "cols",          "rows_inv",     "gather_update", "nccl"};
+                                   "cols",          "rows_inv",     "gather_update", "nccl",
+                                   "heavy_rows"};
 const bool kOwnKernel[K_COUNT] = {true, true, true, true, true, true,
-                                  true, true, true, true, true, false};
+                                  true, true, true, true, true, false, true};
 
 }  // namespace
 
@@ -108,6 +110,11 @@ struct tfdp_ctx {
   float2* xb = nullptr;
   int64_t alloc_xa = 0, alloc_xb = 0;
   float2* fbuf = nullptr;  // n float2: forces of all ranks (tfdp_forces of a reordered shard)
+  // heavy rows (kernels_heavy.cu): chunk index of the current CSR and the chunk sums
+  int64_t hv_items = 0;
+  long long* hv_first = nullptr;
+  float2* hv_part = nullptr;
+  void* hv_scratch = nullptr;
   // schedule
   int t = 0;
   std::vector<int32_t> ksched;
@@ -695,6 +702,14 @@ tfdp_status exchange_phi(const Group& G, int k) {
   return TFDP_OK;
 }
 
+// chunk sums of this shard's heavy rows (before the finishing kernel that adds them)
+void heavy_rows(tfdp_ctx* c, cudaStream_t st) {
+  if (!c->hv_items) return;
+  Scope sc(c, K_HEAVY, st);
+  tfdp::launch_heavy_attr(c->xy[c->cur], c->row_ptr, c->col, c->hv_first, c->lo, c->hi,
+                          c->hv_items, c->fa.beta, c->hv_part, st);
+}
+
 int pdl_max_fft() {
   static const int v = [] {  // TFDP_PDL_MAX_FFT overrides the threshold (A/B runs)
     const char* e = getenv("TFDP_PDL_MAX_FFT");
@@ -734,6 +749,7 @@ void fft_prologue(tfdp_ctx* c, int k, bool* overlap) {
     Scope sc(c, K_KSPEC, ks, 2);  // kspec_rows + kspec_cols
     tfdp::launch_kspec(c->geom, P, c->fa, c->tw[k], c->ka, c->kh[k], ks);
   }
+  heavy_rows(c, ks);  // also off the critical path; joined before cols (< gather_update)
   if (*overlap) cudaEventRecord(c->ev_join, c->side);
 }
 
@@ -762,6 +778,7 @@ tfdp_status evaluate_one(tfdp_ctx* c, int update, float eta, int k) {
       tfdp::launch_exact_partial(xy, c->n, c->lo, n_local, c->chunk, c->n_chunks, c->fa, c->part,
                                  c->stream);
     }
+    heavy_rows(c, c->stream);
     {
       Scope sc(c, K_EXACT_FINISH);
       tfdp::launch_exact_finish(xy, xyn, c->lo, n_local, c->n_chunks, c->part, c->row_ptr,
@@ -972,6 +989,10 @@ tfdp_status reorder_nodes(const Group& G) {
     std::swap(c->perm, c->perm2);
     std::swap(c->inv, c->inv2);
     c->cur ^= 1;
+    if (c->hv_items) {  // chunk index of the renumbered CSR
+      tfdp::launch_heavy_build(c->row_ptr, c->n, c->hv_first, c->hv_scratch, c->stream);
+      c->launches += 4;
+    }
     if (c->focus_on) {  // the mask follows the renumbering
       tfdp::launch_focus_slots(c->label_caller, c->perm, c->inv, c->n, c->region_caller,
                                c->region_m, c->label_slot, c->region_slot, c->stream);
@@ -1362,6 +1383,31 @@ tfdp_status tfdp_init(tfdp_ctx** out, int64_t n, const int64_t* row_ptr, const i
        (nnz > 0 && cudaMemcpyAsync(c->col_o, c->col, nnz * sizeof(int32_t),
                                    cudaMemcpyDeviceToDevice, s) != cudaSuccess)))
     return bail(fail(c, TFDP_ERR_CUDA, "CSR copy failed"));
+#define ALLOC2(ptr, bytes)                                                          \
+  if (cudaMalloc((void**)&(ptr), (bytes)) != cudaSuccess) {                         \
+    cudaGetLastError();                                                             \
+    return bail(fail(c, TFDP_ERR_OOM, "cudaMalloc(%zu) failed", (size_t)(bytes)));  \
+  }
+  {  // heavy rows: chunk count from the host CSR (permutation invariant)
+    int64_t items = 0;
+    for (int64_t i = 0; i < n; ++i) {
+      const int64_t d = row_ptr[i + 1] - row_ptr[i];
+      if (d > tfdp::kHeavyDeg) items += (d + tfdp::kHeavyChunk - 1) / tfdp::kHeavyChunk;
+    }
+    if (const char* e = getenv("TFDP_HEAVY"))  // TFDP_HEAVY=0: one thread per row (A/B runs)
+      if (e[0] == '0') items = 0;
+    if (items > 0) {
+      ALLOC2(c->hv_first, (n + 1) * sizeof(long long));
+      ALLOC2(c->hv_part, items * sizeof(float2));
+      ALLOC2(c->hv_scratch, tfdp::heavy_scratch_bytes(n));
+      c->hv_items = items;
+      tfdp::launch_heavy_build(c->row_ptr, n, c->hv_first, c->hv_scratch, s);
+      c->launches += 4;
+      c->fa.hv_first = c->hv_first;
+      c->fa.hv_part = c->hv_part;
+    }
+  }
+#undef ALLOC2
   tfdp::launch_reset_slots(c->box_part, s);
   if (p.solver == TFDP_IBFFT) {
     if (xy_dev) {  // box of a device layout: one bbox pass
@@ -1818,6 +1864,9 @@ void tfdp_destroy(tfdp_ctx* c) {
   cudaFree(c->xa);
   cudaFree(c->xb);
   cudaFree(c->fbuf);
+  cudaFree(c->hv_first);
+  cudaFree(c->hv_part);
+  cudaFree(c->hv_scratch);
   cudaFree(c->np_scratch);
   cudaFree(c->np_hits);
   cudaFree(c->np_hits2);

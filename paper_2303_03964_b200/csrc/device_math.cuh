@@ -64,13 +64,10 @@ __device__ __forceinline__ float key2f(unsigned int k) {
 // the -alpha factor: sum_j (1 + beta / (1 + d^2)) (x_i - x_j).  Four edges per round: all
 // column indices, then all neighbour positions are loaded before any arithmetic, so a
 // thread keeps up to 8 independent loads in flight (the row walk is latency-bound).
-__device__ __forceinline__ float2 attraction_sum(const float2* __restrict__ xy, float2 xi,
-                                                 const int64_t* __restrict__ row_ptr,
-                                                 const int32_t* __restrict__ col, int64_t i,
-                                                 float beta) {
+__device__ __forceinline__ float2 attraction_edges(const float2* __restrict__ xy, float2 xi,
+                                                   const int32_t* __restrict__ col, int64_t e,
+                                                   int64_t e1, float beta) {
   float sx = 0.f, sy = 0.f;
-  int64_t e = row_ptr[i];
-  const int64_t e1 = row_ptr[i + 1];
   auto term = [&](float2 xj) {
     const float dx = xi.x - xj.x, dy = xi.y - xj.y;
     const float s = fmaf(dx, dx, fmaf(dy, dy, 1.0f));
@@ -89,6 +86,34 @@ __device__ __forceinline__ float2 attraction_sum(const float2* __restrict__ xy, 
   }
   for (; e < e1; ++e) term(__ldg(xy + __ldg(col + e)));
   return make_float2(sx, sy);
+}
+
+__device__ __forceinline__ float2 attraction_sum(const float2* __restrict__ xy, float2 xi,
+                                                 const int64_t* __restrict__ row_ptr,
+                                                 const int32_t* __restrict__ col, int64_t i,
+                                                 float beta) {
+  return attraction_edges(xy, xi, col, row_ptr[i], row_ptr[i + 1], beta);
+}
+
+// Row sum with the heavy-row split: rows above kHeavyDeg edges add their precomputed chunk
+// sums in chunk order (kernels_heavy.cu); the others walk their edges.
+__device__ __forceinline__ float2 attraction_sum_hv(const float2* __restrict__ xy, float2 xi,
+                                                    const int64_t* __restrict__ row_ptr,
+                                                    const int32_t* __restrict__ col, int64_t i,
+                                                    const ForceArgs& fa) {
+  const int64_t e0 = row_ptr[i], e1 = row_ptr[i + 1];
+  if (fa.hv_part && e1 - e0 > kHeavyDeg) {
+    const long long f = fa.hv_first[i];
+    const int nc = (int)((e1 - e0 + kHeavyChunk - 1) / kHeavyChunk);
+    float sx = 0.f, sy = 0.f;
+    for (int c = 0; c < nc; ++c) {
+      const float2 q = fa.hv_part[f + c];
+      sx += q.x;
+      sy += q.y;
+    }
+    return make_float2(sx, sy);
+  }
+  return attraction_edges(xy, xi, col, e0, e1, fa.beta);
 }
 
 // Attraction row sum with the refinement mask's edge weight (la on edges whose both ends are

@@ -179,9 +179,9 @@ void launch_exact_partial(const float2* xy, int64_t n, int64_t lo, int64_t n_loc
 __device__ __forceinline__ float2 attraction_row(const float2* __restrict__ xy, float2 xi,
                                                  const int64_t* __restrict__ row_ptr,
                                                  const int32_t* __restrict__ col, int64_t i,
-                                                 float alpha, float beta) {
-  const float2 s = attraction_sum(xy, xi, row_ptr, col, i, beta);
-  return make_float2(-alpha * s.x, -alpha * s.y);
+                                                 const ForceArgs& fa) {
+  const float2 s = attraction_sum_hv(xy, xi, row_ptr, col, i, fa);
+  return make_float2(-fa.alpha * s.x, -fa.alpha * s.y);
 }
 
 __global__ void __launch_bounds__(kNodeThreads)
@@ -210,7 +210,7 @@ exact_finish_kernel(const float2* __restrict__ xy, float2* __restrict__ xy_next,
     const float2 as = attraction_sum_masked(xy, xi, row_ptr, col, i, fa.beta, fo.label, fo.la);
     A = make_float2(-fa.alpha * as.x, -fa.alpha * as.y);
   } else {
-    A = attraction_row(xy, xi, row_ptr, col, i, fa.alpha, fa.beta);
+    A = attraction_row(xy, xi, row_ptr, col, i, fa);
   }
   if (update) {
     const float nx = fmaf(eta, Rx + A.x, xi.x);

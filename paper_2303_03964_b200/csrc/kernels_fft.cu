@@ -538,7 +538,7 @@ gather_update_kernel(const float2* __restrict__ xy, float2* __restrict__ xy_next
       Ry = Rm.y;
       as = attraction_sum_masked(xy, p, row_ptr, col, i, fa.beta, fo.label, fo.la);
     } else {
-      as = attraction_sum(xy, p, row_ptr, col, i, fa.beta);
+      as = attraction_sum_hv(xy, p, row_ptr, col, i, fa);
     }
     const float ax = -fa.alpha * as.x, ay = -fa.alpha * as.y;
     if (update) {

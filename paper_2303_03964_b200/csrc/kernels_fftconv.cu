@@ -376,6 +376,66 @@ __device__ __forceinline__ void fft_rec(float4* buf, const float2* __restrict__ 
   }
 }
 
+// ---- convolution column: forward FFT -> x K^ -> inverse FFT with the forward's last stage
+// and the inverse's first stage fused in registers.  With radix 16 at both ends, the thread
+// that finishes forward butterfly j holds the outputs X[j + r N/16], r = 0..15 — exactly the
+// inputs x[j + r nb] (nb = N/16) of inverse first-stage butterfly j — so the product with
+// K^ and the first inverse butterfly need no shared-memory round trip (two of the ~14 passes
+// of a column pair).  The forward plan keeps a radix 16 for its last stage (16, ..., 16).
+template <int REM, bool FIRST>
+__host__ __device__ constexpr int radix_last16() {
+  return (FIRST || REM == 16) ? 16 : next_radix(REM / 16);
+}
+
+// forward stages while more than the final radix-16 stage remains (first stage: ZU, src)
+template <int T, int N, int Ns, int REM, class Src>
+__device__ __forceinline__ void fwd_head(float4* buf, const float2* __restrict__ tw, int tid,
+                                         const Src& src) {
+  if constexpr (REM > 16) {
+    constexpr int R = radix_last16<REM, Ns == 1>();
+    stage<T, R, N, Ns, Ns == 1, false>(buf, tw, tid, src, SmemIO{});
+    fwd_head<T, N, Ns * R, REM / R>(buf, tw, tid, src);
+  }
+}
+
+// forward last stage (radix 16, Ns = N/16) -> kmul(u, X[u]) (= conj(X K^)) -> inverse first
+// stage (radix 16, Ns = 1) -> shared memory
+template <int T, int N, class KMul>
+__device__ __forceinline__ void fused_mid(float4* buf, const float2* __restrict__ tw, int tid,
+                                          const KMul& kmul) {
+  constexpr int R = 16, nb = N / R, MB = (nb + T - 1) / T;
+  constexpr int sin_ = nb + (nb >> 4);
+  C2 v[MB][R];
+#pragma unroll
+  for (int b = 0; b < MB; ++b) {
+    const int j = tid + b * T;
+    if (nb % T == 0 || j < nb) {
+      const int pj = j + (j >> 4);
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[b][r] = ld(buf + pj + r * sin_);
+      float2 w[R];
+      twiddles<R>(tw, j, w);  // Ns = nb: k = j, step = 1
+#pragma unroll
+      for (int r = 1; r < R; ++r) v[b][r] = mulw(v[b][r], w[r].x, w[r].y);
+      dft16<false>(v[b]);
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[b][r] = kmul(j + r * nb, v[b][r]);
+      dft16<false>(v[b]);  // inverse first stage: inputs at j + r nb
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int b = 0; b < MB; ++b) {
+    const int j = tid + b * T;
+    if (nb % T == 0 || j < nb) {
+      const int d = j * R;  // first-stage outputs: d = j R + r
+#pragma unroll
+      for (int r = 0; r < R; ++r) st(buf + (d + r) + ((d + r) >> 4), v[b][r]);
+    }
+  }
+  __syncthreads();
+}
+
 // Forward complex FFTs (both lanes) of N elements, N = 2^a 3^b 5^c, N % 256 == 0, in the
 // padded shared buffer (in place) — inputs from src / outputs to dst when those are not
 // SmemIO.  Radix 16 first (so Ns is a multiple of 16 afterwards), then 16/8/4/2, then 3, 5.
@@ -538,12 +598,10 @@ TFDP_FFT_KERNEL(cols_kernel)(const GridGeom* __restrict__ geom, float2* __restri
     }
     return C2{make_float2(va.x, vb.x), make_float2(va.y, vb.y)};
   };
-  auto mult = [&](int u, C2 z) {  // x K^ (real), conjugated for the inverse
+  auto kmul = [&](int u, C2 z) {  // x K^ (real), conjugated for the inverse
     const float2 k = make_float2(__ldg(khA + u), __ldg(khB + u));
-    st(a + pad(u), C2{__fmul2_rn(z.re, k), __fmul2_rn(z.im, neg2(k))});
+    return C2{__fmul2_rn(z.re, k), __fmul2_rn(z.im, neg2(k))};
   };
-  fft_smem<T, P, kZeroUpper>(a, tws, src, mult);
-  __syncthreads();
   auto out = [&](int u, C2 z) {  // u < P/2 (LowOut)
     if (u < M) {
       const int64_t o = ca_row_off(u, H);
@@ -551,7 +609,19 @@ TFDP_FFT_KERNEL(cols_kernel)(const GridGeom* __restrict__ geom, float2* __restri
       if (hB) colB[o] = make_float2(z.re.y, -z.im.y);
     }
   };
-  fft_smem<T, P, kLowOut>(a, tws, SmemIO{}, out);
+  // Fused only where it measured faster (C4, us per launch, separate / fused): P = 2048
+  // 31.1 / 29.1; P = 4096 120.1 / 127.3 and P = 6144 346.4 / 348.6 — there the fused middle
+  // holds both radix-16 butterflies and the K^ loads live at the 80-register cap (spills).
+  if constexpr (P <= 2048) {
+    fwd_head<T, P, 1, P>(a, tws, threadIdx.x, src);  // forward stages but the last
+    fused_mid<T, P>(a, tws, threadIdx.x, kmul);       // last forward, x K^, first inverse
+    fft_rec<T, P, kLowOut, 16, P / 16>(a, tws, threadIdx.x, SmemIO{}, out);
+  } else {
+    auto mult = [&](int u, C2 z) { st(a + pad(u), kmul(u, z)); };
+    fft_smem<T, P, kZeroUpper>(a, tws, src, mult);
+    __syncthreads();
+    fft_smem<T, P, kLowOut>(a, tws, SmemIO{}, out);
+  }
 }
 
 // ================================================================ AoS core (row passes)

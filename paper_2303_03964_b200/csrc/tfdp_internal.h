@@ -43,10 +43,19 @@ struct BoxKeys {
   unsigned int minx, miny, maxx, maxy;
 };
 
+// High-degree rows (degree skew, power-law graphs): a row with more than kHeavyDeg edges is
+// not walked by one thread; its attraction sum comes in chunks of kHeavyChunk edges, one
+// warp per chunk (kernels_heavy.cu), summed by the row's thread in chunk order
+// (deterministic, R15).  hv_first[i] = first chunk of row i (exclusive scan over rows).
+constexpr int kHeavyDeg = 128;
+constexpr int kHeavyChunk = 256;
+
 // Kernel-side parameters of the force law.
 struct ForceArgs {
   float alpha, beta, gamma, rho;
   int gamma_int;  // 1..8 if gamma is that integer, else 0 (general path)
+  const long long* hv_first;  // [n + 1] or nullptr (no heavy rows)
+  const float2* hv_part;      // chunk sums of the heavy rows (sum (1 + beta/s)(x_i - x_j))
 };
 
 // Local (fisheye) refinement mask (SPEC RefinementMask): label[i] = 1 for the focal
@@ -194,6 +203,15 @@ void launch_gather_update(const float2* xy, float2* xy_next, int64_t lo, int64_t
                           FocusArgs fo, float eta, int iter, int update, float2* rep_out,
                           float2* att_out, unsigned long long* diverge, BoxKeys* next_part,
                           cudaStream_t s);
+
+// heavy rows (kernels_heavy.cu): build the chunk index of the current CSR (scratch: 8 (n+1)
+// + sums bytes, heavy_scratch_bytes), then the chunk sums for the rows [lo, hi)
+size_t heavy_scratch_bytes(int64_t n);
+void launch_heavy_build(const int64_t* row_ptr, int64_t n, long long* first, void* scratch,
+                        cudaStream_t s);
+void launch_heavy_attr(const float2* xy, const int64_t* row_ptr, const int32_t* col,
+                       const long long* first, int64_t lo, int64_t hi, int64_t n_items_max,
+                       float beta, float2* part, cudaStream_t s);
 
 // PivotMDS initialisation (kernels_pmds.cu): caller-order CSR, p <= pmds_max_pivots();
 // xy (device, n) receives the layout, pivots_out (host, p) the pivots.
