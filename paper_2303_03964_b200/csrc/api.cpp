@@ -110,6 +110,14 @@ struct tfdp_ctx {
   float2* xb = nullptr;
   int64_t alloc_xa = 0, alloc_xb = 0;
   float2* fbuf = nullptr;  // n float2: forces of all ranks (tfdp_forces of a reordered shard)
+  // slab mode with fused exchanges (peer routes, tfdp_internal.h PeerRoute): one route per k
+  // in device memory; NCCL contexts map the peers' buffers with CUDA IPC (re-mapped after any
+  // re-allocation), virtual ranks get the other contexts' pointers from the group call
+  bool p2p = false;
+  bool route_dirty = true;
+  tfdp::PeerRoute* d_route = nullptr;  // [4]
+  int* bar = nullptr;                  // barrier word of the NCCL phase barriers
+  std::vector<void*> ipc_open;         // peer mappings to close
   // heavy rows (kernels_heavy.cu): chunk index of the current CSR and the chunk sums
   int64_t hv_items = 0;
   long long* hv_first = nullptr;
@@ -484,6 +492,7 @@ tfdp_status configure_fft(tfdp_ctx* c, float L) {
     c->alloc_planes = planes;
     c->alloc_ca = ca;
     c->alloc_ka = ka;
+    c->route_dirty = true;
   }
   for (int k = 1; k <= 3; ++k) {
     if (!k_used(c, k)) continue;
@@ -536,6 +545,7 @@ tfdp_status configure_fft(tfdp_ctx* c, float L) {
       CUDA_TRY(c, cudaMalloc(&c->xb, xb * sizeof(float2)));
       c->alloc_xa = xa;
       c->alloc_xb = xb;
+      c->route_dirty = true;
     }
   }
   CUDA_TRY(c, cudaGetLastError());
@@ -563,9 +573,13 @@ tfdp_status dcopy(tfdp_ctx* c, void* dst, const void* src, size_t bytes) {
 
 // Position all-gather: every rank's own slice [lo, hi) of xy (the update's output buffer)
 // to every other rank.
+tfdp_status phase_barrier(const Group& G);
+
 tfdp_status exchange_positions(const Group& G, int buf) {
   tfdp_ctx* c = G[0];
   if (c->world == 1) return TFDP_OK;
+  if (c->slab && c->p2p && c->p.solver == TFDP_IBFFT)  // gather_update stored into every rank
+    return phase_barrier(G);
   if (G.virt()) {
     for (int r = 0; r < G.p; ++r)
       for (int s = 0; s < G.p; ++s)
@@ -844,6 +858,180 @@ tfdp_status evaluate_one(tfdp_ctx* c, int update, float eta, int k) {
   return TFDP_OK;
 }
 
+// ---------------------------------------------------------------- slab mode: peer routes
+// Phase barrier of the fused exchanges: NCCL contexts order the ranks with a one-word
+// all-reduce on the ctx stream (every rank's previous kernels, and so its peer stores, have
+// completed before any rank passes it); the virtual ranks of one device share a stream.
+tfdp_status phase_barrier(const Group& G) {
+  tfdp_ctx* c = G[0];
+  if (G.virt() || c->world == 1) return TFDP_OK;
+  Scope sc(c, K_COMM);
+  NCCL_TRY(c, c->nccl->AllReduce(c->bar, c->bar, 1, ncclInt32, ncclMax, c->comm, c->stream));
+  return TFDP_OK;
+}
+
+void fill_route(tfdp_ctx* c, int k, tfdp::PeerRoute* r, void* const* xb, void* const* ca,
+                void* const* phi, void* const* xy0, void* const* xy1) {
+  const tfdp::SlabPlan& pl = c->plan[k];
+  memset(r, 0, sizeof(*r));
+  r->world = c->world;
+  r->rank = c->rank;
+  r->R = pl.R;
+  r->ca_pitch = c->ca_pitch;
+  for (int j = 0; j <= c->world; ++j) {
+    r->row0[j] = pl.row0[j];
+    r->q0[j] = pl.q0[j];
+  }
+  for (int j = 0; j < c->world; ++j) {
+    r->xb[j] = static_cast<float2*>(xb[j]);
+    r->ca[j] = static_cast<float2*>(ca[j]);
+    r->phi[j] = static_cast<float*>(phi[j]);
+    r->xy[0][j] = static_cast<float2*>(xy0[j]);
+    r->xy[1][j] = static_cast<float2*>(xy1[j]);
+  }
+}
+
+// Routes of every rank of the group: the virtual ranks' own pointers, or the peers' buffers
+// mapped with CUDA IPC (handles exchanged with NCCL broadcasts; collective, and repeated after
+// a re-allocation, which every rank makes at the same call since the plans are identical).
+tfdp_status setup_routes(const Group& G) {
+  tfdp_ctx* c0 = G[0];
+  const int p = c0->world;
+  tfdp::PeerRoute h[4];
+  if (G.virt()) {
+    std::vector<void*> xb(p), ca(p), phi(p), xy0(p), xy1(p);
+    for (int j = 0; j < p; ++j) {
+      xb[j] = G[j]->xb;
+      ca[j] = G[j]->ca;
+      phi[j] = G[j]->phi;
+      xy0[j] = G[j]->xy[0];
+      xy1[j] = G[j]->xy[1];
+    }
+    for (int i = 0; i < G.p; ++i) {
+      tfdp_ctx* c = G[i];
+      for (int k = 1; k <= 3; ++k)
+        if (k_used(c, k)) fill_route(c, k, &h[k], xb.data(), ca.data(), phi.data(), xy0.data(), xy1.data());
+      CUDA_TRY(c, cudaMemcpyAsync(c->d_route, h, sizeof h, cudaMemcpyHostToDevice, c->stream));
+      c->route_dirty = false;
+    }
+    return TFDP_OK;
+  }
+  tfdp_ctx* c = c0;
+  if (!c->route_dirty) return TFDP_OK;
+  for (void* q : c->ipc_open) cudaIpcCloseMemHandle(q);
+  c->ipc_open.clear();
+  constexpr int kB = 5;  // buffers per rank: xb, ca, phi, xy0, xy1
+  std::vector<cudaIpcMemHandle_t> mine(kB);
+  void* bufs[kB] = {c->xb, c->ca, c->phi, c->xy[0], c->xy[1]};
+  for (int b = 0; b < kB; ++b) CUDA_TRY(c, cudaIpcGetMemHandle(&mine[b], bufs[b]));
+  const size_t hs = sizeof(cudaIpcMemHandle_t) * kB;
+  unsigned char* dh = nullptr;
+  CUDA_TRY(c, cudaMalloc(&dh, hs * p));
+  std::vector<unsigned char> all(hs * p);
+  CUDA_TRY(c, cudaMemcpyAsync(dh + hs * c->rank, mine.data(), hs, cudaMemcpyHostToDevice, c->stream));
+  NCCL_TRY(c, c->nccl->GroupStart());
+  for (int r = 0; r < p; ++r)
+    NCCL_TRY(c, c->nccl->Broadcast(dh + hs * r, dh + hs * r, hs, ncclChar, r, c->comm, c->stream));
+  NCCL_TRY(c, c->nccl->GroupEnd());
+  CUDA_TRY(c, cudaMemcpyAsync(all.data(), dh, hs * p, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  cudaFree(dh);
+  std::vector<void*> ptr[kB];
+  for (int b = 0; b < kB; ++b) ptr[b].resize(p);
+  for (int r = 0; r < p; ++r)
+    for (int b = 0; b < kB; ++b) {
+      if (r == c->rank) {
+        ptr[b][r] = bufs[b];
+        continue;
+      }
+      cudaIpcMemHandle_t hh;
+      memcpy(&hh, all.data() + hs * r + sizeof(cudaIpcMemHandle_t) * b, sizeof hh);
+      void* q = nullptr;
+      if (cudaIpcOpenMemHandle(&q, hh, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess) {
+        c->ipc_open.push_back(q);
+      } else {
+        cudaGetLastError();
+        q = nullptr;
+      }
+      ptr[b][r] = q;
+    }
+  // every rank must be able to map every peer, else all fall back to the copy exchanges
+  int ok = 1;
+  for (int b = 0; b < kB; ++b)
+    for (int r = 0; r < p; ++r) ok &= ptr[b][r] != nullptr;
+  CUDA_TRY(c, cudaMemcpyAsync(c->bar, &ok, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+  NCCL_TRY(c, c->nccl->AllReduce(c->bar, c->bar, 1, ncclInt32, ncclMin, c->comm, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(&ok, c->bar, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  if (!ok) {
+    for (void* q : c->ipc_open) cudaIpcCloseMemHandle(q);
+    c->ipc_open.clear();
+    c->p2p = false;
+    return TFDP_OK;
+  }
+  for (int k = 1; k <= 3; ++k)
+    if (k_used(c, k))
+      fill_route(c, k, &h[k], ptr[0].data(), ptr[1].data(), ptr[2].data(), ptr[3].data(), ptr[4].data());
+  CUDA_TRY(c, cudaMemcpyAsync(c->d_route, h, sizeof h, cudaMemcpyHostToDevice, c->stream));
+  c->route_dirty = false;
+  return TFDP_OK;
+}
+
+// Slab mode with the exchanges fused into the producing kernels (p2p): rows_fwd stores into
+// the column owners' receive buffers, cols into the row owners' half spectra, rows_inv its
+// potential rows and gather_update the new positions into every rank — no pack / unpack, no
+// separate transfers; three phase barriers per evaluation (plus the position barrier).
+tfdp_status evaluate_slab_p2p(const Group& G, int update, float eta, int k) {
+  TRY(setup_routes(G));
+  bool overlap[tfdp::kMaxWorld];
+  for (int i = 0; i < G.p; ++i) {  // phase A: spread of the slab, row FFTs -> peers' xb
+    tfdp_ctx* c = G[i];
+    const tfdp::SlabPlan& pl = c->plan[k];
+    const int r = c->rank;
+    fft_prologue(c, k, &overlap[i]);
+    float4* grid4 = reinterpret_cast<float4*>(c->grid);
+    {
+      Scope sc(c, K_SPREAD);
+      tfdp::launch_spread(c->xy[c->cur], 0, c->n, c->geom, k, grid4, c->stream,
+                          pl.row0[r] / k, pl.row0[r + 1] / k);
+    }
+    Scope sc(c, K_ROWS_FWD);
+    tfdp::launch_rows_fwd(c->geom, grid4, pitch_k(c, k), c->P_of_k[k], pl.row0[r], pl.row0[r + 1],
+                          c->tw[k], c->ca, c->ca_pitch, c->stream, c->d_route + k);
+  }
+  TRY(phase_barrier(G));
+  for (int i = 0; i < G.p; ++i) {  // phase B: column pass of the chunk -> row owners' CA
+    tfdp_ctx* c = G[i];
+    const tfdp::SlabPlan& pl = c->plan[k];
+    if (overlap[i]) CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+    Scope sc(c, K_COLS);
+    tfdp::launch_cols(c->geom, c->xb, pl.R, c->kh[k], c->P_of_k[k], c->tw[k], pl.q0[c->rank],
+                      pl.q0[c->rank + 1], c->stream, c->d_route + k);
+  }
+  TRY(phase_barrier(G));
+  for (int i = 0; i < G.p; ++i) {  // phase C: inverse rows of the slab -> every rank's Phi
+    tfdp_ctx* c = G[i];
+    const tfdp::SlabPlan& pl = c->plan[k];
+    Scope sc(c, K_ROWS_INV);
+    tfdp::launch_rows_inv(c->geom, c->ca, c->ca_pitch, c->P_of_k[k], pl.row0[c->rank],
+                          pl.row0[c->rank + 1], c->tw[k], c->phi, pitch_k(c, k),
+                          reinterpret_cast<float4*>(c->grid), c->stream, c->d_route + k);
+  }
+  TRY(phase_barrier(G));
+  for (int i = 0; i < G.p; ++i) {  // phase D: own nodes -> every rank's next positions
+    tfdp_ctx* c = G[i];
+    const tfdp::FocusArgs fo = focus_prologue(c);
+    Scope sc(c, K_GATHER_UPDATE);
+    tfdp::launch_gather_update(c->xy[c->cur], c->xy[c->cur ^ 1], c->lo, c->hi - c->lo, c->geom, k,
+                               c->phi, c->row_ptr, c->col, c->fa, fo, eta, c->t, update, c->rep,
+                               c->att, c->diverge, nullptr, c->stream,
+                               update ? c->d_route + k : nullptr, c->cur ^ 1);
+    c->box_valid = false;
+    CUDA_TRY(c, cudaGetLastError());
+  }
+  return TFDP_OK;
+}
+
 // ---------------------------------------------------------------- slab mode (p > 1, ibFFT)
 // Per iteration, every rank r: box + setup from the full positions; spread of
 // the nodes in its grid-row slab; row FFTs of that slab; transpose 1; column pass on its
@@ -913,7 +1101,7 @@ tfdp_status evaluate(const Group& G, int update, float eta, int k) {
     if (!G.virt() && !c0->comm)
       return fail(c0, TFDP_ERR_UNSUPPORTED,
                   "slab mode of a virtual shard context: use tfdp_group_step / tfdp_group_forces");
-    TRY(evaluate_slab(G, update, eta, k));
+    TRY(c0->p2p ? evaluate_slab_p2p(G, update, eta, k) : evaluate_slab(G, update, eta, k));
   } else {
     for (int i = 0; i < G.p; ++i) TRY(evaluate_one(G[i], update, eta, k));
   }
@@ -1334,6 +1522,8 @@ tfdp_status tfdp_init(tfdp_ctx** out, int64_t n, const int64_t* row_ptr, const i
   ALLOC(c->box_part, tfdp::kBoxSlots * sizeof(BoxKeys));
   ALLOC(c->geom, sizeof(GridGeom));
   ALLOC(c->kkey, 4 * sizeof(tfdp::KspecKey));
+  ALLOC(c->d_route, 4 * sizeof(tfdp::PeerRoute));
+  ALLOC(c->bar, sizeof(int));
   if (cudaMemsetAsync(c->kkey, 0, 4 * sizeof(tfdp::KspecKey), c->stream ? c->stream : 0) != cudaSuccess)
     return bail(fail(c, TFDP_ERR_CUDA, "kkey memset"));
   if (cudaMallocHost((void**)&c->h_status, 2 * sizeof(unsigned long long) + sizeof(GridGeom)) !=
@@ -1350,6 +1540,10 @@ tfdp_status tfdp_init(tfdp_ctx** out, int64_t n, const int64_t* row_ptr, const i
   c->slab = c->world > 1 && p.solver == TFDP_IBFFT && p.dist_mode == TFDP_DIST_SLAB;
   if (c->slab && c->world > tfdp::kMaxWorld)
     return bail(fail(c, TFDP_ERR_ARG, "slab mode supports world <= %d", tfdp::kMaxWorld));
+  if (c->slab) {  // fused exchanges (peer stores) unless TFDP_P2P=0 (the NCCL / copy path)
+    const char* e = getenv("TFDP_P2P");
+    c->p2p = !(e && e[0] == '0');
+  }
   // internal renumbering: one GPU, or the slab mode (every rank renumbers identically: rank
   // 0's permutation is broadcast)
   c->reorder = p.solver == TFDP_IBFFT && p.node_order == TFDP_ORDER_AUTO && n >= 65536 &&
@@ -1864,6 +2058,9 @@ void tfdp_destroy(tfdp_ctx* c) {
   cudaFree(c->xa);
   cudaFree(c->xb);
   cudaFree(c->fbuf);
+  for (void* q : c->ipc_open) cudaIpcCloseMemHandle(q);
+  cudaFree(c->d_route);
+  cudaFree(c->bar);
   cudaFree(c->hv_first);
   cudaFree(c->hv_part);
   cudaFree(c->hv_scratch);

@@ -499,7 +499,7 @@ gather_update_kernel(const float2* __restrict__ xy, float2* __restrict__ xy_next
                      const int32_t* __restrict__ col, ForceArgs fa, FocusArgs fo, float eta,
                      int iter, int update, float2* __restrict__ rep_out,
                      float2* __restrict__ att_out, unsigned long long* diverge,
-                     BoxKeys* next_part) {
+                     BoxKeys* next_part, const PeerRoute* __restrict__ rt, int next_buf) {
   pdl_wait();
   pdl_trigger();
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -545,6 +545,9 @@ gather_update_kernel(const float2* __restrict__ xy, float2* __restrict__ xy_next
       const float nx = fmaf(eta, Rx + ax, p.x);
       const float ny = fmaf(eta, Ry + ay, p.y);
       xy_next[i] = make_float2(nx, ny);
+      if (rt)  // slab mode, fused position all-gather: into every other rank's copy
+        for (int j = 0; j < rt->world; ++j)
+          if (j != rt->rank) rt->xy[next_buf][j][i] = make_float2(nx, ny);
       if (!isfinite(nx) || !isfinite(ny)) {
         atomicMin(diverge, ((unsigned long long)(unsigned)iter << 32) | (unsigned long long)i);
       } else {
@@ -564,13 +567,13 @@ void launch_gather_update(const float2* xy, float2* xy_next, int64_t lo, int64_t
                           const int64_t* row_ptr, const int32_t* col, ForceArgs fa,
                           FocusArgs fo, float eta, int iter, int update, float2* rep_out,
                           float2* att_out, unsigned long long* diverge, BoxKeys* next_part,
-                          cudaStream_t s) {
+                          cudaStream_t s, const PeerRoute* route, int next_buf) {
   if (n_local <= 0) return;
   const unsigned blocks = (unsigned)((n_local + kNodeThreads - 1) / kNodeThreads);
 #define TFDP_GU(KK)                                                                         \
   launch_chained(gather_update_kernel<KK>, blocks, kNodeThreads, 0, s, xy, xy_next, lo,      \
                  n_local, geom, phi, row_ptr, col, fa, fo, eta, iter, update, rep_out, att_out, \
-                 diverge, next_part)
+                 diverge, next_part, route, next_buf)
   if (k == 1) TFDP_GU(1);
   else if (k == 2) TFDP_GU(2);
   else TFDP_GU(3);

@@ -473,6 +473,17 @@ __device__ __forceinline__ float ksample(float s, float neg_gamma, int gi) {
   }
 }
 
+// Slab-mode output of the column pass (out of line: keeps the one-GPU column pass's register
+// allocation unchanged): rows u of columns (chA, qA), (chB, qB) into the row owner's CA.
+__device__ __noinline__ void route_store_cols(const PeerRoute* __restrict__ rt, int u, int H,
+                                              int chA, int qA, int chB, int qB, bool hB,
+                                              float2 re, float2 im) {
+  float2* ca = rt->ca[route_owner(rt->row0, rt->world, u)];
+  const int64_t o = ca_row_off(u, H);
+  ca[ca_col_base(chA, qA, H, rt->ca_pitch) + o] = make_float2(re.x, -im.x);
+  if (hB) ca[ca_col_base(chB, qB, H, rt->ca_pitch) + o] = make_float2(re.y, -im.y);
+}
+
 #define TFDP_FFT_KERNEL(name) \
   template <int P>            \
   __global__ void __launch_bounds__(fft_threads_c(P), kMinBlocks<fft_threads_c(P)>) name
@@ -567,7 +578,8 @@ TFDP_FFT_KERNEL(kspec_cols_kernel)(const GridGeom* __restrict__ geom,
 // the inverse) in its last; the inverse FFT writes rows 0..M-1 from its last stage.
 TFDP_FFT_KERNEL(cols_kernel)(const GridGeom* __restrict__ geom, float2* __restrict__ CA,
                              int ca_pitch, const float* __restrict__ KH,
-                             const float2* __restrict__ tw, int q_base, int Hl) {
+                             const float2* __restrict__ tw, int q_base, int Hl,
+                             const PeerRoute* __restrict__ rt) {
   TFDP_FFT_PROLOGUE
   const int M = geom->M;
   constexpr int half = P / 2;
@@ -604,9 +616,13 @@ TFDP_FFT_KERNEL(cols_kernel)(const GridGeom* __restrict__ geom, float2* __restri
   };
   auto out = [&](int u, C2 z) {  // u < P/2 (LowOut)
     if (u < M) {
-      const int64_t o = ca_row_off(u, H);
-      colA[o] = make_float2(z.re.x, -z.im.x);
-      if (hB) colB[o] = make_float2(z.re.y, -z.im.y);
+      if (rt) {  // slab mode, fused transpose back: into the row owner's half spectra
+        route_store_cols(rt, u, half + 1, chA, qA, chB, qB, hB, z.re, z.im);
+      } else {
+        const int64_t o = ca_row_off(u, H);
+        colA[o] = make_float2(z.re.x, -z.im.x);
+        if (hB) colB[o] = make_float2(z.re.y, -z.im.y);
+      }
     }
   };
   // Fused only where it measured faster (C4, us per launch, separate / fused): P = 2048
@@ -866,7 +882,8 @@ constexpr int rows_min_blocks() {
 template <int P, int RB>
 __global__ void __launch_bounds__(fft_threads_c(P) * RB, (rows_min_blocks<P, RB>()))
 rows_fwd_kernel(const GridGeom* __restrict__ geom, const float4* __restrict__ C, int cpitch,
-                const float2* __restrict__ tw, float2* __restrict__ CA, int ca_pitch, int row0) {
+                const float2* __restrict__ tw, float2* __restrict__ CA, int ca_pitch, int row0,
+                const PeerRoute* __restrict__ rt) {
   constexpr int T = fft_threads_c(P);
   constexpr int NT = T * RB;
   constexpr int PL = padded_len(P);
@@ -911,7 +928,15 @@ rows_fwd_kernel(const GridGeom* __restrict__ geom, const float4* __restrict__ C,
     const float2 zc = conjf2(ag[pad(q == 0 ? 0 : P - q)]);
     const float2 xa = make_float2(0.5f * (z.x + zc.x), 0.5f * (z.y + zc.y));
     const float2 xb = mul_mi(make_float2(0.5f * (z.x - zc.x), 0.5f * (z.y - zc.y)));
-    float2* o = CA + ca_col_base(ch, q, H, ca_pitch) + ca_row_off(2 * p0 + 2 * gg, H);
+    float2* o;
+    if (rt) {  // slab mode, fused transpose: straight into the column owner's receive buffer
+      const int r = 2 * p0 + 2 * gg, s = route_owner(rt->q0, rt->world, q);
+      const int nq = rt->q0[s + 1] - rt->q0[s];
+      o = rt->xb[s] + (((int64_t)ch * (rt->R / kCaTile) + r / kCaTile) * nq + (q - rt->q0[s])) * kCaTile +
+          r % kCaTile;
+    } else {
+      o = CA + ca_col_base(ch, q, H, ca_pitch) + ca_row_off(2 * p0 + 2 * gg, H);
+    }
     if (2 * gg + 1 < rows_here) *reinterpret_cast<float4*>(o) = make_float4(xa.x, xa.y, xb.x, xb.y);
     else *o = xa;
   }
@@ -924,7 +949,7 @@ template <int P, int RB>
 __global__ void __launch_bounds__(fft_threads_c(P) * RB, (rows_min_blocks<P, RB>()))
 rows_inv_kernel(const GridGeom* __restrict__ geom, const float2* __restrict__ CA, int ca_pitch,
                 const float2* __restrict__ tw, float* __restrict__ Phi, int cpitch,
-                float4* __restrict__ C, int row0) {
+                float4* __restrict__ C, int row0, const PeerRoute* __restrict__ rt) {
   constexpr int T = fft_threads_c(P);
   constexpr int NT = T * RB;
   constexpr int PL = padded_len(P);
@@ -981,6 +1006,18 @@ rows_inv_kernel(const GridGeom* __restrict__ geom, const float2* __restrict__ CA
     const float2 z = a[pad(x)];  // conj(result) = xa + i xb
     pa[x] = z.x;
     if (hb) pb[x] = -z.y;
+  }
+  if (rt) {  // slab mode, fused potential exchange: the same rows into every other rank
+    const int64_t off = pa - Phi;
+    for (int j = 0; j < rt->world; ++j) {
+      if (j == rt->rank) continue;
+      float* qa = rt->phi[j] + off;
+      for (int x = lt; x < M; x += T) {
+        const float2 z = a[pad(x)];
+        qa[x] = z.x;
+        if (hb) qa[cpitch + x] = -z.y;
+      }
+    }
   }
 }
 
@@ -1054,7 +1091,8 @@ kspec_cols1_kernel(const GridGeom* __restrict__ geom, const float* __restrict__ 
 template <int P>
 __global__ void __launch_bounds__(fft_threads_c(P), 1)
 cols1_kernel(const GridGeom* __restrict__ geom, float2* __restrict__ CA, int ca_pitch,
-             const float* __restrict__ KH, const float2* __restrict__ tw, int q_base, int Hl) {
+             const float* __restrict__ KH, const float2* __restrict__ tw, int q_base, int Hl,
+             const PeerRoute* __restrict__ rt) {
   constexpr int T = fft_threads_c(P), half = P / 2;
   extern __shared__ float2 sm[];
   float2* a = sm;
@@ -1080,7 +1118,11 @@ cols1_kernel(const GridGeom* __restrict__ geom, float2* __restrict__ CA, int ca_
   fft_smem<T, P, kLowOut>(a, tws);
   for (int u = threadIdx.x; u < M; u += T) {
     const float2 z = a[pad(u)];
-    col[ca_row_off(u, Hl)] = make_float2(z.x, -z.y);
+    if (rt)  // slab mode: into the row owner's half spectra (as cols_kernel)
+      rt->ca[route_owner(rt->row0, rt->world, u)][ca_col_base(ch, q, half + 1, rt->ca_pitch) +
+                                                  ca_row_off(u, half + 1)] = make_float2(z.x, -z.y);
+    else
+      col[ca_row_off(u, Hl)] = make_float2(z.x, -z.y);
   }
 }
 
@@ -1219,29 +1261,30 @@ void launch_kspec(const GridGeom* geom, int P, ForceArgs fa, const float2* tw, f
   }
 
 void launch_rows_fwd(const GridGeom* geom, const float4* C, int cpitch, int P, int row0,
-                     int row1, const float2* tw, float2* CA, int ca_pitch, cudaStream_t s) {
+                     int row1, const float2* tw, float2* CA, int ca_pitch, cudaStream_t s,
+                     const PeerRoute* route) {
   if (row1 <= row0) return;
 #define TFDP_RF(S)                                                                          \
   case S:                                                                                   \
-    TFDP_ROWS_DISPATCH(S, aos::rows_fwd_kernel, geom, C, cpitch, tw, CA, ca_pitch, row0)    \
+    TFDP_ROWS_DISPATCH(S, aos::rows_fwd_kernel, geom, C, cpitch, tw, CA, ca_pitch, row0, route) \
     break;
   switch (P) { TFDP_FFT_SIZES_ALL(TFDP_RF) default: break; }
 #undef TFDP_RF
 }
 
 void launch_cols(const GridGeom* geom, float2* CA, int ca_pitch, const float* KH, int P,
-                 const float2* tw, int q0, int q1, cudaStream_t s) {
+                 const float2* tw, int q0, int q1, cudaStream_t s, const PeerRoute* route) {
   if (q1 <= q0) return;
   const size_t sm = fftconv_smem_bytes(P);
 #define TFDP_CO(S)                                                                          \
   case S:                                                                                   \
     cols_kernel<S><<<(unsigned)(3 * ((q1 - q0 + 1) / 2)), fft_threads_c(S), sm, s>>>(      \
-        geom, CA, ca_pitch, KH, tw, q0, q1 - q0);                                           \
+        geom, CA, ca_pitch, KH, tw, q0, q1 - q0, route);                                    \
     break;
 #define TFDP_CO_BIG(S)                                                                      \
   case S:                                                                                   \
     launch_chained(aos::cols1_kernel<S>, (unsigned)(3 * (q1 - q0)), fft_threads_c(S), smb1, s, \
-                   geom, CA, ca_pitch, KH, tw, q0, q1 - q0);                                \
+                   geom, CA, ca_pitch, KH, tw, q0, q1 - q0, route);                         \
     break;
   const size_t smb1 = rows_smem_bytes(P, 1);
   switch (P) {
@@ -1255,11 +1298,12 @@ void launch_cols(const GridGeom* geom, float2* CA, int ca_pitch, const float* KH
 
 void launch_rows_inv(const GridGeom* geom, const float2* CA, int ca_pitch, int P, int row0,
                      int row1, const float2* tw, float* Phi, int cpitch, float4* C,
-                     cudaStream_t s) {
+                     cudaStream_t s, const PeerRoute* route) {
   if (row1 <= row0) return;
 #define TFDP_RI(S)                                                                          \
   case S:                                                                                   \
-    TFDP_ROWS_DISPATCH(S, aos::rows_inv_kernel, geom, CA, ca_pitch, tw, Phi, cpitch, C, row0) \
+    TFDP_ROWS_DISPATCH(S, aos::rows_inv_kernel, geom, CA, ca_pitch, tw, Phi, cpitch, C, row0, \
+                       route)                                                               \
     break;
   switch (P) { TFDP_FFT_SIZES_ALL(TFDP_RI) default: break; }
 #undef TFDP_RI

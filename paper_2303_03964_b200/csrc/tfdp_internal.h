@@ -131,25 +131,6 @@ void launch_setup(BoxKeys* slots, int n_part, BoxKeys* keys, GridGeom* geom, int
 void launch_spread(const float2* xy, int64_t lo, int64_t cnt, const GridGeom* geom, int k,
                    float4* grid, cudaStream_t s, int by_lo = 0, int by_hi = 0x7fffffff);
 
-// hand-written FFT convolution (kernels_fftconv.cu)
-bool fft_size_supported(int P);  // P = 256 q, q = 2^a 3^b 5^c (b <= 2, c <= 1), P <= 8192
-cudaError_t fftconv_prepare(int P);
-void launch_twiddles(float2* tw, int P, cudaStream_t s);
-// KA: (P/2 + 1) x (P/2 + 1) floats (pitch P/2 + 1); KH: (P/2 + 1) x P floats.  No-op
-// (early exit) unless geom->kspec.
-void launch_kspec(const GridGeom* geom, int P, ForceArgs fa, const float2* tw, float* KA,
-                  float* KH, cudaStream_t s);
-// row passes over grid rows [row0, row1) (row0 even; rows >= M are skipped on the device)
-void launch_rows_fwd(const GridGeom* geom, const float4* C, int cpitch, int P, int row0,
-                     int row1, const float2* tw, float2* CA, int ca_pitch, cudaStream_t s);
-// column pass over half-spectrum columns [q0, q1) (q0 even), which CA holds as columns
-// 0 .. q1 - q0 - 1 (the whole half spectrum on one GPU: q0 = 0, q1 = P/2 + 1)
-void launch_cols(const GridGeom* geom, float2* CA, int ca_pitch, const float* KH, int P,
-                 const float2* tw, int q0, int q1, cudaStream_t s);
-// rows_inv also re-zeroes the charge rows it covers (consumed by rows_fwd)
-void launch_rows_inv(const GridGeom* geom, const float2* CA, int ca_pitch, int P, int row0,
-                     int row1, const float2* tw, float* Phi, int cpitch, float4* C,
-                     cudaStream_t s);
 // multi-GPU slab mode (kernels_dist.cu): rank r owns grid rows
 // [row0[r], row0[r+1]) of the row passes (multiples of 24: whole CA row tiles of 8 and whole
 // intervals at every k) and half-spectrum columns [q0[r], q0[r+1]) of the column pass (even
@@ -163,6 +144,30 @@ struct SlabPlan {
   int q0[kMaxWorld + 1];
 };
 void slab_plan(int world, int rank, int rows, int P, SlabPlan* pl);
+
+// Peer routing of the slab mode's fused exchanges: the producing kernels store
+// straight into the buffers of the ranks that consume the data — rows_fwd into the column
+// owners' receive buffers xb, cols into the row owners' half spectra CA, rows_inv its
+// potential rows and gather_update the new positions into every rank's copy.  Between
+// processes the pointers are CUDA IPC mappings (NVLink P2P stores); between the virtual ranks
+// of one device they are the other contexts' buffers.  One route per k (the plan's slabs);
+// kept in device memory, nullptr on one GPU.
+struct PeerRoute {
+  int world, rank;
+  int R;         // rows of the xb layout ([ch][R / 8][nq][8])
+  int ca_pitch;  // rows of the full CA layout ([ch][ca_pitch / 8][P/2 + 1][8]), every rank
+  int row0[kMaxWorld + 1];
+  int q0[kMaxWorld + 1];
+  float2* xb[kMaxWorld];
+  float2* ca[kMaxWorld];
+  float* phi[kMaxWorld];
+  float2* xy[2][kMaxWorld];
+};
+__host__ __device__ inline int route_owner(const int* b, int world, int v) {
+  int s = 0;
+  while (s < world - 1 && v >= b[s + 1]) ++s;
+  return s;
+}
 // exchange-1 send / exchange-2 receive layout: [s][ch][rt - rt0(me)][q - q0(s)][8] float2,
 // i.e. segment (s, ch) starts at 3 * nrt * 8 * q0[s] + ch * nrt * nq(s) * 8
 // pack: this rank's slab rows of CA ([ch][ca_pitch / 8][H][8]) -> xa;  unpack: xa -> CA
@@ -171,6 +176,27 @@ void launch_pack_slab(const float2* CA, int ca_pitch, const SlabPlan& pl, float2
 void launch_unpack_slab(const float2* xa, const SlabPlan& pl, float2* CA, int ca_pitch,
                         cudaStream_t s);
 
+// hand-written FFT convolution (kernels_fftconv.cu)
+bool fft_size_supported(int P);  // P = 256 q, q = 2^a 3^b 5^c (b <= 2, c <= 1), P <= 8192
+cudaError_t fftconv_prepare(int P);
+void launch_twiddles(float2* tw, int P, cudaStream_t s);
+// KA: (P/2 + 1) x (P/2 + 1) floats (pitch P/2 + 1); KH: (P/2 + 1) x P floats.  No-op
+// (early exit) unless geom->kspec.
+void launch_kspec(const GridGeom* geom, int P, ForceArgs fa, const float2* tw, float* KA,
+                  float* KH, cudaStream_t s);
+// row passes over grid rows [row0, row1) (row0 even; rows >= M are skipped on the device)
+void launch_rows_fwd(const GridGeom* geom, const float4* C, int cpitch, int P, int row0,
+                     int row1, const float2* tw, float2* CA, int ca_pitch, cudaStream_t s,
+                     const PeerRoute* route = nullptr);
+// column pass over half-spectrum columns [q0, q1) (q0 even), which CA holds as columns
+// 0 .. q1 - q0 - 1 (the whole half spectrum on one GPU: q0 = 0, q1 = P/2 + 1)
+void launch_cols(const GridGeom* geom, float2* CA, int ca_pitch, const float* KH, int P,
+                 const float2* tw, int q0, int q1, cudaStream_t s,
+                 const PeerRoute* route = nullptr);
+// rows_inv also re-zeroes the charge rows it covers (consumed by rows_fwd)
+void launch_rows_inv(const GridGeom* geom, const float2* CA, int ca_pitch, int P, int row0,
+                     int row1, const float2* tw, float* Phi, int cpitch, float4* C,
+                     cudaStream_t s, const PeerRoute* route = nullptr);
 // internal node renumbering (kernels_reorder.cu)
 size_t reorder_scratch_bytes(int64_t n);
 void launch_iota(int* perm, int* inv, int64_t n, cudaStream_t s);
@@ -202,7 +228,7 @@ void launch_gather_update(const float2* xy, float2* xy_next, int64_t lo, int64_t
                           const int64_t* row_ptr, const int32_t* col, ForceArgs fa,
                           FocusArgs fo, float eta, int iter, int update, float2* rep_out,
                           float2* att_out, unsigned long long* diverge, BoxKeys* next_part,
-                          cudaStream_t s);
+                          cudaStream_t s, const PeerRoute* route = nullptr, int next_buf = 0);
 
 // heavy rows (kernels_heavy.cu): build the chunk index of the current CSR (scratch: 8 (n+1)
 // + sums bytes, heavy_scratch_bytes), then the chunk sums for the rows [lo, hi)

@@ -5,7 +5,7 @@ set -x
 mkdir -p gpurun_out
 python tools/kprof.py C4 20 > gpurun_out/kprof.txt 2>&1
 for k in 1 2 3; do
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:"cols_kernel|rows_fwd|rows_inv|gather_update|spread_kernel|kspec" -s 7 -c 7 -o /tmp/full_k$k -f python tools/fft_iter.py $k 8 > gpurun_out/ncu_full_k$k.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"cols_kernel|rows_fwd|rows_inv|gather_update|spread_kernel|kspec|setup_kernel" -s 7 -c 7 -o /tmp/full_k$k -f python tools/fft_iter.py $k 8 > gpurun_out/ncu_full_k$k.log 2>&1
 python tools/ncu_summary.py /tmp/full_k$k.ncu-rep > gpurun_out/ncu_full_k${k}_summary.txt 2>&1
 ncu -i /tmp/full_k$k.ncu-rep --page raw --csv > gpurun_out/ncu_full_k${k}_raw.csv 2>/dev/null
 done

@@ -22,17 +22,22 @@ def kind_of(name):
 
 def main():
     out, files = sys.argv[1], sys.argv[2:]
-    res = {"source": "ncu --set full --clock-control none (tools/gpu_profile_fft.sh, C4, fixed k)",
+    res = {"source": "ncu --set full --clock-control none (tools/gpu_profile_r2.sh, C4, fixed k)",
            "unit": "bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum)", "kernels": {}}
     for k, path in enumerate(files, start=1):
         rows = list(csv.reader(open(path)))
         h, units, data = rows[0], rows[1], rows[2:]
         iname, ird, iwr = h.index("Kernel Name"), h.index("dram__bytes_read.sum"), h.index("dram__bytes_write.sum")
         for r in data:
+            if len(r) <= max(ird, iwr) or r[iname] == "Kernel Name":
+                continue  # header / unit rows of concatenated exports
             kind = kind_of(r[iname])
             if kind is None:
                 continue
-            b = float(r[ird]) * SCALE[units[ird]] + float(r[iwr]) * SCALE[units[iwr]]
+            try:
+                b = float(r[ird]) * SCALE[units[ird]] + float(r[iwr]) * SCALE[units[iwr]]
+            except ValueError:
+                continue
             res["kernels"].setdefault(kind, {})[str(k)] = round(b)
     # the bench times kspec_rows + kspec_cols under one scope
     ks = res["kernels"]
