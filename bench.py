@@ -105,7 +105,7 @@ def load_peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)", {}
 
 
-TRAFFIC_JSON = os.path.join(ROOT, "profiles", "r1_traffic.json")
+TRAFFIC_JSON = os.path.join(ROOT, "profiles", "r2_traffic.json")
 
 
 def ncu_traffic(kind: str, ks) -> float | None:
@@ -304,7 +304,7 @@ def run_fft(args, rank, world, local):
             "work_per_launch": round(bytes_total / dom_n),
             "work_unit": "algorithmic bytes (M-aware: only the M non-zero rows / kept outputs, DESIGN.md §6)"}
     if traffic is not None:
-        roof["traffic_unit"] = "DRAM bytes per launch (ncu, profiles/r1_traffic.json)"
+        roof["traffic_unit"] = "DRAM bytes per launch (ncu, profiles/r2_traffic.json)"
     roof_flop = None
     if dom in FFT_KINDS:
         achieved = total / (dom_ms / 1e3) / 1e12
