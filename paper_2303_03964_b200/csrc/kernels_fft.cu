@@ -230,8 +230,11 @@ struct Cell {
 // the same operations as the oracle's interval_coords, so the integer decision matches.
 __device__ __forceinline__ Cell cell_of(float2 p, const GridGeom& g) {
   Cell c;
-  const float tx = __fdiv_rn(__fsub_rn(p.x, g.lo_x), g.w);
-  const float ty = __fdiv_rn(__fsub_rn(p.y, g.lo_y), g.w);
+  float tx = __fsub_rn(p.x, g.lo_x), ty = __fsub_rn(p.y, g.lo_y);
+  if (g.w != 1.0f) {  // unit-width intervals (R5'): the division by 1 is exact, skip it
+    tx = __fdiv_rn(tx, g.w);
+    ty = __fdiv_rn(ty, g.w);
+  }
   c.bx = max(0, min((int)floorf(tx), g.n_int - 1));
   c.by = max(0, min((int)floorf(ty), g.n_int - 1));
   c.ux = __fsub_rn(tx, (float)c.bx);
