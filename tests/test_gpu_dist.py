@@ -3,6 +3,8 @@ world driven in lockstep by tfdp_group_step / tfdp_group_forces run the same ker
 buffer layouts and message boundaries as the NCCL path, with device copies in place of the
 NCCL calls.  Parity: against the one-rank context and the oracle; the exact path and the
 renumbering are bitwise across rank counts (R15)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -198,3 +200,35 @@ def test_slab_heavy_rows_renumbered(stream):
         assert O.rel_l2(R, O.repulsion_ibfft(Xg, 1)) <= 1e-3
     finally:
         _close(G)
+
+
+@pytest.mark.parametrize("p2p", ["1", "0"])
+def test_slab_group_grows_through_replans(p2p, stream, monkeypatch):
+    """A group whose layout expands far beyond the first plan (strong repulsion, rho = 50):
+    every rank re-plans at the same step (identical boxes), buffers are re-allocated and the
+    peer routes refreshed; the forces at the final layout match the oracle."""
+    import subprocess
+    import sys
+    code = r"""
+import numpy as np, torch, oracle as O, paper_2303_03964_b200 as P
+from synth import random_layout, random_graph
+n = 2000
+X = random_layout(n, 41, 3.0); u, v = random_graph(n, 2 * n, 42); rp, col = O.csr_build(n, u, v)
+s = torch.cuda.Stream().cuda_stream
+prm = P.Params(solver="ibfft", k=1, rho=50.0, iterations=300)
+G = [P.Layout(n, rp, col, X, prm, dist=P.Dist(r, 2, 0, None), stream=s) for r in range(2)]
+P0 = G[0].fft_plan(1)[0]
+P.group_step(G, 96)
+Xg = G[0].layout()
+assert np.array_equal(Xg, G[1].layout())
+R = np.concatenate([o[0] for o in P.group_forces(G)])
+assert G[0].fft_plan(1)[0] > P0, (P0, G[0].fft_plan(1))
+e = O.rel_l2(R, O.repulsion_ibfft(Xg.astype(np.float64), 1, rho=50.0))
+print("rel", e); assert e <= 1e-3
+print("grow ok")
+"""
+    env = dict(os.environ, TFDP_P2P=p2p)
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    print(r.stdout, r.stderr[-2000:])
+    assert r.returncode == 0 and "grow ok" in r.stdout
