@@ -41,14 +41,15 @@ enum Kind {
   K_GATHER_UPDATE,
   K_COMM,
   K_HEAVY,
+  K_ATTR,
   K_COUNT
 };
 const char* kKindNames[K_COUNT] = {"exact_partial", "exact_finish", "bbox",     "setup",
                                    "reorder",       "spread",       "kspec_rows", "rows_fwd",
                                    "cols",          "rows_inv",     "gather_update", "nccl",
-                                   "heavy_rows"};
+                                   "heavy_rows", "attraction"};
 const bool kOwnKernel[K_COUNT] = {true, true, true, true, true, true,
-                                  true, true, true, true, true, false, true};
+                                  true, true, true, true, true, false, true, true};
 
 }  // namespace
 
@@ -62,6 +63,11 @@ struct tfdp_ctx {
   // with spread + rows_fwd; fork/join with events, so the ctx stream order is preserved
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_join2 = nullptr;  // after the side stream's heavy rows + attraction
+  // attraction on the side stream (TFDP_ATTR_SIDE=0: walked inside gather_update)
+  bool attr_side = true;
+  bool attr_pre = false;  // this evaluation's attraction is in attr
+  float2* attr = nullptr;
   bool kspec_overlap = true;  // env TFDP_KSPEC_OVERLAP=0 runs it in line (tuning / A-B)
   float2* xy[2] = {nullptr, nullptr};
   int cur = 0;
@@ -763,8 +769,17 @@ void fft_prologue(tfdp_ctx* c, int k, bool* overlap) {
     Scope sc(c, K_KSPEC, ks, 2);  // kspec_rows + kspec_cols
     tfdp::launch_kspec(c->geom, P, c->fa, c->tw[k], c->ka, c->kh[k], ks);
   }
-  heavy_rows(c, ks);  // also off the critical path; joined before cols (< gather_update)
-  if (*overlap) cudaEventRecord(c->ev_join, c->side);
+  if (*overlap) cudaEventRecord(c->ev_join, c->side);  // cols joins here
+  // the attraction depends only on the positions: heavy-row chunks and the per-node sums also
+  // run beside spread + FFT passes; gather_update joins after them (ev_join2)
+  heavy_rows(c, ks);
+  c->attr_pre = c->attr_side && !c->focus_on && c->attr;
+  if (c->attr_pre) {
+    Scope sc(c, K_ATTR, ks);
+    tfdp::launch_attraction(c->xy[c->cur], c->lo, c->hi - c->lo, c->row_ptr, c->col, c->fa,
+                            c->attr, ks);
+  }
+  if (*overlap) cudaEventRecord(c->ev_join2, c->side);
 }
 
 tfdp::FocusArgs focus_prologue(tfdp_ctx* c) {
@@ -844,13 +859,14 @@ tfdp_status evaluate_one(tfdp_ctx* c, int update, float eta, int k) {
       tfdp::launch_rows_inv(c->geom, c->ca, c->ca_pitch, P, 0, mcap, tw, c->phi, pitch_k(c, k),
                             grid4, c->stream);
     }
+    if (overlap) CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_join2, 0));
     {
       Scope sc(c, K_GATHER_UPDATE);
       BoxKeys* nk = (update && c->world == 1) ? c->box_part : nullptr;
       if (nk) c->n_part = tfdp::kBoxSlots;
       tfdp::launch_gather_update(xy, xyn, c->lo, n_local, c->geom, k, c->phi, c->row_ptr, c->col,
                                  c->fa, fo, eta, c->t, update, c->rep, c->att, c->diverge, nk,
-                                 c->stream);
+                                 c->stream, nullptr, 0, c->attr_pre ? c->attr : nullptr);
     }
     c->box_valid = update && c->world == 1;
   }
@@ -1021,11 +1037,13 @@ tfdp_status evaluate_slab_p2p(const Group& G, int update, float eta, int k) {
   for (int i = 0; i < G.p; ++i) {  // phase D: own nodes -> every rank's next positions
     tfdp_ctx* c = G[i];
     const tfdp::FocusArgs fo = focus_prologue(c);
+    if (overlap[i]) CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_join2, 0));
     Scope sc(c, K_GATHER_UPDATE);
     tfdp::launch_gather_update(c->xy[c->cur], c->xy[c->cur ^ 1], c->lo, c->hi - c->lo, c->geom, k,
                                c->phi, c->row_ptr, c->col, c->fa, fo, eta, c->t, update, c->rep,
                                c->att, c->diverge, nullptr, c->stream,
-                               update ? c->d_route + k : nullptr, c->cur ^ 1);
+                               update ? c->d_route + k : nullptr, c->cur ^ 1,
+                               c->attr_pre ? c->attr : nullptr);
     c->box_valid = false;
     CUDA_TRY(c, cudaGetLastError());
   }
@@ -1084,10 +1102,12 @@ tfdp_status evaluate_slab(const Group& G, int update, float eta, int k) {
   for (int i = 0; i < G.p; ++i) {  // phase D: gather + attraction + update of the own nodes
     tfdp_ctx* c = G[i];
     const tfdp::FocusArgs fo = focus_prologue(c);
+    if (overlap[i]) CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_join2, 0));
     Scope sc(c, K_GATHER_UPDATE);
     tfdp::launch_gather_update(c->xy[c->cur], c->xy[c->cur ^ 1], c->lo, c->hi - c->lo, c->geom, k,
                                c->phi, c->row_ptr, c->col, c->fa, fo, eta, c->t, update, c->rep,
-                               c->att, c->diverge, nullptr, c->stream);
+                               c->att, c->diverge, nullptr, c->stream, nullptr, 0,
+                               c->attr_pre ? c->attr : nullptr);
     c->box_valid = false;
     CUDA_TRY(c, cudaGetLastError());
   }
@@ -1493,7 +1513,8 @@ tfdp_status tfdp_init(tfdp_ctx** out, int64_t n, const int64_t* row_ptr, const i
   }
   if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess)
+      cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_join2, cudaEventDisableTiming) != cudaSuccess)
     return bail(fail(c, TFDP_ERR_CUDA, "side stream / events"));
   if (const char* e = getenv("TFDP_KSPEC_OVERLAP")) c->kspec_overlap = atoi(e) != 0;
   const bool xy_dev = is_device_ptr(xy0);
@@ -1515,6 +1536,9 @@ tfdp_status tfdp_init(tfdp_ctx** out, int64_t n, const int64_t* row_ptr, const i
   ALLOC(c->row_ptr, (n + 1) * sizeof(int64_t));
   ALLOC(c->col, std::max<int64_t>(nnz, 1) * sizeof(int32_t));
   ALLOC(c->rep, std::max<int64_t>(n_local, 1) * sizeof(float2));
+  if (const char* e = getenv("TFDP_ATTR_SIDE")) c->attr_side = e[0] != '0';
+  if (p.solver == TFDP_IBFFT && c->attr_side)
+    ALLOC(c->attr, std::max<int64_t>(n_local, 1) * sizeof(float2));
   ALLOC(c->att, std::max<int64_t>(n_local, 1) * sizeof(float2));
   ALLOC(c->diverge, sizeof(unsigned long long));
   ALLOC(c->capped, sizeof(int));
@@ -2038,6 +2062,7 @@ void tfdp_destroy(tfdp_ctx* c) {
   cudaFree(c->part);
   cudaFree(c->rep);
   cudaFree(c->att);
+  cudaFree(c->attr);
   cudaFree(c->diverge);
   cudaFree(c->capped);
   cudaFree(c->keys);
@@ -2080,6 +2105,7 @@ void tfdp_destroy(tfdp_ctx* c) {
   }
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->ev_join2) cudaEventDestroy(c->ev_join2);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }

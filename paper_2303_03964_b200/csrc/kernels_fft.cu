@@ -502,7 +502,8 @@ gather_update_kernel(const float2* __restrict__ xy, float2* __restrict__ xy_next
                      const int32_t* __restrict__ col, ForceArgs fa, FocusArgs fo, float eta,
                      int iter, int update, float2* __restrict__ rep_out,
                      float2* __restrict__ att_out, unsigned long long* diverge,
-                     BoxKeys* next_part, const PeerRoute* __restrict__ rt, int next_buf) {
+                     BoxKeys* next_part, const PeerRoute* __restrict__ rt, int next_buf,
+                     const float2* __restrict__ A_pre) {
   pdl_wait();
   pdl_trigger();
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -540,10 +541,13 @@ gather_update_kernel(const float2* __restrict__ xy, float2* __restrict__ xy_next
       Rx = Rm.x;
       Ry = Rm.y;
       as = attraction_sum_masked(xy, p, row_ptr, col, i, fa.beta, fo.label, fo.la);
-    } else {
+    } else if (!A_pre) {
       as = attraction_sum_hv(xy, p, row_ptr, col, i, fa);
     }
-    const float ax = -fa.alpha * as.x, ay = -fa.alpha * as.y;
+    // A_pre: the attraction, computed from the same positions by attraction_kernel on the
+    // side stream while the FFT passes ran (it does not depend on the grid)
+    const float ax = A_pre && !fo.label ? A_pre[t].x : -fa.alpha * as.x;
+    const float ay = A_pre && !fo.label ? A_pre[t].y : -fa.alpha * as.y;
     if (update) {
       const float nx = fmaf(eta, Rx + ax, p.x);
       const float ny = fmaf(eta, Ry + ay, p.y);
@@ -565,18 +569,40 @@ gather_update_kernel(const float2* __restrict__ xy, float2* __restrict__ xy_next
   if (update && next_part) block_box_commit(kx0, ky0, kx1, ky1, next_part);
 }
 
+// Attraction of the shard's nodes, A_t = -alpha sum_j (1 + beta/s)(x_i - x_j) (P:286-288,
+// P:301-303), written for gather_update: it depends only on the positions, so it runs on the
+// side stream concurrently with spread and the FFT passes instead of on the critical path.
+__global__ void __launch_bounds__(kNodeThreads)
+attraction_kernel(const float2* __restrict__ xy, int64_t lo, int64_t n_local,
+                  const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+                  ForceArgs fa, float2* __restrict__ A) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_local) return;
+  const int64_t i = lo + t;
+  const float2 s = attraction_sum_hv(xy, xy[i], row_ptr, col, i, fa);
+  A[t] = make_float2(-fa.alpha * s.x, -fa.alpha * s.y);
+}
+
+void launch_attraction(const float2* xy, int64_t lo, int64_t n_local, const int64_t* row_ptr,
+                       const int32_t* col, ForceArgs fa, float2* A, cudaStream_t s) {
+  if (n_local <= 0) return;
+  attraction_kernel<<<(unsigned)((n_local + kNodeThreads - 1) / kNodeThreads), kNodeThreads, 0, s>>>(
+      xy, lo, n_local, row_ptr, col, fa, A);
+}
+
 void launch_gather_update(const float2* xy, float2* xy_next, int64_t lo, int64_t n_local,
                           const GridGeom* geom, int k, const float* phi,
                           const int64_t* row_ptr, const int32_t* col, ForceArgs fa,
                           FocusArgs fo, float eta, int iter, int update, float2* rep_out,
                           float2* att_out, unsigned long long* diverge, BoxKeys* next_part,
-                          cudaStream_t s, const PeerRoute* route, int next_buf) {
+                          cudaStream_t s, const PeerRoute* route, int next_buf,
+                          const float2* A_pre) {
   if (n_local <= 0) return;
   const unsigned blocks = (unsigned)((n_local + kNodeThreads - 1) / kNodeThreads);
 #define TFDP_GU(KK)                                                                         \
   launch_chained(gather_update_kernel<KK>, blocks, kNodeThreads, 0, s, xy, xy_next, lo,      \
                  n_local, geom, phi, row_ptr, col, fa, fo, eta, iter, update, rep_out, att_out, \
-                 diverge, next_part, route, next_buf)
+                 diverge, next_part, route, next_buf, A_pre)
   if (k == 1) TFDP_GU(1);
   else if (k == 2) TFDP_GU(2);
   else TFDP_GU(3);
