@@ -1724,26 +1724,43 @@ tfdp_status tfdp_set_layout(tfdp_ctx* c, const float* xy) {
   if (!c || !xy) return fail(c, TFDP_ERR_ARG, "NULL argument");
   cudaSetDevice(c->device);
   const bool d = is_device_ptr(xy);
-  if (!d) {  // argument check on the host buffer, all cores: first non-finite node
+  if (!d) {
+    // the H2D copy goes to a staging buffer first, so the argument check of the host buffer
+    // (all cores: first non-finite node) runs while the DMA is in flight; a failed
+    // check leaves the layout untouched
+    if (!c->iobuf) CUDA_TRY(c, cudaMalloc(&c->iobuf, c->n * sizeof(float2)));
+    CUDA_TRY(c, cudaMemcpyAsync(c->iobuf, xy, c->n * sizeof(float2), cudaMemcpyHostToDevice,
+                                c->stream));
     const int64_t m = 2 * c->n;
     int64_t first = m;
 #pragma omp parallel for schedule(static) reduction(min : first)
     for (int64_t i = 0; i < m; ++i)
       if (!std::isfinite(xy[i]) && i < first) first = i;
-    if (first < m)
+    if (first < m) {
+      cudaStreamSynchronize(c->stream);  // the caller may free xy on return
       return fail(c, TFDP_ERR_ARG, "layout non-finite at node %lld", (long long)(first / 2));
-  }
-  float2* dst = c->reorder ? c->iobuf : c->xy[c->cur];
-  CUDA_TRY(c, cudaMemcpyAsync(dst, xy, c->n * sizeof(float2),
-                              d ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->stream));
-  if (c->reorder) {  // caller order -> internal order
-    tfdp::launch_permute(c->iobuf, c->perm, c->n, c->xy[c->cur], c->stream);
-    c->launches++;
+    }
+    if (c->reorder) {  // caller order -> internal order
+      tfdp::launch_permute(c->iobuf, c->perm, c->n, c->xy[c->cur], c->stream);
+      c->launches++;
+    } else {
+      CUDA_TRY(c, cudaMemcpyAsync(c->xy[c->cur], c->iobuf, c->n * sizeof(float2),
+                                  cudaMemcpyDeviceToDevice, c->stream));
+    }
+  } else {
+    float2* dst = c->reorder ? c->iobuf : c->xy[c->cur];
+    CUDA_TRY(c, cudaMemcpyAsync(dst, xy, c->n * sizeof(float2), cudaMemcpyDeviceToDevice,
+                                c->stream));
+    if (c->reorder) {  // caller order -> internal order
+      tfdp::launch_permute(c->iobuf, c->perm, c->n, c->xy[c->cur], c->stream);
+      c->launches++;
+    }
   }
   c->box_valid = false;
   // a new layout may need a larger grid: re-plan now (one bbox + a host sync) rather than
   // run up to 32 iterations below the N_int rule (R5) before the in-step check
   if (c->p.solver == TFDP_IBFFT && c->p.n_int_fixed == 0) return replan_from_device(c);
+  if (!d) CUDA_TRY(c, cudaStreamSynchronize(c->stream));  // the host buffer is free on return
   return TFDP_OK;
 }
 
