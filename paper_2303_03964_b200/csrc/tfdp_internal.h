@@ -81,7 +81,9 @@ bool pdl_enabled();
 // Per-iteration switch (host thread): the ibFFT chain uses PDL only up to P = 2048 — at
 // P = 4096 / 6144 the overlapped launches were slower (C4 k = 2: 405 vs 385 us, k = 3: 1091
 // vs 973 us per iteration), at P = 2048 faster (122.6 vs 124.5 us).
-constexpr int kPdlMaxFft = 2048;
+// Round 2 re-measured (bench per-k): P = 4096 324.4 -> 314.2 us with PDL, P = 6144 751.9 ->
+// 773.0 us: the threshold is 4096.
+constexpr int kPdlMaxFft = 4096;
 void set_pdl_active(bool on);
 template <typename... KArgs, typename... Args>
 inline void launch_chained(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
