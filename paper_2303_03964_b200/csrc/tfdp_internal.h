@@ -78,9 +78,9 @@ struct FocusArgs {
 // Every chain kernel calls pdl_wait() before touching any buffer another kernel writes, so
 // the ordering is the plain stream order.  TFDP_PDL=0 disables the attribute (A/B runs).
 bool pdl_enabled();
-// Per-iteration switch (host thread): the ibFFT chain uses PDL only up to P = 2048 — at
-// P = 4096 / 6144 the overlapped launches were slower (C4 k = 2: 405 vs 385 us, k = 3: 1091
-// vs 973 us per iteration), at P = 2048 faster (122.6 vs 124.5 us).
+// Per-iteration switch (host thread): the ibFFT chain uses PDL only up to P = kPdlMaxFft.
+// Round 1 (then-current kernels): P = 4096 / 6144 slower with PDL (C4 k = 2: 405 vs 385 us,
+// k = 3: 1091 vs 973 us per iteration), P = 2048 faster (122.6 vs 124.5 us).
 // Round 2 re-measured (bench per-k): P = 4096 324.4 -> 314.2 us with PDL, P = 6144 751.9 ->
 // 773.0 us: the threshold is 4096.
 constexpr int kPdlMaxFft = 4096;
