@@ -88,7 +88,28 @@ def build(verbose: bool = False, force: bool = False, defines=(), out: str = Non
     if r.returncode != 0:
         raise RuntimeError("nvcc link failed:\n" + " ".join(cmd))
     os.replace(out + ".tmp", out)
+    if out == LIB:
+        build_examples(verbose)
     return out
+
+
+EXAMPLES = os.path.join(ROOT, "examples")
+
+
+def build_examples(verbose: bool = False) -> list:
+    """Plain C clients of the C ABI (examples/*.c), linked against the in-tree libtfdp.so."""
+    outs = []
+    for src in sorted(glob.glob(os.path.join(EXAMPLES, "*.c"))):
+        exe = os.path.splitext(src)[0]
+        cmd = ["gcc", "-O2", "-std=c11", "-I", os.path.join(ROOT, "include"), src, "-L", HERE,
+               "-ltfdp", "-Wl,-rpath,$ORIGIN/../paper_2303_03964_b200", "-lm", "-o", exe]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if verbose or r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+        if r.returncode != 0:
+            raise RuntimeError("gcc failed:\n" + " ".join(cmd))
+        outs.append(exe)
+    return outs
 
 
 if __name__ == "__main__":

@@ -2,6 +2,7 @@
 symbol include/tfdp.h declares, the host CSR builder and shard rule are bit-exact with
 the oracle, argument errors are reported (no compute calls)."""
 import ctypes as C
+import os
 
 import numpy as np
 import pytest
@@ -117,3 +118,10 @@ def test_slab_plan(world, rows, Pf):
     assert d_rows.max() - d_rows.min() <= 24 and d_cols.max() - d_cols.min() <= 3
     with pytest.raises(P.TfdpError):
         P.slab_plan(rows, Pf, 0)
+
+
+def test_c_example_builds_and_links():
+    """examples/*.c compile against include/tfdp.h alone and link libtfdp.so (no GPU needed)."""
+    from paper_2303_03964_b200 import build as B
+    exes = B.build_examples()
+    assert exes and all(os.path.exists(e) for e in exes)
