@@ -412,3 +412,24 @@ def test_large_span_auto_plan():
         assert not L.warnings & 4
     assert geo["P"] == 9216 and geo["n_int"] == O.box_rule(X).n_int
     check_ib(R, oracle_ib(X, 2), "span 2100 k=2")
+
+
+def test_layout_level_band_C2_gpu():
+    """P:655 on the device: full C2 layouts (T = 300, constant step R2') from the exact path
+    and from the ibFFT path with the dynamic 90/5/5 schedule agree on NP1 within +-4 %
+    relative (the oracle's own pin: tests/test_oracle_ibfft.py::test_layout_level_band_C2),
+    and each device NP1 is within 0.01 of the oracle's run of the same path (north star)."""
+    w, rp, col = _case("C2")
+    np1 = {}
+    for solver in ("exact", "ibfft"):
+        prm = P.Params(solver=solver, k=0, cooling="constant", iterations=300)
+        with P.Layout(w.n, rp, col, w.xy, prm) as L:
+            L.step(300)
+            np1[solver] = L.np1()
+    assert abs(np1["ibfft"] - np1["exact"]) / np1["exact"] <= 0.04, np1
+    X0 = w.xy.astype(np.float64)
+    for solver in ("exact", "ibfft"):
+        Xo = O.run(X0, rp, col, O.Params(), T=300, solver=solver, k=0, cooling="constant")
+        no = O.np1(Xo, rp, col)
+        print(f"[np1] C2 {solver}: gpu {np1[solver]:.4f} oracle {no:.4f}")
+        assert abs(np1[solver] - no) <= 0.01, (solver, np1[solver], no)
