@@ -939,7 +939,13 @@ tfdp_status setup_routes(const Group& G) {
   constexpr int kB = 5;  // buffers per rank: xb, ca, phi, xy0, xy1
   std::vector<cudaIpcMemHandle_t> mine(kB);
   void* bufs[kB] = {c->xb, c->ca, c->phi, c->xy[0], c->xy[1]};
-  for (int b = 0; b < kB; ++b) CUDA_TRY(c, cudaIpcGetMemHandle(&mine[b], bufs[b]));
+  int got = 1;  // a failure here must not leave the other ranks in the handle broadcast alone
+  for (int b = 0; b < kB; ++b)
+    if (cudaIpcGetMemHandle(&mine[b], bufs[b]) != cudaSuccess) {
+      cudaGetLastError();
+      memset(&mine[b], 0, sizeof(cudaIpcMemHandle_t));
+      got = 0;
+    }
   const size_t hs = sizeof(cudaIpcMemHandle_t) * kB;
   unsigned char* dh = nullptr;
   CUDA_TRY(c, cudaMalloc(&dh, hs * p));
@@ -960,10 +966,12 @@ tfdp_status setup_routes(const Group& G) {
         ptr[b][r] = bufs[b];
         continue;
       }
-      cudaIpcMemHandle_t hh;
+      cudaIpcMemHandle_t hh, zero;
       memcpy(&hh, all.data() + hs * r + sizeof(cudaIpcMemHandle_t) * b, sizeof hh);
+      memset(&zero, 0, sizeof zero);
       void* q = nullptr;
-      if (cudaIpcOpenMemHandle(&q, hh, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess) {
+      if (memcmp(&hh, &zero, sizeof hh) != 0 &&
+          cudaIpcOpenMemHandle(&q, hh, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess) {
         c->ipc_open.push_back(q);
       } else {
         cudaGetLastError();
@@ -972,7 +980,7 @@ tfdp_status setup_routes(const Group& G) {
       ptr[b][r] = q;
     }
   // every rank must be able to map every peer, else all fall back to the copy exchanges
-  int ok = 1;
+  int ok = got;
   for (int b = 0; b < kB; ++b)
     for (int r = 0; r < p; ++r) ok &= ptr[b][r] != nullptr;
   CUDA_TRY(c, cudaMemcpyAsync(c->bar, &ok, sizeof(int), cudaMemcpyHostToDevice, c->stream));
