@@ -9,7 +9,7 @@ import sys
 
 KINDS = [("kspec_rows_kernel", "kspec_rows"), ("kspec_cols_kernel", "kspec_cols"),
          ("spread_kernel", "spread"), ("rows_fwd_kernel", "rows_fwd"), ("cols_kernel", "cols"),
-         ("rows_inv_kernel", "rows_inv"), ("gather_update_kernel", "gather_update")]
+         ("rows_inv_kernel", "rows_inv"), ("gather_update_kernel", "gather_update"), ("attraction_kernel", "attraction")]
 SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
 
