@@ -1828,8 +1828,8 @@ tfdp_status tfdp_np1(tfdp_ctx* c, double* np1, int32_t* hits) {
     CUDA_TRY(c, cudaMalloc(&c->np_keys, sizeof(BoxKeys)));
     CUDA_TRY(c, cudaMalloc(&c->np_sum, sizeof(double)));
   }
-  if (hits && c->reorder && c->world > 1)
-    return fail(c, TFDP_ERR_UNSUPPORTED, "per-node hits of a renumbered multi-rank context");
+  if (hits && c->reorder && c->world > 1 && !c->comm)
+    return fail(c, TFDP_ERR_UNSUPPORTED, "per-node hits of a renumbered virtual rank");
   const float2* xy = c->xy[c->cur];
   tfdp::launch_reset_slots(c->np_slots, c->stream);
   const int np = tfdp::launch_bbox(xy, c->n, c->np_slots, c->stream);
@@ -1844,7 +1844,25 @@ tfdp_status tfdp_np1(tfdp_ctx* c, double* np1, int32_t* hits) {
   CUDA_TRY(c, cudaGetLastError());
   if (hits) {
     const int* src = c->np_hits;
-    if (c->reorder) {  // internal slot -> caller order
+    if (c->reorder && c->world > 1) {
+      // the shard's internal slots hold caller nodes spread over all ranks: gather every
+      // rank's hits (internal order), un-permute, cut the caller range [lo, hi)
+      int* full = reinterpret_cast<int*>(c->iobuf);  // n float2 >= n ints
+      CUDA_TRY(c, cudaMemcpyAsync(full + c->lo, c->np_hits, n_local * sizeof(int),
+                                  cudaMemcpyDeviceToDevice, c->stream));
+      NCCL_TRY(c, c->nccl->GroupStart());
+      for (int r = 0; r < c->world; ++r) {
+        int64_t lo, hi;
+        tfdp_shard_range(c->n, c->world, r, &lo, &hi);
+        if (hi > lo)
+          NCCL_TRY(c, c->nccl->Broadcast(full + lo, full + lo, (size_t)(hi - lo), ncclInt32, r,
+                                         c->comm, c->stream));
+      }
+      NCCL_TRY(c, c->nccl->GroupEnd());
+      tfdp::launch_unpermute_int(full, c->perm, c->n, c->np_hits2, c->stream);
+      c->launches++;
+      src = c->np_hits2 + c->lo;
+    } else if (c->reorder) {  // internal slot -> caller order
       tfdp::launch_unpermute_int(c->np_hits, c->perm, c->n, c->np_hits2, c->stream);
       c->launches++;
       src = c->np_hits2;
