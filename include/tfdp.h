@@ -286,6 +286,10 @@ tfdp_status tfdp_fft_plan(const tfdp_ctx* ctx, int32_t k, int32_t* fft_size, int
  * Syncs the stream. */
 tfdp_status tfdp_profile(tfdp_ctx* ctx, int32_t enable);
 tfdp_status tfdp_profile_mask(tfdp_ctx* ctx, uint32_t kinds);
+/* Sets the timed kinds WITHOUT resetting the accumulated times or syncing (a host-side
+ * switch): a timed region can instrument a sample of its launches — e.g. every fourth step —
+ * and read the sample's total with tfdp_profile_read at the end. */
+tfdp_status tfdp_profile_select(tfdp_ctx* ctx, uint32_t kinds);
 int32_t tfdp_profile_read(tfdp_ctx* ctx, const char** names, double* ms, int64_t* launches,
                           int32_t cap);
 

@@ -67,6 +67,7 @@ _SIGS = {
     "tfdp_fft_plan": (C.c_int, [_P, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     "tfdp_profile": (C.c_int, [_P, C.c_int32]),
     "tfdp_profile_mask": (C.c_int, [_P, C.c_uint32]),
+    "tfdp_profile_select": (C.c_int, [_P, C.c_uint32]),
     "tfdp_profile_read": (C.c_int32, [_P, C.POINTER(C.c_char_p), C.POINTER(C.c_double),
                                       C.POINTER(C.c_int64), C.c_int32]),
     "tfdp_launch_count": (C.c_int64, [_P]),

@@ -2054,6 +2054,12 @@ tfdp_status tfdp_profile_mask(tfdp_ctx* c, uint32_t kinds) {
   return TFDP_OK;
 }
 
+tfdp_status tfdp_profile_select(tfdp_ctx* c, uint32_t kinds) {
+  if (!c) return TFDP_ERR_ARG;
+  c->prof_mask = kinds;
+  return TFDP_OK;
+}
+
 int32_t tfdp_profile_read(tfdp_ctx* c, const char** names, double* ms, int64_t* launches,
                           int32_t cap) {
   if (!c) return -1;

@@ -297,6 +297,17 @@ class Layout:
             mask |= 1 << order.index(name)
         check(lib().tfdp_profile_mask(self._ctx, mask), self._ctx)
 
+    def kinds_mask(self, kinds) -> int:
+        order = self.kernel_kinds()
+        mask = 0
+        for name in kinds:
+            mask |= 1 << order.index(name)
+        return mask
+
+    def profile_select(self, mask: int):
+        """tfdp_profile_select: switch the timed kinds without reset or sync."""
+        check(lib().tfdp_profile_select(self._ctx, int(mask)), self._ctx)
+
     def profile_read(self) -> dict:
         cap = 32
         names = (C.c_char_p * cap)()
