@@ -584,7 +584,7 @@ tfdp_status phase_barrier(const Group& G);
 tfdp_status exchange_positions(const Group& G, int buf) {
   tfdp_ctx* c = G[0];
   if (c->world == 1) return TFDP_OK;
-  if (c->slab && c->p2p && c->p.solver == TFDP_IBFFT)  // gather_update stored into every rank
+  if (c->p2p && (c->slab || c->p.solver == TFDP_EXACT))  // the update stored into every rank
     return phase_barrier(G);
   if (G.virt()) {
     for (int r = 0; r < G.p; ++r)
@@ -812,7 +812,8 @@ tfdp_status evaluate_one(tfdp_ctx* c, int update, float eta, int k) {
       Scope sc(c, K_EXACT_FINISH);
       tfdp::launch_exact_finish(xy, xyn, c->lo, n_local, c->n_chunks, c->part, c->row_ptr,
                                 c->col, c->fa, fo, eta, c->t, update, c->rep, c->att, c->diverge,
-                                c->stream);
+                                c->stream, update && c->p2p && c->world > 1 ? c->d_route : nullptr,
+                                c->cur ^ 1);
     }
   } else {
     const bool allreduce = c->world > 1 && c->p.dist_mode == TFDP_DIST_GRID_ALLREDUCE;
@@ -888,15 +889,17 @@ tfdp_status phase_barrier(const Group& G) {
 
 void fill_route(tfdp_ctx* c, int k, tfdp::PeerRoute* r, void* const* xb, void* const* ca,
                 void* const* phi, void* const* xy0, void* const* xy1) {
-  const tfdp::SlabPlan& pl = c->plan[k];
   memset(r, 0, sizeof(*r));
   r->world = c->world;
   r->rank = c->rank;
-  r->R = pl.R;
-  r->ca_pitch = c->ca_pitch;
-  for (int j = 0; j <= c->world; ++j) {
-    r->row0[j] = pl.row0[j];
-    r->q0[j] = pl.q0[j];
+  if (k > 0) {  // (route 0: positions only — the exact path)
+    const tfdp::SlabPlan& pl = c->plan[k];
+    r->R = pl.R;
+    r->ca_pitch = c->ca_pitch;
+    for (int j = 0; j <= c->world; ++j) {
+      r->row0[j] = pl.row0[j];
+      r->q0[j] = pl.q0[j];
+    }
   }
   for (int j = 0; j < c->world; ++j) {
     r->xb[j] = static_cast<float2*>(xb[j]);
@@ -925,8 +928,10 @@ tfdp_status setup_routes(const Group& G) {
     }
     for (int i = 0; i < G.p; ++i) {
       tfdp_ctx* c = G[i];
-      for (int k = 1; k <= 3; ++k)
-        if (k_used(c, k)) fill_route(c, k, &h[k], xb.data(), ca.data(), phi.data(), xy0.data(), xy1.data());
+      fill_route(c, 0, &h[0], xb.data(), ca.data(), phi.data(), xy0.data(), xy1.data());
+      if (c->p.solver == TFDP_IBFFT)
+        for (int k = 1; k <= 3; ++k)
+          if (k_used(c, k)) fill_route(c, k, &h[k], xb.data(), ca.data(), phi.data(), xy0.data(), xy1.data());
       CUDA_TRY(c, cudaMemcpyAsync(c->d_route, h, sizeof h, cudaMemcpyHostToDevice, c->stream));
       c->route_dirty = false;
     }
@@ -941,7 +946,9 @@ tfdp_status setup_routes(const Group& G) {
   void* bufs[kB] = {c->xb, c->ca, c->phi, c->xy[0], c->xy[1]};
   int got = 1;  // a failure here must not leave the other ranks in the handle broadcast alone
   for (int b = 0; b < kB; ++b)
-    if (cudaIpcGetMemHandle(&mine[b], bufs[b]) != cudaSuccess) {
+    if (!bufs[b]) {  // (the exact path exchanges positions only)
+      memset(&mine[b], 0, sizeof(cudaIpcMemHandle_t));
+    } else if (cudaIpcGetMemHandle(&mine[b], bufs[b]) != cudaSuccess) {
       cudaGetLastError();
       memset(&mine[b], 0, sizeof(cudaIpcMemHandle_t));
       got = 0;
@@ -962,8 +969,8 @@ tfdp_status setup_routes(const Group& G) {
   for (int b = 0; b < kB; ++b) ptr[b].resize(p);
   for (int r = 0; r < p; ++r)
     for (int b = 0; b < kB; ++b) {
-      if (r == c->rank) {
-        ptr[b][r] = bufs[b];
+      if (r == c->rank || !bufs[b]) {
+        ptr[b][r] = r == c->rank ? bufs[b] : nullptr;
         continue;
       }
       cudaIpcMemHandle_t hh, zero;
@@ -982,7 +989,7 @@ tfdp_status setup_routes(const Group& G) {
   // every rank must be able to map every peer, else all fall back to the copy exchanges
   int ok = got;
   for (int b = 0; b < kB; ++b)
-    for (int r = 0; r < p; ++r) ok &= ptr[b][r] != nullptr;
+    for (int r = 0; r < p; ++r) ok &= !bufs[b] || ptr[b][r] != nullptr;
   CUDA_TRY(c, cudaMemcpyAsync(c->bar, &ok, sizeof(int), cudaMemcpyHostToDevice, c->stream));
   NCCL_TRY(c, c->nccl->AllReduce(c->bar, c->bar, 1, ncclInt32, ncclMin, c->comm, c->stream));
   CUDA_TRY(c, cudaMemcpyAsync(&ok, c->bar, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
@@ -993,9 +1000,11 @@ tfdp_status setup_routes(const Group& G) {
     c->p2p = false;
     return TFDP_OK;
   }
-  for (int k = 1; k <= 3; ++k)
-    if (k_used(c, k))
-      fill_route(c, k, &h[k], ptr[0].data(), ptr[1].data(), ptr[2].data(), ptr[3].data(), ptr[4].data());
+  fill_route(c, 0, &h[0], ptr[0].data(), ptr[1].data(), ptr[2].data(), ptr[3].data(), ptr[4].data());
+  if (c->p.solver == TFDP_IBFFT)
+    for (int k = 1; k <= 3; ++k)
+      if (k_used(c, k))
+        fill_route(c, k, &h[k], ptr[0].data(), ptr[1].data(), ptr[2].data(), ptr[3].data(), ptr[4].data());
   CUDA_TRY(c, cudaMemcpyAsync(c->d_route, h, sizeof h, cudaMemcpyHostToDevice, c->stream));
   c->route_dirty = false;
   return TFDP_OK;
@@ -1131,6 +1140,12 @@ tfdp_status evaluate(const Group& G, int update, float eta, int k) {
                   "slab mode of a virtual shard context: use tfdp_group_step / tfdp_group_forces");
     TRY(c0->p2p ? evaluate_slab_p2p(G, update, eta, k) : evaluate_slab(G, update, eta, k));
   } else {
+    if (update && c0->p.solver == TFDP_EXACT && c0->p2p && c0->world > 1) {
+      if (!G.virt() && !c0->comm)
+        return fail(c0, TFDP_ERR_UNSUPPORTED,
+                    "virtual shard context (no NCCL id): use tfdp_group_step / tfdp_group_forces");
+      TRY(setup_routes(G));
+    }
     for (int i = 0; i < G.p; ++i) TRY(evaluate_one(G[i], update, eta, k));
   }
   if (update) {
@@ -1572,7 +1587,8 @@ tfdp_status tfdp_init(tfdp_ctx** out, int64_t n, const int64_t* row_ptr, const i
   c->slab = c->world > 1 && p.solver == TFDP_IBFFT && p.dist_mode == TFDP_DIST_SLAB;
   if (c->slab && c->world > tfdp::kMaxWorld)
     return bail(fail(c, TFDP_ERR_ARG, "slab mode supports world <= %d", tfdp::kMaxWorld));
-  if (c->slab) {  // fused exchanges (peer stores) unless TFDP_P2P=0 (the NCCL / copy path)
+  if (c->slab || (c->world > 1 && p.solver == TFDP_EXACT)) {
+    // fused exchanges (peer stores) unless TFDP_P2P=0 (the NCCL / copy path)
     const char* e = getenv("TFDP_P2P");
     c->p2p = !(e && e[0] == '0');
   }

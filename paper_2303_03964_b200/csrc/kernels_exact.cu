@@ -190,7 +190,7 @@ exact_finish_kernel(const float2* __restrict__ xy, float2* __restrict__ xy_next,
                     const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
                     ForceArgs fa, FocusArgs fo, float eta, int iter, int update,
                     float2* __restrict__ rep_out, float2* __restrict__ att_out,
-                    unsigned long long* diverge) {
+                    unsigned long long* diverge, const PeerRoute* __restrict__ rt, int next_buf) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n_local) return;
   const int64_t i = lo + t;
@@ -216,6 +216,9 @@ exact_finish_kernel(const float2* __restrict__ xy, float2* __restrict__ xy_next,
     const float nx = fmaf(eta, Rx + A.x, xi.x);
     const float ny = fmaf(eta, Ry + A.y, xi.y);
     xy_next[i] = make_float2(nx, ny);
+    if (rt)  // p > 1, fused position all-gather: into every other rank's copy
+      for (int j = 0; j < rt->world; ++j)
+        if (j != rt->rank) rt->xy[next_buf][j][i] = make_float2(nx, ny);
     if (!isfinite(nx) || !isfinite(ny))
       atomicMin(diverge, ((unsigned long long)(unsigned)iter << 32) | (unsigned long long)i);
   } else {
@@ -228,12 +231,14 @@ void launch_exact_finish(const float2* xy, float2* xy_next, int64_t lo, int64_t 
                          int n_chunks, const double2* part, const int64_t* row_ptr,
                          const int32_t* col, ForceArgs fa, FocusArgs fo, float eta, int iter,
                          int update, float2* rep_out, float2* att_out,
-                         unsigned long long* diverge, cudaStream_t s) {
+                         unsigned long long* diverge, cudaStream_t s, const PeerRoute* route,
+                         int next_buf) {
   if (n_local <= 0) return;
   const unsigned blocks = (unsigned)((n_local + kNodeThreads - 1) / kNodeThreads);
   exact_finish_kernel<<<blocks, kNodeThreads, 0, s>>>(xy, xy_next, lo, n_local, n_chunks, part,
                                                       row_ptr, col, fa, fo, eta, iter, update,
-                                                      rep_out, att_out, diverge);
+                                                      rep_out, att_out, diverge, route,
+                                                      next_buf);
 }
 
 }  // namespace tfdp

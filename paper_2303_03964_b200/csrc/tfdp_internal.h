@@ -111,7 +111,8 @@ void launch_exact_finish(const float2* xy, float2* xy_next, int64_t lo, int64_t 
                          int n_chunks, const double2* part, const int64_t* row_ptr,
                          const int32_t* col, ForceArgs fa, FocusArgs fo, float eta, int iter,
                          int update, float2* rep_out, float2* att_out,
-                         unsigned long long* diverge, cudaStream_t s);
+                         unsigned long long* diverge, cudaStream_t s,
+                         const struct PeerRoute* route = nullptr, int next_buf = 0);
 
 // ibFFT path
 // Box: producers merge one block-reduced BoxKeys per block into kBoxSlots slots (atomic

@@ -121,9 +121,12 @@ def test_modes_small_graph(mode, stream):
         _close(G)
 
 
-def test_exact_group_step_bitwise(stream):
+@pytest.mark.parametrize("p2p", ["1", "0"])
+def test_exact_group_step_bitwise(p2p, stream, monkeypatch):
     """Exact path: 4 ranks x 3 steps through the group equal the one-rank steps bit for bit
-    (fixed per-target source order, R15)."""
+    (fixed per-target source order, R15), with the position all-gather fused into the update
+    (peer stores, TFDP_P2P=1) or as device copies (TFDP_P2P=0)."""
+    monkeypatch.setenv("TFDP_P2P", p2p)
     w, rp, col = _case("C2")
     prm = P.Params(solver="exact")
     with P.Layout(w.n, rp, col, w.xy, prm) as L1:
