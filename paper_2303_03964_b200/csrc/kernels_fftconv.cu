@@ -33,6 +33,7 @@
 // kernel samples.
 #include <algorithm>
 #include <cstdlib>
+#include <string>
 #include <type_traits>
 
 #include "device_math.cuh"
@@ -1128,6 +1129,253 @@ cols1_kernel(const GridGeom* __restrict__ geom, float2* __restrict__ CA, int ca_
 
 }  // namespace aos
 
+// ================================================================ register core (columns)
+// One warp per (channel, column) item, the FFT of P = 32 A points held in registers as a
+// four-step transform (lane b owns the residue class n = b mod 32):
+//   1. lane b: DFT_A over a of x[b + 32 a] (in registers; a >= A/2 is zero padding)
+//   2. twiddle W_P^(b k1)
+//   3. transpose through shared memory (lane L gets k1 = L + 32 kk, all b)
+//   4. lane L: DFT_32 over b -> X[k1 + A k2]
+// then x conj(K^) and the inverse as the same steps in reverse order (DFT_32 in registers,
+// twiddle, transpose, DFT_A with only its low half of outputs kept).  Two shared-memory
+// round trips per FFT instead of one per radix-16 stage, no block barrier, and every lane
+// holds 32-64 independent values (the radix-16 column pass is bound by shared-memory
+// wavefronts and barrier stalls).  Sub-DFTs use compile-time twiddles.
+namespace reg {
+
+constexpr double kPiD = 3.14159265358979323846;
+constexpr double cx_sin(double x) {  // |x| <= 3 pi / 2 after cx_red
+  double t = x, s = x;
+  for (int i = 1; i < 30; ++i) {
+    t *= -x * x / ((2.0 * i) * (2.0 * i + 1));
+    s += t;
+  }
+  return s;
+}
+constexpr double cx_red(double x) {
+  while (x > kPiD) x -= 2 * kPiD;
+  while (x < -kPiD) x += 2 * kPiD;
+  return x;
+}
+// W_N^e = exp(-2 pi i e / N), e = 0..N-1, rounded from double
+template <int N>
+struct WTab {
+  float c[N], s[N];
+  constexpr WTab() : c(), s() {
+    for (int e = 0; e < N; ++e) {
+      const double a = -2.0 * kPiD * e / N;
+      s[e] = (float)cx_sin(cx_red(a));
+      c[e] = (float)cx_sin(cx_red(a + kPiD / 2));
+    }
+  }
+};
+template <int N>
+__device__ constexpr WTab<N> kW{};
+
+// In-register DFT of N = 16 A' values, natural order in and out: n = n1 + A' n2, k = k2 + 16 k1
+// (DFT_16 over n2, twiddle W_N^(n1 k2), DFT_A' over n1).  ZU: inputs n >= N/2 are zero
+// (never read).  Outputs the caller never uses are dead code to the compiler.
+template <int N, bool ZU>
+__device__ __forceinline__ void dftr(float2 (&v)[N]) {
+  if constexpr (N == 16) {
+    aos::dft16<ZU>(v);
+  } else {
+    static_assert(N == 32 || N == 64, "register DFT size");
+    constexpr int A1 = N / 16;
+    float2 t[A1][16];
+#pragma unroll
+    for (int n1 = 0; n1 < A1; ++n1) {
+#pragma unroll
+      for (int n2 = 0; n2 < 16; ++n2)
+        t[n1][n2] = (ZU && n2 >= 8) ? make_float2(0.f, 0.f) : v[n1 + A1 * n2];
+      aos::dft16<ZU>(t[n1]);
+#pragma unroll
+      for (int k2 = 1; k2 < 16; ++k2)
+        if (n1 > 0) t[n1][k2] = cmul(t[n1][k2], make_float2(kW<N>.c[n1 * k2], kW<N>.s[n1 * k2]));
+    }
+#pragma unroll
+    for (int k2 = 0; k2 < 16; ++k2) {
+      float2 u[A1];
+#pragma unroll
+      for (int n1 = 0; n1 < A1; ++n1) u[n1] = t[n1][k2];
+      aos::dft<A1>(u);
+#pragma unroll
+      for (int k1 = 0; k1 < A1; ++k1) v[k2 + 16 * k1] = u[k1];
+    }
+  }
+}
+
+// slab mode: the lane's outputs G[lane + 32 nb] (staged in buf[nb * 32 + lane]) into the
+// row owners' half spectra, conjugated (out of line: keeps the kernel's allocation)
+__device__ __noinline__ void route_store_col(const PeerRoute* __restrict__ rt,
+                                             const float2* buf, int lane, int nbs, int M,
+                                             int ch, int qg, int H) {
+  for (int nb = 0; nb < nbs; ++nb) {
+    const int u = lane + 32 * nb;
+    if (u >= M) break;
+    const float2 z = buf[nb * 32 + lane];
+    rt->ca[route_owner(rt->row0, rt->world, u)][ca_col_base(ch, qg, H, rt->ca_pitch) +
+                                                ca_row_off(u, H)] = make_float2(z.x, -z.y);
+  }
+}
+
+// v[8 i + j] *= W_P^(m (8 i + j)) from the two-level table (short product chains)
+template <int P, int NV>
+__device__ __forceinline__ void twiddle_row(const float2* __restrict__ tws, int m, float2 (&v)[NV]) {
+  float2 p[8];
+  p[0] = make_float2(1.f, 0.f);
+#pragma unroll
+  for (int j = 1; j < 8; ++j) p[j] = tw_at(tws, (m * j) % P);
+#pragma unroll
+  for (int i = 0; i < NV / 8; ++i) {
+    const float2 qi = i == 0 ? make_float2(1.f, 0.f) : tw_at(tws, (8 * m * i) % P);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (i == 0 && j == 0) continue;
+      v[8 * i + j] = cmul(v[8 * i + j], i == 0 ? p[j] : j == 0 ? qi : cmul(qi, p[j]));
+    }
+  }
+}
+
+constexpr int kWarps = 4;  // items (warps) per block
+template <int P>
+__host__ __device__ constexpr int xbuf_len() {
+  return (P / 32) * 33;
+}
+template <int P>
+__host__ __device__ constexpr size_t smem_bytes() {
+  return (size_t)(kWarps * xbuf_len<P>() + tw_len(P)) * sizeof(float2);
+}
+
+template <int P, int MINB>
+__global__ void __launch_bounds__(32 * kWarps, MINB)
+cols_reg_kernel(const GridGeom* __restrict__ geom, float2* __restrict__ CA, int ca_pitch,
+                const float* __restrict__ KH, const float2* __restrict__ tw, int q_base, int Hl,
+                const PeerRoute* __restrict__ rt) {
+  constexpr int A = P / 32, KPL = A / 32, SA = 33;
+  constexpr int half = P / 2;
+  extern __shared__ float2 sm[];
+  float2* tws = sm + kWarps * xbuf_len<P>();
+  load_tw(tws, tw, P);
+  pdl_wait();
+  pdl_trigger();
+  __syncthreads();
+  const int M = geom->M;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  float2* xb = sm + wid * xbuf_len<P>();
+  const int items = 3 * Hl;
+  for (int it = blockIdx.x * kWarps + wid; it < items; it += gridDim.x * kWarps) {
+    const int ql = it / 3, ch = it - 3 * ql, qg = q_base + ql;
+    const float2* col = CA + ca_col_base(ch, ql, Hl, ca_pitch);
+    // 1. DFT_A over a of x[lane + 32 a] (a < A/2; the rest is zero padding, M <= P/2)
+    // rows u = lane + 32 a sit at ca_row_off(lane, Hl) + a * 32 Hl (kCaTile divides 32)
+    const int64_t rstride = (int64_t)(32 / kCaTile) * kCaTile * Hl;
+    float2 v[A];
+    {
+      const float2* pl = col + ca_row_off(lane, Hl);
+#pragma unroll
+      for (int a = 0; a < A / 2; ++a)
+        v[a] = lane + 32 * a < M ? pl[a * rstride] : make_float2(0.f, 0.f);
+    }
+    dftr<A, true>(v);
+    // 2. twiddle W_P^(lane k1);  3. transpose: row k1 of the buffer (stride 33) = (b -> Y[b][k1])
+    twiddle_row<P, A>(tws, lane, v);
+#pragma unroll
+    for (int k1 = 0; k1 < A; ++k1) xb[k1 * SA + lane] = v[k1];
+    __syncwarp();
+    const float* kh = KH + (int64_t)qg * P;
+    // lane L owns rows k1 = L + 32 kk: reads its row, writes the inverse's row back in place
+    // (row k1 = (n_a -> S[k1][n_a])), so no lane touches another lane's row in between
+#pragma unroll 1
+    for (int kk = 0; kk < KPL; ++kk) {
+      const int k1 = lane + 32 * kk;
+      float2 w[32];
+#pragma unroll
+      for (int b = 0; b < 32; ++b) w[b] = xb[k1 * SA + b];
+      // 4. DFT_32 over b -> X[k1 + A k2];  x K^ (real), conjugated for the inverse
+      dftr<32, false>(w);
+#pragma unroll
+      for (int k2 = 0; k2 < 32; ++k2) {
+        const float kv = __ldg(kh + k1 + A * k2);
+        w[k2] = make_float2(w[k2].x * kv, -w[k2].y * kv);
+      }
+      // inverse: DFT_32 over k2 -> S[k1][n_a], twiddle W_P^(n_a k1)
+      dftr<32, false>(w);
+      twiddle_row<P, 32>(tws, k1, w);
+#pragma unroll
+      for (int na = 0; na < 32; ++na) xb[k1 * SA + na] = w[na];
+    }
+    __syncwarp();
+    float2 y[A];
+#pragma unroll
+    for (int k1 = 0; k1 < A; ++k1) y[k1] = xb[k1 * SA + lane];
+    __syncwarp();
+    // DFT_A over k1 -> G[lane + 32 n_b]; rows u < M <= P/2 kept (n_b < A/2), conjugated
+    dftr<A, false>(y);
+    if (rt) {  // slab mode, fused transpose back: via the warp's buffer, out of line
+#pragma unroll
+      for (int nb = 0; nb < A / 2; ++nb) xb[nb * 32 + lane] = y[nb];
+      __syncwarp();
+      route_store_col(rt, xb, lane, A / 2, M, ch, qg, half + 1);
+      __syncwarp();
+    } else {
+      // the store addresses recomputed (opaque stride): the load phase's do not stay live
+      int64_t rs;
+      asm volatile("mov.b64 %0, %1;" : "=l"(rs) : "l"(rstride));
+      float2* pl = CA + ca_col_base(ch, ql, Hl, ca_pitch) + ca_row_off(lane, Hl);
+#pragma unroll
+      for (int nb = 0; nb < A / 2; ++nb)
+        if (lane + 32 * nb < M) pl[nb * rs] = make_float2(y[nb].x, -y[nb].y);
+    }
+  }
+}
+
+// sizes with a register column kernel
+template <int P>
+constexpr bool has() {
+  return P == 2048;
+}
+
+template <int P>
+cudaError_t prepare() {
+  if constexpr (has<P>()) {
+    cudaError_t e = cudaFuncSetAttribute(cols_reg_kernel<P, 3>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem_bytes<P>());
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(cols_reg_kernel<P, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem_bytes<P>());
+    return e;
+  } else
+    return cudaSuccess;
+}
+
+template <int P>
+bool launch(const GridGeom* geom, float2* CA, int ca_pitch, const float* KH, const float2* tw,
+            int q0, int q1, cudaStream_t s, const PeerRoute* route) {
+  if constexpr (has<P>()) {
+    // persistent: one wave of MINB blocks per SM, items strided over the warps.  MINB = 3
+    // (168 registers, ~200 B of spills) or 2 (255 registers): TFDP_COLS_MINB
+    static const int minb = [] {
+      const char* e = std::getenv("TFDP_COLS_MINB");
+      return e && e[0] == '2' ? 2 : 3;
+    }();
+    const int items = 3 * (q1 - q0);
+    const int blocks = std::min((items + kWarps - 1) / kWarps, 148 * minb);
+    if (minb == 2)
+      cols_reg_kernel<P, 2><<<(unsigned)blocks, 32 * kWarps, smem_bytes<P>(), s>>>(
+          geom, CA, ca_pitch, KH, tw, q0, q1 - q0, route);
+    else
+      cols_reg_kernel<P, 3><<<(unsigned)blocks, 32 * kWarps, smem_bytes<P>(), s>>>(
+          geom, CA, ca_pitch, KH, tw, q0, q1 - q0, route);
+    return true;
+  } else {
+    return false;
+  }
+}
+
+}  // namespace reg
+
 }  // namespace
 
 // Supported FFT sizes: P = 256 q, q = 2^a 3^b 5^c with b <= 2, c <= 1, P <= 16384.  The SoA
@@ -1187,6 +1435,7 @@ cudaError_t fftconv_prepare(int P) {
       e = cudaFuncSetAttribute(kspec_cols_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, b); \
     if (e == cudaSuccess)                                                                     \
       e = cudaFuncSetAttribute(cols_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, b); \
+    if (e == cudaSuccess) e = reg::prepare<S>();                                              \
     TFDP_PREP_ROWS(S, 1)                                                                      \
     TFDP_PREP_ROWS(S, 2)                                                                      \
     TFDP_PREP_ROWS(S, 4)                                                                      \
@@ -1272,12 +1521,24 @@ void launch_rows_fwd(const GridGeom* geom, const float4* C, int cpitch, int P, i
 #undef TFDP_RF
 }
 
+// Column pass core: the radix-16 shared-memory kernel; TFDP_COLS=reg selects the register
+// four-step kernel where it exists (P = 2048), measured slower and kept as an A/B variant
+// (C4 k = 1: 39.4 / 37.7 us at 3 / 2 blocks per SM against 30.0 us).
+static bool cols_reg() {
+  static const bool on = [] {
+    const char* e = std::getenv("TFDP_COLS");
+    return e && std::string(e) == "reg";
+  }();
+  return on;
+}
+
 void launch_cols(const GridGeom* geom, float2* CA, int ca_pitch, const float* KH, int P,
                  const float2* tw, int q0, int q1, cudaStream_t s, const PeerRoute* route) {
   if (q1 <= q0) return;
   const size_t sm = fftconv_smem_bytes(P);
 #define TFDP_CO(S)                                                                          \
   case S:                                                                                   \
+    if (cols_reg() && reg::launch<S>(geom, CA, ca_pitch, KH, tw, q0, q1, s, route)) break;  \
     cols_kernel<S><<<(unsigned)(3 * ((q1 - q0 + 1) / 2)), fft_threads_c(S), sm, s>>>(      \
         geom, CA, ca_pitch, KH, tw, q0, q1 - q0, route);                                    \
     break;

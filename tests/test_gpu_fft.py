@@ -381,6 +381,38 @@ print("tile ok")
     assert r.returncode == 0 and "tile ok" in r.stdout
 
 
+def test_cols_register_variant_subprocess():
+    """The register four-step column kernel (TFDP_COLS=reg, P = 2048; measured slower and
+    kept as an A/B variant) is parity-tested too: forced P = 2048 grids at k = 1, 2, 3, equal
+    to the radix-16 kernel up to fp32 rounding, and the slab mode's routed stores (3 virtual
+    ranks)."""
+    import subprocess
+    import sys
+    code = r"""
+import numpy as np, torch, oracle as O, paper_2303_03964_b200 as P
+from synth import random_layout, random_graph
+n = 6000
+X = random_layout(n, 31, 30.0); u, v = random_graph(n, 4 * n, 32); rp, col = O.csr_build(n, u, v)
+for k, nf in ((1, 1000), (2, 500), (3, 333)):
+    prm = P.Params(solver="ibfft", k=k, n_int_fixed=nf, fft_size=2048)
+    with P.Layout(n, rp, col, X, prm) as L:
+        R, _ = L.forces(); assert L.fft_geometry()["P"] == 2048
+    e = O.rel_l2(R, O.repulsion_ibfft(X.astype(np.float64), k, n_int_fixed=nf))
+    print(k, e); assert e <= 1e-4, (k, e)
+    s = torch.cuda.Stream().cuda_stream
+    G = [P.Layout(n, rp, col, X, prm, dist=P.Dist(r, 3, 0, None), stream=s) for r in range(3)]
+    Rg = np.concatenate([o[0] for o in P.group_forces(G)])
+    for L in G: L.close()
+    eg = O.rel_l2(Rg, R); print("slab", k, eg); assert eg <= 1e-4, (k, eg)  # atomics order (R15)
+print("reg ok")
+"""
+    env = dict(os.environ, TFDP_COLS="reg")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    print(r.stdout, r.stderr[-2000:])
+    assert r.returncode == 0 and "reg ok" in r.stdout
+
+
 @pytest.mark.parametrize("P_", [9216, 12288, 16384])
 @pytest.mark.parametrize("k", [1, 3])
 def test_large_fft_sizes_forced(P_, k):
