@@ -90,6 +90,7 @@ def build(verbose: bool = False, force: bool = False, defines=(), out: str = Non
     os.replace(out + ".tmp", out)
     if out == LIB:
         build_examples(verbose)
+        build_nccl_loopback(verbose)
     return out
 
 
@@ -110,6 +111,25 @@ def build_examples(verbose: bool = False) -> list:
             raise RuntimeError("gcc failed:\n" + " ".join(cmd))
         outs.append(exe)
     return outs
+
+
+LOOPBACK_SRC = os.path.join(ROOT, "tests", "nccl_loopback", "nccl_loopback.cpp")
+LOOPBACK_LIB = os.path.join(ROOT, "tests", "nccl_loopback", "libnccl_loopback.so")
+
+
+def build_nccl_loopback(verbose: bool = False) -> str:
+    """The tests' in-process NCCL stand-in (TFDP_NCCL_LIB; test infrastructure, not linked
+    into libtfdp.so): g++ against the CUDA runtime."""
+    cuda = os.path.dirname(os.path.dirname(_nvcc()))
+    cmd = ["g++", "-O2", "-std=c++17", "-shared", "-fPIC", "-I", os.path.join(cuda, "include"),
+           "-I", _nccl_include(), LOOPBACK_SRC, "-L", os.path.join(cuda, "lib64"), "-lcudart",
+           "-Wl,-rpath," + os.path.join(cuda, "lib64"), "-o", LOOPBACK_LIB]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if verbose or r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+    if r.returncode != 0:
+        raise RuntimeError("g++ failed:\n" + " ".join(cmd))
+    return LOOPBACK_LIB
 
 
 if __name__ == "__main__":

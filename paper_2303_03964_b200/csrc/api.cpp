@@ -944,10 +944,19 @@ tfdp_status setup_routes(const Group& G) {
   constexpr int kB = 5;  // buffers per rank: xb, ca, phi, xy0, xy1
   std::vector<cudaIpcMemHandle_t> mine(kB);
   void* bufs[kB] = {c->xb, c->ca, c->phi, c->xy[0], c->xy[1]};
+  // TFDP_IPC_LOOPBACK=1 (tests only: the ranks are threads of one process, whose own
+  // allocations CUDA IPC cannot open): the exchanged "handles" carry the raw device pointers
+  static const bool loopback = [] {
+    const char* e = getenv("TFDP_IPC_LOOPBACK");
+    return e && e[0] == '1';
+  }();
   int got = 1;  // a failure here must not leave the other ranks in the handle broadcast alone
   for (int b = 0; b < kB; ++b)
     if (!bufs[b]) {  // (the exact path exchanges positions only)
       memset(&mine[b], 0, sizeof(cudaIpcMemHandle_t));
+    } else if (loopback) {
+      memset(&mine[b], 0, sizeof(cudaIpcMemHandle_t));
+      memcpy(&mine[b], &bufs[b], sizeof(void*));
     } else if (cudaIpcGetMemHandle(&mine[b], bufs[b]) != cudaSuccess) {
       cudaGetLastError();
       memset(&mine[b], 0, sizeof(cudaIpcMemHandle_t));
@@ -977,8 +986,10 @@ tfdp_status setup_routes(const Group& G) {
       memcpy(&hh, all.data() + hs * r + sizeof(cudaIpcMemHandle_t) * b, sizeof hh);
       memset(&zero, 0, sizeof zero);
       void* q = nullptr;
-      if (memcmp(&hh, &zero, sizeof hh) != 0 &&
-          cudaIpcOpenMemHandle(&q, hh, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess) {
+      if (loopback) {
+        memcpy(&q, &hh, sizeof(void*));
+      } else if (memcmp(&hh, &zero, sizeof hh) != 0 &&
+                 cudaIpcOpenMemHandle(&q, hh, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess) {
         c->ipc_open.push_back(q);
       } else {
         cudaGetLastError();
@@ -1015,7 +1026,6 @@ tfdp_status setup_routes(const Group& G) {
 // potential rows and gather_update the new positions into every rank — no pack / unpack, no
 // separate transfers; three phase barriers per evaluation (plus the position barrier).
 tfdp_status evaluate_slab_p2p(const Group& G, int update, float eta, int k) {
-  TRY(setup_routes(G));
   bool overlap[tfdp::kMaxWorld];
   for (int i = 0; i < G.p; ++i) {  // phase A: spread of the slab, row FFTs -> peers' xb
     tfdp_ctx* c = G[i];
@@ -1138,6 +1148,8 @@ tfdp_status evaluate(const Group& G, int update, float eta, int k) {
     if (!G.virt() && !c0->comm)
       return fail(c0, TFDP_ERR_UNSUPPORTED,
                   "slab mode of a virtual shard context: use tfdp_group_step / tfdp_group_forces");
+    // the routes first: a rank that cannot map a peer turns every rank to the copy path
+    if (c0->p2p) TRY(setup_routes(G));
     TRY(c0->p2p ? evaluate_slab_p2p(G, update, eta, k) : evaluate_slab(G, update, eta, k));
   } else {
     if (update && c0->p.solver == TFDP_EXACT && c0->p2p && c0->world > 1) {

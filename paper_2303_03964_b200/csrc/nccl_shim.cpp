@@ -2,6 +2,8 @@
 
 #include <dlfcn.h>
 
+#include <cstdlib>
+
 #include <mutex>
 
 namespace tfdp {
@@ -11,8 +13,20 @@ const NcclApi* nccl_api(const char** err) {
   static std::once_flag once;
   static const char* load_err = nullptr;
   std::call_once(once, [] {
-    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
-    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    // TFDP_NCCL_LIB: another implementation of the NCCL API (the tests' in-process loopback
+    // stand-in, tests/nccl_loopback), loaded privately so it cannot shadow torch's NCCL
+    const char* alt = getenv("TFDP_NCCL_LIB");
+    void* h = nullptr;
+    if (alt && alt[0]) {
+      h = dlopen(alt, RTLD_NOW | RTLD_LOCAL);
+      if (!h) {
+        load_err = "TFDP_NCCL_LIB could not be loaded";
+        return;
+      }
+    } else {
+      h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+      if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    }
     if (!h) {
       load_err = "libnccl.so.2 not found (import torch first, or set LD_LIBRARY_PATH)";
       return;

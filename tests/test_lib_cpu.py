@@ -125,3 +125,16 @@ def test_c_example_builds_and_links():
     from paper_2303_03964_b200 import build as B
     exes = B.build_examples()
     assert exes and all(os.path.exists(e) for e in exes)
+
+
+def test_nccl_loopback_builds_and_exports():
+    """The tests' in-process NCCL stand-in (tests/nccl_loopback) builds with g++ and exports
+    every NCCL entry point libtfdp.so resolves (csrc/nccl_shim.cpp)."""
+    import ctypes
+    from paper_2303_03964_b200 import build as B
+    path = B.build_nccl_loopback()
+    lb = ctypes.CDLL(path)
+    for s in ("ncclGetUniqueId", "ncclCommInitRank", "ncclCommDestroy", "ncclGroupStart",
+              "ncclGroupEnd", "ncclBroadcast", "ncclAllReduce", "ncclSend", "ncclRecv",
+              "ncclGetErrorString"):
+        assert hasattr(lb, s), s
