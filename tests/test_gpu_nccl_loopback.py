@@ -156,3 +156,43 @@ def test_np1_and_divergence_nccl():
     """NP1 gathered over the communicator equals one rank's on the same layout; a diverging
     layout fails both ranks at the same check (divergence word all-reduced)."""
     _run(MISC, TFDP_IPC_LOOPBACK="1")
+
+
+GROW = r"""
+from synth import random_layout, random_graph
+n = 2000
+X = random_layout(n, 41, 3.0); u, v = random_graph(n, 2 * n, 42); rp, col = O.csr_build(n, u, v)
+prm = P.Params(solver="ibfft", k=1, rho=50.0, iterations=300)
+def fn(L):
+    P0 = L.fft_plan(1)[0]
+    L.step(96)
+    R, _ = L.forces()
+    return P0, L.fft_plan(1)[0], L.layout(), R
+out = group(2, n, rp, col, X, prm, fn)
+assert np.array_equal(out[0][2], out[1][2])
+assert out[0][1] > out[0][0] and out[1][1] == out[0][1], [(o[0], o[1]) for o in out]
+R = np.concatenate([o[3] for o in out])
+e = O.rel_l2(R, O.repulsion_ibfft(out[0][2].astype(np.float64), 1, rho=50.0))
+print("grow", out[0][0], "->", out[0][1], "rel", e, flush=True); assert e <= 1e-3
+# host-path set_layout + PivotMDS at p = 2: every rank holds the same layout as one rank
+w, rp, col = case("C3")
+prm = P.Params(solver="ibfft", k=1)
+def fp(L):
+    L.pivot_mds(20, seed=5); Xp = L.layout()
+    L.set_layout(w.xy); Xs = L.layout()
+    return Xp, Xs
+Xp1, _ = one(w.n, rp, col, w.xy, prm, fp)
+out = group(2, w.n, rp, col, w.xy, prm, fp)
+for Xp, Xs in out:
+    assert np.array_equal(Xs, w.xy.astype(np.float32))
+    assert O.rel_l2(Xp, Xp1) <= 1e-5
+print("pmds/set_layout ok", flush=True)
+print("ALL OK")
+"""
+
+
+def test_replans_pmds_set_layout_nccl():
+    """A layout growing far beyond its first plan re-plans on every rank at the same step
+    (buffers re-allocated, peer routes re-exchanged over the communicator); PivotMDS and a
+    host set_layout at p = 2 leave every rank with one rank's layout."""
+    _run(GROW, TFDP_IPC_LOOPBACK="1")
