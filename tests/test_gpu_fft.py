@@ -381,6 +381,45 @@ print("tile ok")
     assert r.returncode == 0 and "tile ok" in r.stdout
 
 
+@pytest.mark.parametrize("env", ["TFDP_ATTR_SIDE=0", "TFDP_HEAVY=0", "TFDP_PDL=0",
+                                 "TFDP_KSPEC_OVERLAP=0", "TFDP_ROWS_RB=1", "TFDP_ROWS_RB=4",
+                                 "TFDP_PDL_MAX_FFT=8192"])
+def test_env_variants_subprocess(env):
+    """Every A/B switch of DESIGN §7 keeps parity: Morton-ordered C3 forces at k = 1, 2, 3
+    against the oracle after 8 steps, 40 iterations of the dynamic schedule, and the
+    attraction (exact definition) on a Chung-Lu graph with hub rows."""
+    import subprocess
+    import sys
+    code = r"""
+import numpy as np, oracle as O, paper_2303_03964_b200 as P
+from synth import make_config, random_layout
+w = make_config("C3"); rp, col = O.csr_build(w.n, w.u, w.v)
+for k in (1, 2, 3):
+    with P.Layout(w.n, rp, col, w.xy, P.Params(solver="ibfft", k=k, step0=1e-4)) as L:
+        L.step(8); R, A = L.forces(); X = L.layout().astype(np.float64)
+    e = O.rel_l2(R, O.repulsion_ibfft(X, k)); ea = O.rel_l2(A, O.attraction(X, rp, col))
+    print(k, e, ea); assert e <= 1e-3 and ea <= 1e-4, (k, e, ea)
+with P.Layout(w.n, rp, col, w.xy, P.Params(solver="ibfft", k=0, iterations=40)) as L:
+    L.step(40); assert np.isfinite(L.layout()).all()
+from synth import chung_lu_graph
+n = 20000
+u, v = chung_lu_graph(n, 12.0, 2.1, 9)  # power-law degrees: hub rows above the 128 split
+rp, col = O.csr_build(n, u, v)
+assert np.diff(rp).max() > 300
+X = random_layout(n, 7, 40.0)
+with P.Layout(n, rp, col, X, P.Params(solver="ibfft", k=1)) as L:
+    _, A = L.forces()
+ea = O.rel_l2(A, O.attraction(X.astype(np.float64), rp, col)); print("hubs", ea); assert ea <= 1e-4
+print("variant ok")
+"""
+    k, v = env.split("=")
+    e = dict(os.environ, **{k: v})
+    r = subprocess.run([sys.executable, "-c", code], env=e, capture_output=True, text=True,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    print(r.stdout, r.stderr[-2000:])
+    assert r.returncode == 0 and "variant ok" in r.stdout
+
+
 def test_cols_register_variant_subprocess():
     """The register four-step column kernel (TFDP_COLS=reg, P = 2048; measured slower and
     kept as an A/B variant) is parity-tested too: forced P = 2048 grids at k = 1, 2, 3, equal
