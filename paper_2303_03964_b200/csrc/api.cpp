@@ -69,6 +69,12 @@ struct tfdp_ctx {
   bool attr_pre = false;  // this evaluation's attraction is in attr
   float2* attr = nullptr;
   bool kspec_overlap = true;  // env TFDP_KSPEC_OVERLAP=0 runs it in line (tuning / A-B)
+  // where the side stream's attraction forks off the FFT chain (TFDP_ATTR_AT): 0 after setup,
+  // 1 after rows_fwd, 2 after cols; its grid (TFDP_ATTR_BLOCKS: 0 = one thread per node)
+  int attr_at = 0;
+  int attr_blocks = 0;
+  bool attr_deferred = false;
+  cudaEvent_t ev_fork2 = nullptr;
   float2* xy[2] = {nullptr, nullptr};
   int cur = 0;
   int64_t* row_ptr = nullptr;
@@ -739,7 +745,27 @@ int pdl_max_fft() {
 }
 
 // bbox (when the box is not known) + setup + the kernel spectrum forked on the side stream
-void fft_prologue(tfdp_ctx* c, int k, bool* overlap) {
+// heavy-row chunks + the per-node attraction on stream st; the join event for gather_update
+void side_attraction(tfdp_ctx* c, cudaStream_t st, bool overlap) {
+  heavy_rows(c, st);
+  if (c->attr_pre) {
+    Scope sc(c, K_ATTR, st);
+    tfdp::launch_attraction(c->xy[c->cur], c->lo, c->hi - c->lo, c->row_ptr, c->col, c->fa,
+                            c->attr, st, c->attr_blocks);
+  }
+  if (overlap) cudaEventRecord(c->ev_join2, st);
+}
+
+// the deferred side-stream attraction, forked at this point of the main stream
+void fork_attraction(tfdp_ctx* c, bool overlap, int at) {
+  if (!c->attr_deferred || c->attr_at != at) return;
+  c->attr_deferred = false;
+  cudaEventRecord(c->ev_fork2, c->stream);
+  cudaStreamWaitEvent(c->side, c->ev_fork2, 0);
+  side_attraction(c, c->side, overlap);
+}
+
+void fft_prologue(tfdp_ctx* c, int k, bool* overlap, bool allow_defer = false) {
   const int P = c->P_of_k[k];
   tfdp::set_pdl_active(P <= pdl_max_fft());
   if (!c->box_valid || c->world > 1) {
@@ -772,14 +798,9 @@ void fft_prologue(tfdp_ctx* c, int k, bool* overlap) {
   if (*overlap) cudaEventRecord(c->ev_join, c->side);  // cols joins here
   // the attraction depends only on the positions: heavy-row chunks and the per-node sums also
   // run beside spread + FFT passes; gather_update joins after them (ev_join2)
-  heavy_rows(c, ks);
   c->attr_pre = c->attr_side && !c->focus_on && c->attr;
-  if (c->attr_pre) {
-    Scope sc(c, K_ATTR, ks);
-    tfdp::launch_attraction(c->xy[c->cur], c->lo, c->hi - c->lo, c->row_ptr, c->col, c->fa,
-                            c->attr, ks);
-  }
-  if (*overlap) cudaEventRecord(c->ev_join2, c->side);
+  c->attr_deferred = allow_defer && *overlap && c->attr_at > 0;
+  if (!c->attr_deferred) side_attraction(c, ks, *overlap);
 }
 
 tfdp::FocusArgs focus_prologue(tfdp_ctx* c) {
@@ -823,7 +844,7 @@ tfdp_status evaluate_one(tfdp_ctx* c, int update, float eta, int k) {
     const int mcap = c->cap_of_k[k] * k;
     const float2* tw = c->tw[k];
     bool overlap;
-    fft_prologue(c, k, &overlap);
+    fft_prologue(c, k, &overlap, true);
     // The charges are all-zero here: they start zeroed and rows_inv clears the rows rows_fwd
     // consumed (no separate zeroing pass).
     float4* grid4 = reinterpret_cast<float4*>(c->grid);
@@ -850,11 +871,13 @@ tfdp_status evaluate_one(tfdp_ctx* c, int update, float eta, int k) {
       tfdp::launch_rows_fwd(c->geom, grid4, pitch_k(c, k), P, 0, mcap, tw, c->ca, c->ca_pitch,
                             c->stream);
     }
+    fork_attraction(c, overlap, 1);
     if (overlap) CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_join, 0));
     {
       Scope sc(c, K_COLS);
       tfdp::launch_cols(c->geom, c->ca, c->ca_pitch, c->kh[k], P, tw, 0, P / 2 + 1, c->stream);
     }
+    fork_attraction(c, overlap, 2);
     {
       Scope sc(c, K_ROWS_INV);
       tfdp::launch_rows_inv(c->geom, c->ca, c->ca_pitch, P, 0, mcap, tw, c->phi, pitch_k(c, k),
@@ -1549,9 +1572,12 @@ tfdp_status tfdp_init(tfdp_ctx** out, int64_t n, const int64_t* row_ptr, const i
   if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&c->ev_join2, cudaEventDisableTiming) != cudaSuccess)
+      cudaEventCreateWithFlags(&c->ev_join2, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_fork2, cudaEventDisableTiming) != cudaSuccess)
     return bail(fail(c, TFDP_ERR_CUDA, "side stream / events"));
   if (const char* e = getenv("TFDP_KSPEC_OVERLAP")) c->kspec_overlap = atoi(e) != 0;
+  if (const char* e = getenv("TFDP_ATTR_AT")) c->attr_at = std::max(0, std::min(2, atoi(e)));
+  if (const char* e = getenv("TFDP_ATTR_BLOCKS")) c->attr_blocks = std::max(0, atoi(e));
   const bool xy_dev = is_device_ptr(xy0);
   float L0 = 1.f;
   if (!xy_dev) {
@@ -2183,6 +2209,7 @@ void tfdp_destroy(tfdp_ctx* c) {
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
   if (c->ev_join2) cudaEventDestroy(c->ev_join2);
+  if (c->ev_fork2) cudaEventDestroy(c->ev_fork2);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }

@@ -576,18 +576,22 @@ __global__ void __launch_bounds__(kNodeThreads)
 attraction_kernel(const float2* __restrict__ xy, int64_t lo, int64_t n_local,
                   const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
                   ForceArgs fa, float2* __restrict__ A) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n_local) return;
-  const int64_t i = lo + t;
-  const float2 s = attraction_sum_hv(xy, xy[i], row_ptr, col, i, fa);
-  A[t] = make_float2(-fa.alpha * s.x, -fa.alpha * s.y);
+  // grid-stride: the default grid is one thread per node; a small grid (blocks > 0 in
+  // launch_attraction) trickles beside the FFT passes instead of flooding the SMs
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n_local;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = lo + t;
+    const float2 s = attraction_sum_hv(xy, xy[i], row_ptr, col, i, fa);
+    A[t] = make_float2(-fa.alpha * s.x, -fa.alpha * s.y);
+  }
 }
 
 void launch_attraction(const float2* xy, int64_t lo, int64_t n_local, const int64_t* row_ptr,
-                       const int32_t* col, ForceArgs fa, float2* A, cudaStream_t s) {
+                       const int32_t* col, ForceArgs fa, float2* A, cudaStream_t s, int blocks) {
   if (n_local <= 0) return;
-  attraction_kernel<<<(unsigned)((n_local + kNodeThreads - 1) / kNodeThreads), kNodeThreads, 0, s>>>(
-      xy, lo, n_local, row_ptr, col, fa, A);
+  const int64_t full = (n_local + kNodeThreads - 1) / kNodeThreads;
+  const unsigned g = (unsigned)(blocks > 0 ? std::min<int64_t>(blocks, full) : full);
+  attraction_kernel<<<g, kNodeThreads, 0, s>>>(xy, lo, n_local, row_ptr, col, fa, A);
 }
 
 void launch_gather_update(const float2* xy, float2* xy_next, int64_t lo, int64_t n_local,

@@ -235,7 +235,8 @@ void launch_gather_update(const float2* xy, float2* xy_next, int64_t lo, int64_t
                           const float2* A_pre = nullptr);
 // attraction of the shard's nodes into A (gather_update's A_pre)
 void launch_attraction(const float2* xy, int64_t lo, int64_t n_local, const int64_t* row_ptr,
-                       const int32_t* col, ForceArgs fa, float2* A, cudaStream_t s);
+                       const int32_t* col, ForceArgs fa, float2* A, cudaStream_t s,
+                       int blocks = 0);
 
 // heavy rows (kernels_heavy.cu): build the chunk index of the current CSR (scratch: 8 (n+1)
 // + sums bytes, heavy_scratch_bytes), then the chunk sums for the rows [lo, hi)

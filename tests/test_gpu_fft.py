@@ -383,7 +383,8 @@ print("tile ok")
 
 @pytest.mark.parametrize("env", ["TFDP_ATTR_SIDE=0", "TFDP_HEAVY=0", "TFDP_PDL=0",
                                  "TFDP_KSPEC_OVERLAP=0", "TFDP_ROWS_RB=1", "TFDP_ROWS_RB=4",
-                                 "TFDP_PDL_MAX_FFT=8192"])
+                                 "TFDP_PDL_MAX_FFT=8192", "TFDP_ATTR_AT=1", "TFDP_ATTR_AT=2",
+                                 "TFDP_ATTR_BLOCKS=296"])
 def test_env_variants_subprocess(env):
     """Every A/B switch of DESIGN §7 keeps parity: Morton-ordered C3 forces at k = 1, 2, 3
     against the oracle after 8 steps, 40 iterations of the dynamic schedule, and the
