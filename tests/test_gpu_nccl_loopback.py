@@ -196,3 +196,42 @@ def test_replans_pmds_set_layout_nccl():
     (buffers re-allocated, peer routes re-exchanged over the communicator); PivotMDS and a
     host set_layout at p = 2 leave every rank with one rank's layout."""
     _run(GROW, TFDP_IPC_LOOPBACK="1")
+
+
+REFINE = r"""
+w, rp, col = case("C2rgg")
+focal = [10, 900]
+# local (fisheye) refinement at p = 2, 3: exact steps bitwise equal to one rank
+prm = P.Params(solver="exact", iterations=40)
+def fl(L):
+    L.step(10); L.local_refine(focal, 4.0, 2.0, 2.0, iterations=4); return L.layout()
+X1 = one(w.n, rp, col, w.xy, prm, fl)
+for p in (2, 3):
+    for X in group(p, w.n, rp, col, w.xy, prm, fl):
+        assert np.array_equal(X, X1), p
+print("local_refine exact ok", flush=True)
+# global refinement (gamma / rho overrides) on the slab-distributed ibFFT path at p = 2
+w, rp, col = case("C3")
+prm = P.Params(solver="ibfft", k=1, iterations=20)
+def fg(L):
+    L.step(4); L.global_refine(gamma=4.0, rho=2.0, iterations=4); R, _ = L.forces()
+    return L.layout(), R
+out = group(2, w.n, rp, col, w.xy, prm, fg)
+assert np.array_equal(out[0][0], out[1][0])
+Xg = out[0][0]
+R = np.concatenate([o[1] for o in out])
+# one rank at the group's final layout, same overrides (the trajectories themselves part by
+# the atomics order, R15)
+R1 = one(w.n, rp, col, Xg, P.Params(solver="ibfft", k=1, gamma=4.0, rho=2.0),
+         lambda L: L.forces()[0])
+e1 = O.rel_l2(R, R1)
+e = O.rel_l2(R, O.repulsion_ibfft(Xg.astype(np.float64), 1, gamma=4.0, rho=2.0))
+print("global_refine", e1, e, flush=True); assert e1 <= 1e-4 and e <= 1e-3
+print("ALL OK")
+"""
+
+
+def test_refinement_nccl():
+    """Local refinement (exact, p = 2, 3: bitwise equal to one rank) and global refinement
+    (ibFFT slab, p = 2: the γ / ρ overrides against the oracle) over the NCCL paths."""
+    _run(REFINE, TFDP_IPC_LOOPBACK="1")
