@@ -1,3 +1,4 @@
+# ncu --set full of the column pass at C4 k = 1, 2, 3 (summary, raw and source pages under gpurun_out/)
 mkdir -p gpurun_out
 for k in 1 2 3; do
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:"^cols_kernel" -s 1 -c 1 -o /tmp/r2c_k$k -f python tools/fft_iter.py $k 8 > /dev/null 2>&1

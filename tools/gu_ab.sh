@@ -1,3 +1,4 @@
+# Round-1 A/B of gather_update variants (libtfdp_<v>.so built with -D switches of that tree; the log is profiles/r1_gu_ab.txt)
 mkdir -p gpurun_out
 for v in base minb8 new; do
   lib=paper_2303_03964_b200/libtfdp_$v.so; [ $v = new ] && lib=paper_2303_03964_b200/libtfdp.so
