@@ -783,14 +783,22 @@ __device__ __forceinline__ void dft<16>(float2 (&v)[16]) {
 // In-place Stockham autosort stage (Govindaraju et al. 2008 formulation): radix R, size N,
 // sub-transform size Ns (1 for the first stage, else a multiple of 16 since N % 256 == 0 and
 // the first stage is radix 16).  Loads + butterflies into registers, barrier, stores, barrier.
-template <int T, int R, int N, int Ns, bool ZERO_UPPER, bool LOW_OUT>
-__device__ __forceinline__ void stage(float2* buf, const float2* __restrict__ tw, int tid) {
+// I/O fusion as in the SoA core: the first stage takes its inputs from src(x) and the last
+// hands its outputs to dst(x, v) (natural order) unless they are SmemIO — no shared-memory
+// round trip (and no barrier) for the kernel's global loads / stores.
+template <int T, int R, int N, int Ns, bool ZERO_UPPER, bool LOW_OUT, class Src, class Dst>
+__device__ __forceinline__ void stage(float2* buf, const float2* __restrict__ tw, int tid,
+                                      const Src& src, const Dst& dst) {
   constexpr int nb = N / R;
   constexpr int MB = (nb + T - 1) / T;  // butterflies per thread
   constexpr int step = nb / Ns;         // N / (Ns R)
   constexpr int sin_ = nb + (nb >> 4);  // padded stride of the loads (nb % 16 == 0)
   constexpr int sout = Ns == 1 ? 1 : Ns + (Ns >> 4);
   constexpr bool p2 = (Ns & (Ns - 1)) == 0;
+  constexpr bool first = Ns == 1;
+  constexpr bool last = Ns * R == N;
+  constexpr bool src_smem = !first || std::is_same<Src, SmemIO>::value;
+  constexpr bool dst_smem = !last || std::is_same<Dst, SmemIO>::value;
   float2 v[MB][R];
 #pragma unroll
   for (int b = 0; b < MB; ++b) {
@@ -800,7 +808,8 @@ __device__ __forceinline__ void stage(float2* buf, const float2* __restrict__ tw
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         if (ZERO_UPPER && 2 * r >= R) v[b][r] = make_float2(0.f, 0.f);
-        else v[b][r] = buf[pj + r * sin_];
+        else if constexpr (src_smem) v[b][r] = buf[pj + r * sin_];
+        else v[b][r] = src(j + r * nb);
       }
       if constexpr (Ns > 1) {
         const int k = p2 ? (j & (Ns - 1)) : (j % Ns);
@@ -813,7 +822,7 @@ __device__ __forceinline__ void stage(float2* buf, const float2* __restrict__ tw
       else dft<R>(v[b]);
     }
   }
-  __syncthreads();
+  if constexpr (src_smem && dst_smem) __syncthreads();
 #pragma unroll
   for (int b = 0; b < MB; ++b) {
     const int j = tid + b * T;
@@ -822,22 +831,27 @@ __device__ __forceinline__ void stage(float2* buf, const float2* __restrict__ tw
       const int d = (j - k) * R + k;
       const int pd = d + (d >> 4);
 #pragma unroll
-      for (int r = 0; r < R; ++r)
-        if (!LOW_OUT || 2 * r < R) buf[pd + r * sout] = v[b][r];
+      for (int r = 0; r < R; ++r) {
+        if (!LOW_OUT || 2 * r < R) {
+          if constexpr (dst_smem) buf[pd + r * sout] = v[b][r];
+          else dst(d + r * Ns, v[b][r]);
+        }
+      }
     }
   }
-  __syncthreads();
+  if constexpr (dst_smem) __syncthreads();
 }
 
 
-template <int T, int N, int FLAGS, int Ns, int REM>
-__device__ __forceinline__ void fft_rec(float2* buf, const float2* __restrict__ tw, int tid) {
+template <int T, int N, int FLAGS, int Ns, int REM, class Src, class Dst>
+__device__ __forceinline__ void fft_rec(float2* buf, const float2* __restrict__ tw, int tid,
+                                        const Src& src, const Dst& dst) {
   if constexpr (REM > 1) {
     constexpr int R = next_radix(REM);
     constexpr bool first = Ns == 1, last = REM == R;
     stage<T, R, N, Ns, first && (FLAGS & kZeroUpper) != 0,
-          last && (FLAGS & kLowOut) != 0 && R % 2 == 0>(buf, tw, tid);
-    fft_rec<T, N, FLAGS, Ns * R, REM / R>(buf, tw, tid);
+          last && (FLAGS & kLowOut) != 0 && R % 2 == 0>(buf, tw, tid, src, dst);
+    fft_rec<T, N, FLAGS, Ns * R, REM / R>(buf, tw, tid, src, dst);
   }
 }
 
@@ -845,11 +859,12 @@ __device__ __forceinline__ void fft_rec(float2* buf, const float2* __restrict__ 
 // Radix 16 first (so Ns is a multiple of 16 afterwards), then 16/8/4/2, then 3, 5.  Called
 // by the whole block after a barrier (threads tid = 0..T-1 of each group of T own one FFT;
 // the barriers are block-wide, so every group runs the same plan); ends with a barrier.
-template <int T, int N, int FLAGS>
+template <int T, int N, int FLAGS, class Src = SmemIO, class Dst = SmemIO>
 __device__ __forceinline__ void fft_smem(float2* buf, const float2* __restrict__ tw,
-                                         int tid = threadIdx.x) {
+                                         int tid = threadIdx.x, const Src& src = Src{},
+                                         const Dst& dst = Dst{}) {
   static_assert(N % 256 == 0 && T * 16 >= N, "FFT plan");
-  fft_rec<T, N, FLAGS, 1, N>(buf, tw, tid);
+  fft_rec<T, N, FLAGS, 1, N>(buf, tw, tid, src, dst);
 }
 
 // ---------------------------------------------------------------- forward rows
@@ -880,6 +895,15 @@ constexpr int rows_min_blocks() {
   return kMinBlocksA<fft_threads_c(P)> / RB > 0 ? kMinBlocksA<fft_threads_c(P)> / RB : 1;
 }
 
+// First-stage global loads (rows_fwd) and last-stage global stores (rows_inv) fused into
+// the FFT: C4 rows_fwd k = 1 23.0 -> 18.9 us, k = 3 156.7 -> 140.5; rows_inv k = 3 146.0 ->
+// 142.3 (k = 1 unchanged).  Not at P = 4096, whose 40-register cap (3 blocks per SM) it
+// overflows: rows_fwd 65.7 -> 67.9, rows_inv 70.0 -> 73.8 us.
+template <int P>
+__host__ __device__ constexpr bool rows_fuse_io() {
+  return P != 4096;
+}
+
 template <int P, int RB>
 __global__ void __launch_bounds__(fft_threads_c(P) * RB, (rows_min_blocks<P, RB>()))
 rows_fwd_kernel(const GridGeom* __restrict__ geom, const float4* __restrict__ C, int cpitch,
@@ -908,17 +932,23 @@ rows_fwd_kernel(const GridGeom* __restrict__ geom, const float4* __restrict__ C,
   const float* rowa = reinterpret_cast<const float*>(C + (int64_t)ra * cpitch) + ch;
   const float* rowb = rowa + 4 * (int64_t)cpitch;
   constexpr int half = P / 2;
-#pragma unroll
-  for (int x = lt; x < half; x += T) {  // [P/2, P) is zero and never read
+  auto src = [&](int x) {  // [P/2, P) is zero and never read
     float va = 0.f, vb = 0.f;
     if (x < M) {
       if (ha) va = rowa[4 * x];
       if (hb) vb = rowb[4 * x];
     }
-    a[pad(x)] = make_float2(va, vb);
+    return make_float2(va, vb);
+  };
+  if constexpr (rows_fuse_io<P>()) {
+    // the first stage reads the two rows straight from global memory
+    fft_smem<T, P, kZeroUpper>(a, tws, lt, src);
+  } else {
+#pragma unroll
+    for (int x = lt; x < half; x += T) a[pad(x)] = src(x);
+    __syncthreads();
+    fft_smem<T, P, kZeroUpper>(a, tws, lt);
   }
-  __syncthreads();
-  fft_smem<T, P, kZeroUpper>(a, tws, lt);
   const int rows_here = min(2 * RB, M - 2 * p0);
   constexpr int H = half + 1;
   for (int f = threadIdx.x; f < (half + 1) * RB; f += NT) {
@@ -997,26 +1027,46 @@ rows_inv_kernel(const GridGeom* __restrict__ geom, const float2* __restrict__ CA
   __syncthreads();
   const int g = threadIdx.x / T, lt = threadIdx.x - g * T;
   float2* a = sm + g * PL;
-  fft_smem<T, P, kLowOut>(a, tws, lt);
   const int ra = 2 * (p0 + g), rb = ra + 1;
-  if (ra >= M) return;
-  const bool hb = rb < M;
-  float* pa = Phi + ((int64_t)ch * cpitch + ra) * cpitch;
+  const bool ha = ra < M, hb = rb < M;
+  float* pa = Phi + ((int64_t)ch * cpitch + (ha ? ra : 0)) * cpitch;
   float* pb = pa + cpitch;
-  for (int x = lt; x < M; x += T) {
-    const float2 z = a[pad(x)];  // conj(result) = xa + i xb
-    pa[x] = z.x;
-    if (hb) pb[x] = -z.y;
-  }
-  if (rt) {  // slab mode, fused potential exchange: the same rows into every other rank
-    const int64_t off = pa - Phi;
-    for (int j = 0; j < rt->world; ++j) {
-      if (j == rt->rank) continue;
-      float* qa = rt->phi[j] + off;
-      for (int x = lt; x < M; x += T) {
-        const float2 z = a[pad(x)];
-        qa[x] = z.x;
-        if (hb) qa[cpitch + x] = -z.y;
+  auto dst = [&](int x, float2 z) {  // conj(result) = xa + i xb
+    if (ha && x < M) {
+      pa[x] = z.x;
+      if (hb) pb[x] = -z.y;
+      if (rt) {  // slab mode, fused potential exchange: the same rows into every other rank
+        const int64_t off = pa - Phi;
+        for (int j = 0; j < rt->world; ++j) {
+          if (j == rt->rank) continue;
+          float* qa = rt->phi[j] + off;
+          qa[x] = z.x;
+          if (hb) qa[cpitch + x] = -z.y;
+        }
+      }
+    }
+  };
+  if constexpr (rows_fuse_io<P>()) {
+    // the last stage writes the potential rows straight to global memory (x < M <= P/2)
+    fft_smem<T, P, kLowOut>(a, tws, lt, SmemIO{}, dst);
+  } else {
+    fft_smem<T, P, kLowOut>(a, tws, lt);
+    if (!ha) return;
+    for (int x = lt; x < M; x += T) {
+      const float2 z = a[pad(x)];
+      pa[x] = z.x;
+      if (hb) pb[x] = -z.y;
+    }
+    if (rt) {
+      const int64_t off = pa - Phi;
+      for (int j = 0; j < rt->world; ++j) {
+        if (j == rt->rank) continue;
+        float* qa = rt->phi[j] + off;
+        for (int x = lt; x < M; x += T) {
+          const float2 z = a[pad(x)];
+          qa[x] = z.x;
+          if (hb) qa[cpitch + x] = -z.y;
+        }
       }
     }
   }
