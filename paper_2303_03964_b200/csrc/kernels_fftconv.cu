@@ -898,7 +898,9 @@ constexpr int rows_min_blocks() {
 // First-stage global loads (rows_fwd) and last-stage global stores (rows_inv) fused into
 // the FFT: C4 rows_fwd k = 1 23.0 -> 18.9 us, k = 3 156.7 -> 140.5; rows_inv k = 3 146.0 ->
 // 142.3 (k = 1 unchanged).  Not at P = 4096, whose 40-register cap (3 blocks per SM) it
-// overflows: rows_fwd 65.7 -> 67.9, rows_inv 70.0 -> 73.8 us.
+// overflows: rows_fwd 65.7 -> 67.9, rows_inv 70.0 -> 73.8 us.  rows_inv's transposed
+// half-spectrum loads fused into its first stage too (each entry read twice, for q and its
+// mirror P - q) measured slower: k = 1 20.9 -> 25.0 us, k = 3 142.4 -> 154.5.
 template <int P>
 __host__ __device__ constexpr bool rows_fuse_io() {
   return P != 4096;
