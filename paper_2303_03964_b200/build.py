@@ -90,7 +90,10 @@ def build(verbose: bool = False, force: bool = False, defines=(), out: str = Non
     os.replace(out + ".tmp", out)
     if out == LIB:
         build_examples(verbose)
-        build_nccl_loopback(verbose)
+        try:  # test infrastructure: never fails the product build
+            build_nccl_loopback(verbose)
+        except Exception as e:  # noqa: BLE001
+            sys.stderr.write(f"[build] tests/nccl_loopback not built: {e}\n")
     return out
 
 
